@@ -1,0 +1,150 @@
+/*
+ * fcpb.h -- C ABI of the B200-native FCP block-attention data plane (libfcpb.so).
+ *
+ * The reference (arxiv 2605.08524, package `blocksched`) has no FFI: its data
+ * plane is the analytic stand-in
+ *     simulate(assignment, plan, units, deps, hw, cfg, curve, opts) -> SimReport
+ * (reference pkg/src/blocksched/simulator.py:154-232), and attention math exists
+ * only in the paper.  These entry points are what a binding of
+ * that data plane needs: they *execute* the (Q chunk, KV chunk) tiles of
+ * DependencyMap.q_to_kv (reference sharding.py:172-201) that simulate() only
+ * times (simulator.py:73-109), merge the per-stage partial outputs, and reduce
+ * the dK/dV partials that return along the reversed edges of the plan
+ * (planner.py:81-102, reversed).
+ *
+ * Conventions
+ *  - All tensors are dense, token-major: Q/O/dO [T, Hq, D], K/V [T, Hkv, D],
+ *    bf16 unless noted; LSE is fp32 [T, Hq], natural log; softmax scale given.
+ *  - q-head h uses kv-head h / (Hq/Hkv)  (GQA; the reference leaves this open).
+ *  - Every pointer is a device pointer owned by the caller; the library
+ *    allocates nothing and never synchronises; `stream` is a cudaStream_t.
+ *  - Returns 0 (FCPB_OK) or a negative fcpb_status; fcpb_last_error() gives the
+ *    message (thread-local).  Python maps these onto ParameterError / NativeError.
+ *  - sm_100a only (B200).  D = 128, Hq/Hkv even for the tcgen05 kernels.
+ */
+#ifndef FCPB_H_
+#define FCPB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../paper_2605_08524_b200/csrc/fcpb_types.h"
+
+#if defined(__GNUC__)
+#define FCPB_API __attribute__((visibility("default")))
+#else
+#define FCPB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fcpb_status {
+  FCPB_OK = 0,
+  FCPB_ERR_INVALID = -1,   /* bad shape / argument (ParameterError)            */
+  FCPB_ERR_CUDA = -2,      /* CUDA runtime / driver failure (NativeError)      */
+  FCPB_ERR_UNSUPPORTED = -3 /* device is not sm_100 or shape not compiled     */
+};
+
+/* Forward (K1).  Replaces the per-tile compute that simulate() accounts for in
+ * _tile_seconds_by_release (simulator.py:73-109). */
+typedef struct {
+  int32_t num_q_heads, num_kv_heads, head_dim;
+  float softmax_scale;
+  const void* q;           int64_t q_tokens;          /* [Tq, Hq, D] bf16            */
+  const void* k;           const void* v;             /* local KV [Tkv, Hkv, D] bf16 */
+  int64_t kv_tokens;
+  const void* k_recv;      const void* v_recv;        /* receive arena (may be NULL) */
+  int64_t kv_recv_tokens;
+  void* o;                 float* lse;                /* final outputs                */
+  float* o_partial;        float* lse_partial;        /* [P, Hq, D] / [P, Hq] or NULL */
+  int64_t partial_rows;
+  const FcpbSegment* segments; int32_t num_segments;  /* device tables (worklist.py) */
+  const FcpbKvRef* kv_refs;    int32_t num_kv_refs;
+  const FcpbItem* items;       int32_t num_items;     /* LPT-ordered                  */
+  int32_t num_ctas;            /* 0 = one per SM                                      */
+} FcpbFwdArgs;
+
+FCPB_API int fcpb_attn_fwd(const FcpbFwdArgs* args, void* stream);
+
+/* K3: LSE merge of per-stage partial outputs.  Group g covers Q tokens
+ * [q_off, q_off+q_len) whose partial rows start at part_rows[part_begin..part_end). */
+typedef struct {
+  int32_t q_off, q_len, part_begin, part_end;
+  int32_t tok_begin;           /* prefix sum of q_len over preceding groups */
+  int32_t pad_;
+} FcpbMergeGroup;
+
+typedef struct {
+  int32_t num_q_heads, head_dim;
+  const float* o_partial; const float* lse_partial;
+  const FcpbMergeGroup* groups; int32_t num_groups;
+  const int32_t* part_rows;
+  int64_t merged_tokens;       /* sum of q_len over groups */
+  void* o; float* lse;         /* bf16 [Tq,Hq,D], fp32 [Tq,Hq] */
+} FcpbMergeArgs;
+
+FCPB_API int fcpb_lse_merge(const FcpbMergeArgs* args, void* stream);
+
+/* K2 preprocess: delta[t,h] = sum_d dO[t,h,d] * O[t,h,d] (fp32), and zero the
+ * fp32 dQ accumulator. */
+FCPB_API int fcpb_bwd_preprocess(const void* o, const void* dout, float* delta, float* dq_accum,
+                        int64_t tokens, int32_t num_q_heads, int32_t head_dim, void* stream);
+
+/* K2: backward.  Work is organised by KV tile: for each KV chunk reference (local
+ * or received) the list of local Q chunks that attend to it.  dK/dV accumulate in
+ * fp32 per KV arena row; dQ accumulates in fp32 (dq_accum) and is converted by
+ * fcpb_dq_convert. */
+typedef struct {
+  int32_t kv_off, kv_len;       /* arena rows of the KV chunk                       */
+  int32_t flags;                /* FCPB_KV_RECV: lives in the receive arena         */
+  int32_t q_begin, q_end;       /* [q_begin,q_end) into FcpbBwdQRef                  */
+  int32_t pad_;
+} FcpbBwdKvSeg;
+
+typedef struct {
+  int32_t q_off, q_len;
+  int32_t diag;                 /* causal diagonal tile (Q chunk == KV chunk)       */
+  int32_t pad_;
+} FcpbBwdQRef;
+
+typedef struct {
+  int32_t kvseg;                /* FcpbBwdKvSeg index                                */
+  int32_t nblock;               /* 128-row KV block inside the chunk                */
+} FcpbBwdItem;
+
+typedef struct {
+  int32_t num_q_heads, num_kv_heads, head_dim;
+  float softmax_scale;
+  const void* q; const void* dout; const float* lse; const float* delta;
+  int64_t q_tokens;
+  const void* k; const void* v; int64_t kv_tokens;
+  const void* k_recv; const void* v_recv; int64_t kv_recv_tokens;
+  float* dq_accum;              /* [Tq, Hq, D] fp32 (atomically accumulated)        */
+  float* dk_accum; float* dv_accum;             /* local  [Tkv, Hkv, D] fp32         */
+  float* dk_recv_accum; float* dv_recv_accum;   /* recv   [Trecv, Hkv, D] fp32       */
+  const FcpbBwdKvSeg* kvsegs; int32_t num_kvsegs;
+  const FcpbBwdQRef* qrefs; int32_t num_qrefs;
+  const FcpbBwdItem* items; int32_t num_items;
+  int32_t num_ctas;
+} FcpbBwdArgs;
+
+FCPB_API int fcpb_attn_bwd(const FcpbBwdArgs* args, void* stream);
+
+/* fp32 -> bf16 conversion of an accumulator (dQ, dK, dV). */
+FCPB_API int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* K4: dK/dV reduce at the owner: dst[rows[i]] += src[i] for `n_rows` rows of
+ * `row_elems` fp32 each (partials returned along reversed plan edges). */
+FCPB_API int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64_t n_rows,
+                    int64_t row_elems, void* stream);
+
+FCPB_API const char* fcpb_last_error(void);
+FCPB_API int fcpb_version(void);
+FCPB_API int fcpb_device_supported(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCPB_H_ */

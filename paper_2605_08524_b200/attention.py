@@ -1,0 +1,239 @@
+"""Block-attention forward/backward entry points of one rank (K1-K4 launches).
+
+``BlockAttention`` holds one rank's device work lists (built once per batch
+from the ``ScheduleResult`` by ``worklist.build_rank_work``) and launches the
+sm_100a kernels through the C ABI.  It is reused by every attention layer of
+the batch.  The multi-GPU executor (``executor.py``) drives it wave by wave,
+interleaved with the KV exchange; on one GPU ``forward``/``backward`` run the
+whole rank at once.
+
+Numerics: bf16 inputs, fp32 accumulation in TMEM, fp32 LSE (natural log),
+fp32 dQ/dK/dV accumulators rounded to bf16 at the end.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import native
+from .costmodel import ModelConfig
+from .errors import ParameterError
+from .worklist import FwdWave, RankWork
+
+
+def _dev_i32(arr, device):
+    return torch.from_numpy(arr.copy()).to(device=device, dtype=torch.int32).contiguous()
+
+
+def _check(t, name, shape, dtype=torch.bfloat16):
+    if t is None:
+        raise ParameterError(f"{name} is required")
+    if not t.is_cuda:
+        raise ParameterError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ParameterError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ParameterError(f"{name} shape {tuple(t.shape)} != expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise ParameterError(f"{name} must be contiguous")
+
+
+class BlockAttention:
+    def __init__(self, work: RankWork, cfg: ModelConfig, device=None,
+                 softmax_scale: float | None = None, num_ctas: int = 0):
+        if cfg.head_dim != 128:
+            raise ParameterError("the sm_100a kernels are compiled for head_dim 128")
+        self.lib = native.load()
+        self.work = work
+        self.cfg = cfg
+        self.device = torch.device(device or "cuda")
+        self.scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(cfg.head_dim)
+        self.num_ctas = num_ctas
+        lay = work.layout
+        self.tokens = lay.tokens
+        self.recv_tokens = lay.recv_tokens
+        dev = self.device
+        self._waves = [(w, _dev_i32(w.segments, dev), _dev_i32(w.kvrefs, dev), _dev_i32(w.items, dev))
+                       for w in work.fwd.waves]
+        f = work.fwd
+        self._merge = None
+        if len(f.merge_groups):
+            self._merge = (_dev_i32(f.merge_groups, dev), _dev_i32(f.merge_part_rows, dev))
+        self._bwd = [(b, _dev_i32(b.kvsegs, dev), _dev_i32(b.qrefs, dev), _dev_i32(b.items, dev))
+                     for b in work.bwd]
+        self.launches = 0   # kernel launches issued by this object (bench accounting)
+
+    # ------------------------------------------------------------------ shapes
+    def q_shape(self):
+        return (self.tokens, self.cfg.q_heads, self.cfg.head_dim)
+
+    def kv_shape(self, recv=False):
+        return (self.recv_tokens if recv else self.tokens, self.cfg.kv_heads, self.cfg.head_dim)
+
+    def _stream(self, stream):
+        return native.stream_handle(stream if stream is not None else torch.cuda.current_stream())
+
+    # ------------------------------------------------------------------ forward
+    def alloc_forward_outputs(self):
+        H, D = self.cfg.q_heads, self.cfg.head_dim
+        o = torch.empty(self.q_shape(), dtype=torch.bfloat16, device=self.device)
+        lse = torch.empty((self.tokens, H), dtype=torch.float32, device=self.device)
+        rows = self.work.fwd.partial_rows
+        op = lp = None
+        if rows:
+            op = torch.empty((rows, H, D), dtype=torch.float32, device=self.device)
+            lp = torch.empty((rows, H), dtype=torch.float32, device=self.device)
+        return o, lse, op, lp
+
+    def forward_wave(self, idx, q, k, v, k_recv, v_recv, outs, stream=None):
+        wave, segs, refs, items = self._waves[idx]
+        o, lse, op, lp = outs
+        a = native.FwdArgs()
+        a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
+        a.softmax_scale = self.scale
+        a.q, a.q_tokens = native.ptr(q), self.tokens
+        a.k, a.v, a.kv_tokens = native.ptr(k), native.ptr(v), self.tokens
+        a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
+        a.o, a.lse = native.ptr(o), native.ptr(lse)
+        a.o_partial, a.lse_partial = native.ptr(op), native.ptr(lp)
+        a.partial_rows = self.work.fwd.partial_rows
+        a.segments, a.num_segments = native.ptr(segs), len(wave.segments)
+        a.kv_refs, a.num_kv_refs = native.ptr(refs), len(wave.kvrefs)
+        a.items, a.num_items = native.ptr(items), len(wave.items)
+        a.num_ctas = self.num_ctas
+        native.check(self.lib.fcpb_attn_fwd(ctypes_ref(a), self._stream(stream)))
+        self.launches += 1
+
+    def merge(self, outs, stream=None):
+        if self._merge is None:
+            return
+        o, lse, op, lp = outs
+        groups, rows = self._merge
+        a = native.MergeArgs()
+        a.num_q_heads, a.head_dim = self.cfg.q_heads, self.cfg.head_dim
+        a.o_partial, a.lse_partial = native.ptr(op), native.ptr(lp)
+        a.groups, a.num_groups = native.ptr(groups), len(self.work.fwd.merge_groups)
+        a.part_rows, a.merged_tokens = native.ptr(rows), self.work.fwd.merged_tokens
+        a.o, a.lse = native.ptr(o), native.ptr(lse)
+        native.check(self.lib.fcpb_lse_merge(ctypes_ref(a), self._stream(stream)))
+        self.launches += 1
+
+    @property
+    def num_waves(self) -> int:
+        return len(self._waves)
+
+    def wave_stage(self, idx) -> int:
+        return self._waves[idx][0].stage
+
+    def forward(self, q, k, v, k_recv=None, v_recv=None, stream=None):
+        """All waves then the merge; returns (o bf16 [T,Hq,D], lse fp32 [T,Hq])."""
+        self.validate(q, k, v, k_recv, v_recv)
+        outs = self.alloc_forward_outputs()
+        for i in range(self.num_waves):
+            self.forward_wave(i, q, k, v, k_recv, v_recv, outs, stream)
+        self.merge(outs, stream)
+        return outs[0], outs[1]
+
+    def validate(self, q, k, v, k_recv=None, v_recv=None):
+        _check(q, "q", self.q_shape())
+        _check(k, "k", self.kv_shape())
+        _check(v, "v", self.kv_shape())
+        if self.recv_tokens:
+            _check(k_recv, "k_recv", self.kv_shape(True))
+            _check(v_recv, "v_recv", self.kv_shape(True))
+
+    # ------------------------------------------------------------------ backward
+    def backward_prepare(self, o, do, stream=None):
+        """delta = rowsum(dO*O) and a zeroed fp32 dQ accumulator."""
+        H = self.cfg.q_heads
+        delta = torch.empty((self.tokens, H), dtype=torch.float32, device=self.device)
+        dq = torch.empty(self.q_shape(), dtype=torch.float32, device=self.device)
+        native.check(self.lib.fcpb_bwd_preprocess(native.ptr(o), native.ptr(do), native.ptr(delta),
+                                                  native.ptr(dq), self.tokens, H, self.cfg.head_dim,
+                                                  self._stream(stream)))
+        self.launches += 1
+        return delta, dq
+
+    def alloc_dkv(self, recv: bool):
+        shape = self.kv_shape(recv)
+        if shape[0] == 0:
+            return None, None
+        return (torch.empty(shape, dtype=torch.float32, device=self.device),
+                torch.empty(shape, dtype=torch.float32, device=self.device))
+
+    def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, lse, delta, do, dq,
+                        dk, dv, dk_r, dv_r, stream=None):
+        for b, kvsegs, qrefs, items in self._bwd:
+            if b.recv != recv:
+                continue
+            a = native.BwdArgs()
+            a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
+            a.softmax_scale = self.scale
+            a.q, a.dout, a.lse, a.delta = native.ptr(q), native.ptr(do), native.ptr(lse), native.ptr(delta)
+            a.q_tokens = self.tokens
+            a.k, a.v, a.kv_tokens = native.ptr(k), native.ptr(v), self.tokens
+            a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
+            a.dq_accum, a.dk_accum, a.dv_accum = native.ptr(dq), native.ptr(dk), native.ptr(dv)
+            a.dk_recv_accum, a.dv_recv_accum = native.ptr(dk_r), native.ptr(dv_r)
+            a.kvsegs, a.num_kvsegs = native.ptr(kvsegs), len(b.kvsegs)
+            a.qrefs, a.num_qrefs = native.ptr(qrefs), len(b.qrefs)
+            a.items, a.num_items = native.ptr(items), len(b.items)
+            a.num_ctas = self.num_ctas
+            native.check(self.lib.fcpb_attn_bwd(ctypes_ref(a), self._stream(stream)))
+            self.launches += 1
+
+    def to_bf16(self, src, stream=None):
+        dst = torch.empty(src.shape, dtype=torch.bfloat16, device=self.device)
+        native.check(self.lib.fcpb_f32_to_bf16(native.ptr(src), native.ptr(dst), src.numel(),
+                                               self._stream(stream)))
+        self.launches += 1
+        return dst
+
+    def reduce_dkv(self, dst, src, dst_rows, stream=None):
+        """K4: dst[dst_rows[i]] += src[i] over token rows of Hkv*D floats."""
+        row = self.cfg.kv_heads * self.cfg.head_dim
+        native.check(self.lib.fcpb_dkv_reduce(native.ptr(dst), native.ptr(src), native.ptr(dst_rows),
+                                              src.shape[0], row, self._stream(stream)))
+        self.launches += 1
+
+    def backward(self, q, k, v, o, lse, do, k_recv=None, v_recv=None, stream=None):
+        """Single-rank backward.  Returns (dq, dk, dv) bf16 and, if the rank
+        received KV, the fp32 (dk_recv, dv_recv) partials owed to their owners."""
+        self.validate(q, k, v, k_recv, v_recv)
+        _check(do, "do", self.q_shape())
+        delta, dq = self.backward_prepare(o, do, stream)
+        dk, dv = self.alloc_dkv(False)
+        dk_r, dv_r = self.alloc_dkv(True)
+        self.backward_launch(True, q, k, v, k_recv, v_recv, lse, delta, do, dq, dk, dv, dk_r, dv_r, stream)
+        self.backward_launch(False, q, k, v, k_recv, v_recv, lse, delta, do, dq, dk, dv, dk_r, dv_r, stream)
+        return (self.to_bf16(dq, stream), self.to_bf16(dk, stream), self.to_bf16(dv, stream),
+                dk_r, dv_r)
+
+
+def ctypes_ref(s):
+    import ctypes
+    return ctypes.byref(s)
+
+
+class _FcpAttentionFn(torch.autograd.Function):
+    """Autograd wrapper for a single rank without exchange (N=1)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, op: BlockAttention):
+        o, lse = op.forward(q, k, v)
+        ctx.save_for_backward(q, k, v, o, lse)
+        ctx.op = op
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv, _, _ = ctx.op.backward(q, k, v, o, lse, do.contiguous())
+        return dq, dk, dv, None
+
+
+def fcp_attention(q, k, v, op: BlockAttention):
+    """Differentiable block attention of one rank (no KV exchange)."""
+    return _FcpAttentionFn.apply(q, k, v, op)

@@ -1,0 +1,388 @@
+// K1: varlen block-pair attention forward on sm_100a (tcgen05 + TMEM + TMA).
+//
+// One persistent CTA per SM.  A work item is 128 query rows of one FCP segment
+// (a Q chunk plus the ordered KV chunks it attends to in this launch) for a
+// *pair* of query heads that share one KV head (GQA), so every K/V tile that
+// TMA stages in shared memory feeds two Q tiles.
+//
+// Warp roles (12 warps):
+//   w0      TMA producer: Q pair once per item, then K(j), V(j) into a 4-slot ring
+//   w1      MMA issuer (one elected lane): S_h = Q_h K^T (SS), O_h += P_h V (TS)
+//   w2      TMEM allocator (512 columns)
+//   w3      idle
+//   w4-7    softmax/epilogue for head 0 of the pair (thread == query row)
+//   w8-11   softmax/epilogue for head 1 of the pair
+// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_h (bf16,
+// 64 columns) overwrites the first half of S_h once S_h has been read.
+// MMA order per KV tile j:  PV0(j), S0(j+1), PV1(j), S1(j+1): the tensor pipe
+// runs one head's matmuls while the other head's warps do the softmax.
+#pragma once
+#include "fcpb_types.h"
+#include "sm100_ptx.cuh"
+
+namespace fcpb {
+namespace fwd {
+
+constexpr int kD = 128;          // head dim
+constexpr int kBM = 128;         // query rows per tile
+constexpr int kBN = 128;         // kv rows per tile
+constexpr int kSlots = 4;        // K/V ring slots (each one K or one V tile)
+constexpr int kTileBytes = kBN * kD * 2;        // 32 KB
+constexpr int kHalfBytes = kTileBytes / 2;      // one 64-column swizzle panel
+constexpr int kThreads = 384;
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO0 = 256, kColO1 = 384;
+
+struct Smem {
+  uint8_t q[2][kTileBytes];           // 64 KB, 1024-aligned panels
+  uint8_t kv[kSlots][kTileBytes];     // 128 KB
+  uint64_t q_full, q_empty;
+  uint64_t kv_full[kSlots], kv_empty[kSlots];
+  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint32_t tmem_base;
+};
+
+struct Params {
+  const FcpbSegment* segs;
+  const FcpbKvRef* kvrefs;
+  const FcpbItem* items;
+  int32_t num_items;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  float scale_log2;      // softmax_scale * log2(e)
+  float scale;           // softmax_scale
+  __nv_bfloat16* o;      // [Tq, Hq, D]
+  float* lse;            // [Tq, Hq]
+  float* o_part;         // [P, Hq, D]
+  float* lse_part;       // [P, Hq]
+};
+
+// Number of 128-row KV tiles a Q tile at m-block `mb` visits in `ref`.
+FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
+  int n = (ref.len + kBN - 1) / kBN;
+  if (ref.flags & FCPB_KV_DIAG) n = min(n, mb + 1);
+  return n;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_v,
+                const __grid_constant__ CUtensorMap tm_k_recv,
+                const __grid_constant__ CUtensorMap tm_v_recv,
+                const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t warp = warp_id();
+  const int head_pairs = p.num_q_heads / 2;
+  const int group = p.num_q_heads / p.num_kv_heads;
+  const int total = p.num_items * head_pairs;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_k_recv);
+    tma_prefetch_desc(&tm_v_recv);
+  }
+  if (warp == 1 && elect_one()) {
+    mbar_init(&sm.q_full, 1);
+    mbar_init(&sm.q_empty, 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&sm.s_full[h], 1);
+      mbar_init(&sm.p_full[h], 128);
+      mbar_init(&sm.o_full[h], 1);
+      mbar_init(&sm.o_empty[h], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t keep = policy_evict_last();
+      uint32_t q_phase = 0, slot = 0, slot_phase = 0;
+      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+        const FcpbItem it = p.items[g / head_pairs];
+        const int hp = g % head_pairs;
+        const FcpbSegment seg = p.segs[it.seg];
+        const int h0 = 2 * hp;
+        const int kvh = h0 / group;
+        const int row0 = seg.q_off + it.mblock * kBM;
+        mbar_wait(&sm.q_empty, q_phase ^ 1);
+        q_phase ^= 1;
+        mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+        for (int h = 0; h < 2; ++h)
+          for (int half = 0; half < 2; ++half)
+            tma_load_3d(&sm.q[h][half * kHalfBytes], &tm_q, &sm.q_full, half * 64, h0 + h, row0);
+        for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
+          const FcpbKvRef ref = p.kvrefs[r];
+          const bool recv = ref.flags & FCPB_KV_RECV;
+          const CUtensorMap* mk = recv ? &tm_k_recv : &tm_k;
+          const CUtensorMap* mv = recv ? &tm_v_recv : &tm_v;
+          const int nt = kv_tiles(ref, it.mblock);
+          for (int t = 0; t < nt; ++t) {
+            const int krow = ref.off + t * kBN;
+            for (int kv = 0; kv < 2; ++kv) {
+              mbar_wait(&sm.kv_empty[slot], slot_phase ^ 1);
+              mbar_arrive_expect_tx(&sm.kv_full[slot], kTileBytes);
+              const CUtensorMap* m = kv ? mv : mk;
+              for (int half = 0; half < 2; ++half)
+                tma_load_3d_hint(&sm.kv[slot][half * kHalfBytes], m, &sm.kv_full[slot], half * 64,
+                                 kvh, krow, keep);
+              if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t id_s = idesc_bf16_f32(kBM, kBN, false, false);
+    const uint32_t id_o = idesc_bf16_f32(kBM, kD, false, true);
+    const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
+    const uint32_t col_s[2] = {kColS0, kColS1};
+    const uint32_t col_o[2] = {kColO0, kColO1};
+    uint32_t q_phase = 0, slot = 0, slot_phase = 0, p_phase = 0, oe_phase = 0;
+    const bool leader = elect_one();
+    auto issue_s = [&](int h, uint32_t kslot) {
+      if (leader) {
+        const uint32_t kb = smem_u32(sm.kv[kslot]);
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+          mma_ss(tmem + col_s[h], smem_desc_sw128(q_addr[h] + off, 16, 1024),
+                 smem_desc_sw128(kb + off, 16, 1024), id_s, kk > 0);
+        }
+        mma_commit(&sm.s_full[h]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int h, uint32_t vslot, bool acc) {
+      if (leader) {
+        const uint32_t vb = smem_u32(sm.kv[vslot]);
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          mma_ts(tmem + col_o[h], tmem + col_s[h] + kk * 8,
+                 smem_desc_sw128(vb + kk * 2048, kHalfBytes, 1024), id_o, (acc || kk > 0));
+        }
+      }
+      __syncwarp();
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (leader) mma_commit(bar);
+      __syncwarp();
+    };
+    // Take the next ring position and wait until TMA has filled it.
+    auto take_full = [&]() {
+      const uint32_t cur = slot;
+      mbar_wait(&sm.kv_full[cur], slot_phase);
+      if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+      return cur;
+    };
+
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const FcpbItem it = p.items[g / head_pairs];
+      const FcpbSegment seg = p.segs[it.seg];
+      int n = 0;
+      for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
+      mbar_wait(&sm.q_full, q_phase);
+      q_phase ^= 1;
+      // O accumulators of the previous item must have been drained by the epilogue.
+      mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
+      mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
+      oe_phase ^= 1;
+      tc_fence_after();
+      // K(0)
+      const uint32_t ks = take_full();
+      tc_fence_after();
+      issue_s(0, ks);
+      issue_s(1, ks);
+      commit(&sm.kv_empty[ks]);
+      if (n == 1) commit(&sm.q_empty);
+      for (int j = 0; j < n; ++j) {
+        const uint32_t vs = take_full();
+        mbar_wait(&sm.p_full[0], p_phase);
+        tc_fence_after();
+        issue_pv(0, vs, j > 0);
+        if (j == n - 1) commit(&sm.o_full[0]);
+        uint32_t ks2 = 0;
+        if (j + 1 < n) {
+          ks2 = take_full();
+          tc_fence_after();
+          issue_s(0, ks2);
+        }
+        mbar_wait(&sm.p_full[1], p_phase);
+        tc_fence_after();
+        issue_pv(1, vs, j > 0);
+        commit(&sm.kv_empty[vs]);
+        if (j == n - 1) commit(&sm.o_full[1]);
+        if (j + 1 < n) {
+          issue_s(1, ks2);
+          commit(&sm.kv_empty[ks2]);
+          if (j + 2 == n) commit(&sm.q_empty);
+        }
+        p_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int h = (warp - 4) >> 2;           // which head of the pair
+    const int row = (warp & 3) * 32 + lane_id();
+    const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_bits + (h ? kColS1 : kColS0);
+    const uint32_t t_o = tmem + lane_bits + (h ? kColO1 : kColO0);
+    uint32_t s_phase = 0, o_phase = 0;
+    const float sl2 = p.scale_log2;
+
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const FcpbItem it = p.items[g / head_pairs];
+      const int head = 2 * (g % head_pairs) + h;
+      const FcpbSegment seg = p.segs[it.seg];
+      float m_run = -INFINITY, l_run = 0.f;
+      bool first = true;
+      for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
+        const FcpbKvRef ref = p.kvrefs[r];
+        const int nt = kv_tiles(ref, it.mblock);
+        const bool diag = ref.flags & FCPB_KV_DIAG;
+        for (int t = 0; t < nt; ++t) {
+          mbar_wait(&sm.s_full[h], s_phase);
+          s_phase ^= 1;
+          tc_fence_after();
+          float s[kBN];
+#pragma unroll
+          for (int c = 0; c < kBN / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(t_s + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(v[i]);
+          }
+          // masking: ragged KV tail, causal diagonal (col <= row within the block)
+          const int valid = ref.len - t * kBN;
+          if (diag && t == it.mblock) {
+#pragma unroll
+            for (int i = 0; i < kBN; ++i)
+              if (i > row) s[i] = -INFINITY;
+          } else if (valid < kBN) {
+#pragma unroll
+            for (int i = 0; i < kBN; ++i)
+              if (i >= valid) s[i] = -INFINITY;
+          }
+          float mp[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) mp[i] = m_run;
+#pragma unroll
+          for (int i = 0; i < kBN; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
+          const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
+                                 fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
+          const float m_use = (mx == -INFINITY) ? 0.f : mx;
+          const float neg = -m_use * sl2;
+          float sp[4] = {0.f, 0.f, 0.f, 0.f};
+          // P (bf16 pairs) overwrites the first 64 columns of S, 16 columns per 32 scores.
+#pragma unroll
+          for (int c = 0; c < kBN / 32; ++c) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float a = ex2(fmaf(s[c * 32 + i], sl2, neg));
+              const float b = ex2(fmaf(s[c * 32 + i + 1], sl2, neg));
+              sp[(i >> 1) & 3] += a + b;
+              pk[i / 2] = pack_bf16(a, b);
+            }
+            tmem_st16(t_s + c * 16, pk);
+          }
+          const float sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+          const float alpha = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_use) * sl2);
+          l_run = l_run * alpha + sum;
+          // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.
+          if (!first && __any_sync(0xffffffffu, alpha != 1.f)) {
+            // O_h(j-1) is final here: S_h(j) completed after PV_h(j-1) in the tensor pipe.
+#pragma unroll
+            for (int c = 0; c < kD / 32; ++c) {
+              uint32_t v[32];
+              tmem_ld32(t_o + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st32(t_o + c * 32, v);
+            }
+          }
+          m_run = mx;
+          first = false;
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&sm.p_full[h]);
+        }
+      }
+      // -------------------------------------------------------- epilogue
+      mbar_wait(&sm.o_full[h], o_phase);
+      o_phase ^= 1;
+      tc_fence_after();
+      const int qrow = it.mblock * kBM + row;
+      const bool live = qrow < seg.q_len;
+      const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
+      const float lse = (l_run > 0.f) ? (m_run == -INFINITY ? 0.f : m_run) * p.scale + logf(l_run)
+                                      : -INFINITY;
+      if (seg.out_row < 0) {
+        __nv_bfloat16* dst = p.o + (static_cast<size_t>(seg.q_off + qrow) * p.num_q_heads + head) * kD;
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_o + c * 32, v);
+          tmem_wait_ld();
+          if (live) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              uint4 w;
+              w.x = pack_bf16(__uint_as_float(v[i + 0]) * inv_l, __uint_as_float(v[i + 1]) * inv_l);
+              w.y = pack_bf16(__uint_as_float(v[i + 2]) * inv_l, __uint_as_float(v[i + 3]) * inv_l);
+              w.z = pack_bf16(__uint_as_float(v[i + 4]) * inv_l, __uint_as_float(v[i + 5]) * inv_l);
+              w.w = pack_bf16(__uint_as_float(v[i + 6]) * inv_l, __uint_as_float(v[i + 7]) * inv_l);
+              d4[i / 8] = w;
+            }
+          }
+        }
+        if (live) p.lse[static_cast<size_t>(seg.q_off + qrow) * p.num_q_heads + head] = lse;
+      } else {
+        float* dst = p.o_part + (static_cast<size_t>(seg.out_row + qrow) * p.num_q_heads + head) * kD;
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(t_o + c * 32, v);
+          tmem_wait_ld();
+          if (live) {
+            float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              d4[i / 4] = make_float4(__uint_as_float(v[i]) * inv_l, __uint_as_float(v[i + 1]) * inv_l,
+                                      __uint_as_float(v[i + 2]) * inv_l, __uint_as_float(v[i + 3]) * inv_l);
+          }
+        }
+        if (live) p.lse_part[static_cast<size_t>(seg.out_row + qrow) * p.num_q_heads + head] = lse;
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.o_empty[h]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace fwd
+}  // namespace fcpb

@@ -1,0 +1,107 @@
+// HBM-bound helper kernels: K3 LSE merge, K2 preprocess, K4 dK/dV reduce, fp32->bf16.
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "../../include/fcpb.h"
+
+namespace fcpb {
+namespace aux {
+
+// K3: one warp per (merged token, q-head); lane owns 4 of the 128 head-dim values.
+// lse = logsumexp_s lse_s ; O = sum_s exp(lse_s - lse) O_s   (partials are normalised).
+__global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int H = a.num_q_heads;
+  if (w >= a.merged_tokens * H) return;
+  const int tok = static_cast<int>(w / H);
+  const int h = static_cast<int>(w % H);
+  int lo = 0, hi = a.num_groups - 1;  // last group with tok_begin <= tok
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.groups[mid].tok_begin <= tok) lo = mid; else hi = mid - 1;
+  }
+  const FcpbMergeGroup g = a.groups[lo];
+  const int t = tok - g.tok_begin;
+  float m = -INFINITY;
+  for (int s = g.part_begin; s < g.part_end; ++s)
+    m = fmaxf(m, a.lse_partial[static_cast<int64_t>(a.part_rows[s] + t) * H + h]);
+  const float mu = (m == -INFINITY) ? 0.f : m;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float wsum = 0.f;
+  for (int s = g.part_begin; s < g.part_end; ++s) {
+    const int64_t row = static_cast<int64_t>(a.part_rows[s] + t) * H + h;
+    const float wt = __expf(a.lse_partial[row] - mu);
+    const float4 o = reinterpret_cast<const float4*>(a.o_partial + row * 128)[lane];
+    acc.x += wt * o.x; acc.y += wt * o.y; acc.z += wt * o.z; acc.w += wt * o.w;
+    wsum += wt;
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+  const int64_t out = static_cast<int64_t>(g.q_off + t) * H + h;
+  __nv_bfloat162 lo2 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  __nv_bfloat162 hi2 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  uint2 packed;
+  packed.x = *reinterpret_cast<uint32_t*>(&lo2);
+  packed.y = *reinterpret_cast<uint32_t*>(&hi2);
+  reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) + out * 128)[lane] = packed;
+  if (lane == 0) a.lse[out] = wsum > 0.f ? mu + __logf(wsum) : -INFINITY;
+}
+
+// delta[row] = <dO[row,:], O[row,:]> and dq_accum[row,:] = 0; one warp per (token, head).
+__global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
+                                                              const __nv_bfloat16* __restrict__ dout,
+                                                              float* __restrict__ delta,
+                                                              float* __restrict__ dq, int64_t rows) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const uint2 ov = reinterpret_cast<const uint2*>(o + w * 128)[lane];
+  const uint2 dv = reinterpret_cast<const uint2*>(dout + w * 128)[lane];
+  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+  const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float2 a = __bfloat1622float2(o2[i]);
+    const float2 b = __bfloat1622float2(d2[i]);
+    s = fmaf(a.x, b.x, s);
+    s = fmaf(a.y, b.y, s);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) delta[w] = s;
+  if (dq) reinterpret_cast<float4*>(dq + w * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float4* __restrict__ src,
+                                                           uint2* __restrict__ dst, int64_t n4) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = src[i];
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(v.z, v.w);
+    uint2 r;
+    r.x = *reinterpret_cast<uint32_t*>(&lo);
+    r.y = *reinterpret_cast<uint32_t*>(&hi);
+    dst[i] = r;
+  }
+}
+
+// K4: dst row dst_rows[i] += src row i (rows of `row4` float4).
+__global__ void __launch_bounds__(256) dkv_reduce_kernel(float4* __restrict__ dst,
+                                                          const float4* __restrict__ src,
+                                                          const int32_t* __restrict__ dst_rows,
+                                                          int64_t n_rows, int64_t row4) {
+  const int64_t work = n_rows * row4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < work;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / row4, c = i % row4;
+    const float4 s = src[i];
+    float4& d = dst[static_cast<int64_t>(dst_rows[r]) * row4 + c];
+    d.x += s.x; d.y += s.y; d.z += s.z; d.w += s.w;
+  }
+}
+
+}  // namespace aux
+}  // namespace fcpb

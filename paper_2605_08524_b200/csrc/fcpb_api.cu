@@ -1,0 +1,254 @@
+// libfcpb.so: C ABI over the sm_100a FCP block-attention kernels (see include/fcpb.h).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/fcpb.h"
+#include "attn_bwd_sm100.cuh"
+#include "attn_fwd_sm100.cuh"
+#include "aux_kernels.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define FCPB_CUDA(expr)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(FCPB_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
+                  __FILE__, __LINE__);                                               \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// Token-major [T, H, 128] bf16 -> 3-D map (d, head, token), box (64, 1, 128), SW128.
+int make_map(CUtensorMap* m, const void* base, int64_t tokens, int heads, int d) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(FCPB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return fail(FCPB_ERR_INVALID, "tensor base must be 16-byte aligned");
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(heads),
+                              static_cast<cuuint64_t>(tokens > 0 ? tokens : 1)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2,
+                                 static_cast<cuuint64_t>(heads) * d * 2};
+  const cuuint32_t box[3] = {64, 1, 128};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FCPB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return FCPB_OK;
+}
+
+int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+constexpr size_t kFwdSmem = sizeof(fcpb::fwd::Smem) + 1024;
+constexpr size_t kBwdSmem = sizeof(fcpb::bwd::Smem) + 1024;
+static_assert(kFwdSmem <= 232448, "fwd smem budget");
+static_assert(kBwdSmem <= 232448, "bwd smem budget");
+
+}  // namespace
+
+extern "C" {
+
+const char* fcpb_last_error(void) { return g_err; }
+int fcpb_version(void) { return 1; }
+
+int fcpb_device_supported(int device) {
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
+    return 0;
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+  return major == 10 && minor == 0;
+}
+
+int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
+  if (!a) return fail(FCPB_ERR_INVALID, "null args");
+  if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d (need 128)", a->head_dim);
+  if (a->num_q_heads % 2 || a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads ||
+      (a->num_q_heads / a->num_kv_heads) % 2)
+    return fail(FCPB_ERR_UNSUPPORTED, "need Hq/Hkv even (Hq=%d Hkv=%d)", a->num_q_heads,
+                a->num_kv_heads);
+  if (a->num_items <= 0) return FCPB_OK;
+  CUtensorMap tq, tk, tv, tkr, tvr;
+  int rc;
+  if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128))) return rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
+  if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     a->num_kv_heads, 128)))
+    return rc;
+  if ((rc = make_map(&tvr, has_recv ? a->v_recv : a->v, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     a->num_kv_heads, 128)))
+    return rc;
+  fcpb::fwd::Params p;
+  p.segs = a->segments;
+  p.kvrefs = a->kv_refs;
+  p.items = a->items;
+  p.num_items = a->num_items;
+  p.num_q_heads = a->num_q_heads;
+  p.num_kv_heads = a->num_kv_heads;
+  p.scale = a->softmax_scale;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  p.o = static_cast<__nv_bfloat16*>(a->o);
+  p.lse = a->lse;
+  p.o_part = a->o_partial;
+  p.lse_part = a->lse_partial;
+  static bool attr = false;
+  if (!attr) {
+    FCPB_CUDA(cudaFuncSetAttribute(fcpb::fwd::attn_fwd_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem));
+    attr = true;
+  }
+  const int total = a->num_items * (a->num_q_heads / 2);
+  int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
+  if (grid > total) grid = total;
+  fcpb::fwd::attn_fwd_kernel<<<grid, fcpb::fwd::kThreads, kFwdSmem,
+                               static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tkr, tvr, p);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
+  if (!a) return fail(FCPB_ERR_INVALID, "null args");
+  if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d (need 128)", a->head_dim);
+  if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
+    return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
+  if (a->num_items <= 0) return FCPB_OK;
+  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
+  int rc;
+  if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128))) return rc;
+  if ((rc = make_map(&tdo, a->dout, a->q_tokens, a->num_q_heads, 128))) return rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
+  if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     a->num_kv_heads, 128)))
+    return rc;
+  if ((rc = make_map(&tvr, has_recv ? a->v_recv : a->v, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     a->num_kv_heads, 128)))
+    return rc;
+  fcpb::bwd::Params p;
+  p.kvsegs = reinterpret_cast<const fcpb::bwd::KvSeg*>(a->kvsegs);
+  p.qrefs = reinterpret_cast<const fcpb::bwd::QRef*>(a->qrefs);
+  p.items = reinterpret_cast<const fcpb::bwd::Item*>(a->items);
+  p.num_items = a->num_items;
+  p.num_q_heads = a->num_q_heads;
+  p.num_kv_heads = a->num_kv_heads;
+  p.scale = a->softmax_scale;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  p.lse = a->lse;
+  p.delta = a->delta;
+  p.dq = a->dq_accum;
+  p.dk = a->dk_accum;
+  p.dv = a->dv_accum;
+  p.dk_recv = a->dk_recv_accum;
+  p.dv_recv = a->dv_recv_accum;
+  static bool attr = false;
+  if (!attr) {
+    FCPB_CUDA(cudaFuncSetAttribute(fcpb::bwd::attn_bwd_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem));
+    attr = true;
+  }
+  const int total = a->num_items * a->num_kv_heads;
+  int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
+  if (grid > total) grid = total;
+  fcpb::bwd::attn_bwd_kernel<<<grid, fcpb::bwd::kThreads, kBwdSmem,
+                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, p);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_lse_merge(const FcpbMergeArgs* a, void* stream) {
+  if (!a) return fail(FCPB_ERR_INVALID, "null args");
+  if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", a->head_dim);
+  if (a->num_groups <= 0) return FCPB_OK;
+  const int64_t rows = a->merged_tokens * a->num_q_heads;  // one warp per (token, head)
+  const int block = 256;
+  const int64_t grid = (rows * 32 + block - 1) / block;
+  fcpb::aux::lse_merge_kernel<<<static_cast<unsigned>(grid), block, 0,
+                                static_cast<cudaStream_t>(stream)>>>(*a);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_bwd_preprocess(const void* o, const void* dout, float* delta, float* dq_accum,
+                        int64_t tokens, int32_t num_q_heads, int32_t head_dim, void* stream) {
+  if (head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", head_dim);
+  const int64_t rows = tokens * num_q_heads;
+  if (rows == 0) return FCPB_OK;
+  const int block = 256;
+  const int64_t grid = (rows * 32 + block - 1) / block;
+  fcpb::aux::bwd_preprocess_kernel<<<static_cast<unsigned>(grid), block, 0,
+                                     static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), delta,
+      dq_accum, rows);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  if (n <= 0) return FCPB_OK;
+  if (n % 4) return fail(FCPB_ERR_INVALID, "n must be a multiple of 4");
+  const int block = 256;
+  const int64_t n4 = n / 4;
+  int64_t grid = (n4 + block - 1) / block;
+  if (grid > 148 * 16) grid = 148 * 16;
+  fcpb::aux::f32_to_bf16_kernel<<<static_cast<unsigned>(grid), block, 0,
+                                  static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), n4);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64_t n_rows,
+                    int64_t row_elems, void* stream) {
+  if (n_rows <= 0) return FCPB_OK;
+  if (row_elems % 4) return fail(FCPB_ERR_INVALID, "row_elems must be a multiple of 4");
+  const int block = 256;
+  const int64_t work = n_rows * (row_elems / 4);
+  int64_t grid = (work + block - 1) / block;
+  if (grid > 148 * 16) grid = 148 * 16;
+  fcpb::aux::dkv_reduce_kernel<<<static_cast<unsigned>(grid), block, 0,
+                                 static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), dst_rows, n_rows,
+      row_elems / 4);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+"""ctypes binding of ``libfcpb.so`` (the C ABI declared in ``include/fcpb.h``).
+
+This is the only way the package reaches the GPU kernels.  There is no CPU
+or PyTorch fallback: if the library is missing, or the device is not sm_100,
+every entry point raises ``NativeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeError, ParameterError
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcpb.so")
+
+c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+
+
+class FwdArgs(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
+                ("softmax_scale", c_f32),
+                ("q", c_vp), ("q_tokens", c_i64),
+                ("k", c_vp), ("v", c_vp), ("kv_tokens", c_i64),
+                ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
+                ("o", c_vp), ("lse", c_vp),
+                ("o_partial", c_vp), ("lse_partial", c_vp), ("partial_rows", c_i64),
+                ("segments", c_vp), ("num_segments", c_i32),
+                ("kv_refs", c_vp), ("num_kv_refs", c_i32),
+                ("items", c_vp), ("num_items", c_i32),
+                ("num_ctas", c_i32)]
+
+
+class MergeArgs(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("head_dim", c_i32),
+                ("o_partial", c_vp), ("lse_partial", c_vp),
+                ("groups", c_vp), ("num_groups", c_i32),
+                ("part_rows", c_vp), ("merged_tokens", c_i64),
+                ("o", c_vp), ("lse", c_vp)]
+
+
+class BwdArgs(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
+                ("softmax_scale", c_f32),
+                ("q", c_vp), ("dout", c_vp), ("lse", c_vp), ("delta", c_vp), ("q_tokens", c_i64),
+                ("k", c_vp), ("v", c_vp), ("kv_tokens", c_i64),
+                ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
+                ("dq_accum", c_vp), ("dk_accum", c_vp), ("dv_accum", c_vp),
+                ("dk_recv_accum", c_vp), ("dv_recv_accum", c_vp),
+                ("kvsegs", c_vp), ("num_kvsegs", c_i32),
+                ("qrefs", c_vp), ("num_qrefs", c_i32),
+                ("items", c_vp), ("num_items", c_i32),
+                ("num_ctas", c_i32)]
+
+
+EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_lse_merge", "fcpb_bwd_preprocess",
+           "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_last_error", "fcpb_version",
+           "fcpb_device_supported")
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and type the shared library; raises NativeError if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or _LIB_PATH
+    if not os.path.exists(p):
+        raise NativeError(f"{p} not built: run `make` (or __graft_entry__.build())")
+    lib = ctypes.CDLL(p)
+    lib.fcpb_attn_fwd.argtypes = [ctypes.POINTER(FwdArgs), c_vp]
+    lib.fcpb_attn_bwd.argtypes = [ctypes.POINTER(BwdArgs), c_vp]
+    lib.fcpb_lse_merge.argtypes = [ctypes.POINTER(MergeArgs), c_vp]
+    lib.fcpb_bwd_preprocess.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]
+    lib.fcpb_f32_to_bf16.argtypes = [c_vp, c_vp, c_i64, c_vp]
+    lib.fcpb_dkv_reduce.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]
+    lib.fcpb_last_error.restype = ctypes.c_char_p
+    lib.fcpb_device_supported.argtypes = [ctypes.c_int]
+    for name in EXPORTS:
+        getattr(lib, name).restype = ctypes.c_char_p if name == "fcpb_last_error" else ctypes.c_int
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = load().fcpb_last_error().decode(errors="replace")
+    if rc == -1:
+        raise ParameterError(msg)
+    raise NativeError(f"libfcpb status {rc}: {msg}")
+
+
+def ptr(t) -> int:
+    """Device pointer of a torch tensor, or 0 for None."""
+    return 0 if t is None else t.data_ptr()
+
+
+def stream_handle(stream) -> int:
+    return stream.cuda_stream if stream is not None else 0

@@ -1,0 +1,245 @@
+"""H1: turn a ``ScheduleResult`` into per-rank device work lists.
+
+Nothing here exists in the reference: it is the bridge from the plan the
+reference computes (``pipeline.py:31-60``) to the tiles its simulator only
+times (``simulator.py:73-109``).  For rank ``r``:
+
+* **Layout.**  Local chunks are packed token-major in unit-id order (members
+  in unit order); this is the layout of the rank's Q, K, V, O, dO, dQ, dK, dV.
+  Remote chunks the rank receives get slots in a *receive arena*, ordered by
+  the coalesced stage that delivers them, then by plan edge order
+  (``simulator.py:112-133`` defines the arrival stage).
+* **Forward waves.**  Wave -1 holds every (Q chunk, KV chunk) tile whose KV is
+  local -- the dependency-free prologue; wave s holds tiles whose KV arrives
+  with coalesced stage s.  A Q chunk whose tiles span several waves writes one
+  fp32 partial (O, LSE) per wave, merged by K3 afterwards; a Q chunk served by
+  a single wave writes its final bf16 O directly.
+* **Backward.**  Work is keyed by KV chunk (local or received): the KV block
+  iterates over every local Q chunk attending to it.  Received chunks form
+  their own launch so their dK/dV partials can travel back along the reversed
+  plan edges while the local chunks compute.
+
+Work items are sorted longest-first (LPT over the persistent grid).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .costmodel import tile_token_pairs
+from .distributor import chunk_placement
+from .errors import ConsistencyError, ParameterError
+from .pipeline import ScheduleResult
+from .sharding import CAUSAL, ChunkKey
+from .simmodel import arrival_stages
+
+TILE = 128
+KV_DIAG = 1
+KV_RECV = 2
+LOCAL_WAVE = -1
+
+
+def _cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+@dataclass
+class RankLayout:
+    rank: int
+    chunks: list[ChunkKey]
+    offset: dict[ChunkKey, int]
+    tokens: int
+    recv_chunks: list[ChunkKey]
+    recv_offset: dict[ChunkKey, int]
+    recv_tokens: int
+    recv_stage: dict[ChunkKey, int]
+    chunk_tokens: dict[ChunkKey, int]
+
+
+@dataclass
+class FwdWave:
+    stage: int                   # LOCAL_WAVE or the coalesced stage that releases it
+    segments: np.ndarray         # int32 [S, 6]: q_off q_len kv_begin kv_end out_row pad
+    kvrefs: np.ndarray           # int32 [R, 4]: off len flags pad
+    items: np.ndarray            # int32 [I, 2]: seg mblock
+    pairs: int                   # visible token pairs (reference tile_token_pairs)
+
+
+@dataclass
+class FwdPlan:
+    waves: list[FwdWave]
+    partial_rows: int
+    merge_groups: np.ndarray     # int32 [G, 6]: q_off q_len part_begin part_end tok_begin pad
+    merge_part_rows: np.ndarray  # int32 [P]
+    merged_tokens: int
+
+
+@dataclass
+class BwdLaunch:
+    recv: bool
+    kvsegs: np.ndarray           # int32 [K, 6]: kv_off kv_len flags q_begin q_end pad
+    qrefs: np.ndarray            # int32 [Q, 4]: q_off q_len diag pad
+    items: np.ndarray            # int32 [I, 2]: kvseg nblock
+    pairs: int
+
+
+@dataclass
+class RankWork:
+    layout: RankLayout
+    fwd: FwdPlan
+    bwd: list[BwdLaunch] = field(default_factory=list)
+    pairs: int = 0
+
+
+def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
+    n = result.assignment.n_workers
+    if not 0 <= rank < n:
+        raise ParameterError(f"rank {rank} outside [0, {n})")
+    chunks: list[ChunkKey] = []
+    sizes = dict(result.deps.chunk_tokens)
+    for u in sorted(result.units, key=lambda u: u.unit_id):
+        if result.assignment.worker_of(u.unit_id) == rank:
+            chunks += [c.key for c in u.members]
+    offset, pos = {}, 0
+    for c in chunks:
+        offset[c] = pos
+        pos += sizes[c]
+    where = chunk_placement(result.assignment, result.units)
+    arrival = arrival_stages(result.plan.stages, where)
+    recv = []
+    for s, stage in enumerate(result.plan.stages):
+        for e in stage:
+            if e.dst == rank:
+                for c in e.chunks:
+                    if arrival[(c, rank)] == s and c not in recv:
+                        recv.append(c)
+    roff, rpos = {}, 0
+    for c in recv:
+        roff[c] = rpos
+        rpos += sizes[c]
+    rstage = {c: arrival[(c, rank)] for c in recv}
+    return RankLayout(rank, chunks, offset, pos, recv, roff, rpos, rstage, sizes)
+
+
+def _kv_location(lay: RankLayout, kv: ChunkKey) -> tuple[int, int, int]:
+    """(wave, arena offset, flags) of a KV chunk as seen from this rank."""
+    if kv in lay.offset:
+        return LOCAL_WAVE, lay.offset[kv], 0
+    if kv in lay.recv_offset:
+        return lay.recv_stage[kv], lay.recv_offset[kv], KV_RECV
+    raise ConsistencyError(f"plan never delivers chunk {kv} to rank {lay.rank}")
+
+
+def build_forward(result: ScheduleResult, lay: RankLayout) -> FwdPlan:
+    deps = result.deps
+    causal = deps.mask == CAUSAL
+    # per Q chunk: wave -> ordered kv list
+    per_q: dict[ChunkKey, dict[int, list[tuple[int, int, int, int]]]] = {}
+    for q in lay.chunks:
+        waves: dict[int, list] = {}
+        for kv in deps.q_to_kv[q]:
+            wave, off, flags = _kv_location(lay, kv)
+            if causal and kv == q:
+                flags |= KV_DIAG
+            waves.setdefault(wave, []).append((off, deps.chunk_tokens[kv], flags, 0))
+        per_q[q] = waves
+
+    wave_ids = sorted({w for waves in per_q.values() for w in waves})
+    part_rows = 0
+    partial_of: dict[ChunkKey, list[tuple[int, int]]] = {}   # q -> [(wave, row)]
+    seg_rows: dict[tuple[ChunkKey, int], int] = {}
+    for q in lay.chunks:
+        waves = per_q[q]
+        if len(waves) > 1:
+            for w in sorted(waves):
+                seg_rows[(q, w)] = part_rows
+                partial_of.setdefault(q, []).append((w, part_rows))
+                part_rows += deps.chunk_tokens[q]
+    out = []
+    for w in wave_ids:
+        segs, refs, items, pairs = [], [], [], 0
+        for q in lay.chunks:
+            kvs = per_q[q].get(w)
+            if not kvs:
+                continue
+            qn = deps.chunk_tokens[q]
+            begin = len(refs)
+            refs += kvs
+            for off, kn, flags, _ in kvs:
+                pairs += tile_token_pairs(qn, kn, bool(flags & KV_DIAG))
+            out_row = seg_rows.get((q, w), -1)
+            sidx = len(segs)
+            segs.append((lay.offset[q], qn, begin, len(refs), out_row, 0))
+            for mb in range(_cdiv(qn, TILE)):
+                cost = 0
+                for off, kn, flags, _ in kvs:
+                    nt = _cdiv(kn, TILE)
+                    cost += min(nt, mb + 1) if flags & KV_DIAG else nt
+                items.append((cost, sidx, mb))
+        items.sort(key=lambda t: (-t[0], t[1], t[2]))
+        out.append(FwdWave(
+            w, np.asarray(segs, dtype=np.int32).reshape(-1, 6),
+            np.asarray(refs, dtype=np.int32).reshape(-1, 4),
+            np.asarray([(s, m) for _, s, m in items], dtype=np.int32).reshape(-1, 2), pairs))
+    groups, rows, tok = [], [], 0
+    for q in lay.chunks:
+        if q in partial_of:
+            begin = len(rows)
+            rows += [r for _, r in partial_of[q]]
+            groups.append((lay.offset[q], deps.chunk_tokens[q], begin, len(rows), tok, 0))
+            tok += deps.chunk_tokens[q]
+    return FwdPlan(out, part_rows, np.asarray(groups, dtype=np.int32).reshape(-1, 6),
+                   np.asarray(rows, dtype=np.int32), tok)
+
+
+def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
+    deps = result.deps
+    causal = deps.mask == CAUSAL
+    consumers: dict[ChunkKey, list[ChunkKey]] = {}
+    local = set(lay.chunks)
+    for q in lay.chunks:
+        for kv in deps.q_to_kv[q]:
+            consumers.setdefault(kv, []).append(q)
+    launches = []
+    for recv in (True, False):
+        kv_list = lay.recv_chunks if recv else lay.chunks
+        kvsegs, qrefs, items, pairs = [], [], [], 0
+        for kv in kv_list:
+            qs = consumers.get(kv, [])
+            if not qs:
+                if not recv:
+                    continue
+                raise ConsistencyError(f"received chunk {kv} has no consumer on rank {lay.rank}")
+            kn = deps.chunk_tokens[kv]
+            off = lay.recv_offset[kv] if recv else lay.offset[kv]
+            begin = len(qrefs)
+            for q in qs:
+                assert q in local
+                diag = int(causal and q == kv)
+                qrefs.append((lay.offset[q], deps.chunk_tokens[q], diag, 0))
+                pairs += tile_token_pairs(deps.chunk_tokens[q], kn, bool(diag))
+            kidx = len(kvsegs)
+            kvsegs.append((off, kn, KV_RECV if recv else 0, begin, len(qrefs), 0))
+            for nb in range(_cdiv(kn, TILE)):
+                cost = 0
+                for q in qs:
+                    qb = _cdiv(deps.chunk_tokens[q], TILE)
+                    cost += qb - nb if (causal and q == kv) else qb
+                items.append((cost, kidx, nb))
+        if not kvsegs:
+            continue
+        items.sort(key=lambda t: (-t[0], t[1], t[2]))
+        launches.append(BwdLaunch(
+            recv, np.asarray(kvsegs, dtype=np.int32).reshape(-1, 6),
+            np.asarray(qrefs, dtype=np.int32).reshape(-1, 4),
+            np.asarray([(k, b) for _, k, b in items], dtype=np.int32).reshape(-1, 2), pairs))
+    return launches
+
+
+def build_rank_work(result: ScheduleResult, rank: int) -> RankWork:
+    lay = rank_layout(result, rank)
+    fwd = build_forward(result, lay)
+    bwd = build_backward(result, lay)
+    return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves))

@@ -1,0 +1,151 @@
+"""CPU oracle ladder: SDPA pin -> dense -> tiled -> work-list emulation (N=1, 2, 3).
+
+Level 3 interprets the exact device work lists the kernels consume, with
+in-process copies standing in for the NVLink exchange, so the host side of the
+data plane (layout, waves, partial rows, merge groups, KV-keyed backward, dKV
+return) is verified here without a GPU.
+"""
+
+import math
+
+import pytest
+import torch
+
+from oracle.attention_ref import (emulate_backward, emulate_forward, mono_bwd, mono_fwd,
+                                  sequence_rows, tiled_fwd)
+from oracle.simworkers import (gather_rank, global_offsets, global_sequence_rows,
+                               return_partials, scatter_rank)
+from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, ModelConfig
+from paper_2605_08524_b200.distributor import chunk_placement
+from paper_2605_08524_b200.pipeline import fcp_schedule
+from paper_2605_08524_b200.sharding import ShardingConfig
+from paper_2605_08524_b200.workload import Batch, Sequence
+from paper_2605_08524_b200.worklist import build_rank_work
+
+MODEL = ModelConfig(q_heads=4, kv_heads=2, head_dim=32, dtype_bytes=2)
+
+
+def _schedule(lengths, n, block, mask="causal"):
+    tpw = -(-sum(lengths) // n)
+    batch = Batch(tuple(Sequence(i, l) for i, l in enumerate(lengths)), n, tpw)
+    return fcp_schedule(batch, n, ShardingConfig(block, mask), MODEL, DEFAULT_EFFICIENCY)
+
+
+def _inputs(T, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    H, Hk, D = MODEL.q_heads, MODEL.kv_heads, MODEL.head_dim
+    mk = lambda h: torch.randn((T, h, D), generator=g, dtype=torch.float64)
+    return mk(H), mk(Hk), mk(Hk), mk(H)
+
+
+def test_dense_matches_torch_sdpa():
+    lengths = [300, 77, 1]
+    T = sum(lengths)
+    q, k, v, _ = _inputs(T)
+    rows, pos = {}, 0
+    for i, l in enumerate(lengths):
+        rows[i] = torch.arange(pos, pos + l)
+        pos += l
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    o, _ = mono_fwd(q, k, v, rows, scale)
+    for idx in rows.values():
+        qq = q[idx].transpose(0, 1)
+        kk = k[idx].repeat_interleave(2, 1).transpose(0, 1)
+        vv = v[idx].repeat_interleave(2, 1).transpose(0, 1)
+        ref = torch.nn.functional.scaled_dot_product_attention(qq, kk, vv, is_causal=True)
+        assert torch.allclose(o[idx].transpose(0, 1), ref, atol=1e-12)
+
+
+def test_dense_backward_matches_autograd():
+    lengths = [200, 31]
+    T = sum(lengths)
+    q, k, v, do = _inputs(T, 1)
+    rows = {0: torch.arange(0, 200), 1: torch.arange(200, 231)}
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    qa, ka, va = (x.clone().requires_grad_() for x in (q, k, v))
+    o, lse = mono_fwd(q, k, v, rows, scale)
+    dq, dk, dv = mono_bwd(q, k, v, o, lse, do, rows, scale)
+    outs = []
+    for idx in rows.values():
+        qq = qa[idx].transpose(0, 1)
+        kk = ka[idx].repeat_interleave(2, 1).transpose(0, 1)
+        vv = va[idx].repeat_interleave(2, 1).transpose(0, 1)
+        outs.append((idx, torch.nn.functional.scaled_dot_product_attention(qq, kk, vv, is_causal=True)))
+    loss = sum((y.transpose(0, 1) * do[idx]).sum() for idx, y in outs)
+    loss.backward()
+    for a, b in ((dq, qa.grad), (dk, ka.grad), (dv, va.grad)):
+        assert torch.allclose(a, b, atol=1e-10)
+
+
+@pytest.mark.parametrize("mask", ["causal", "full"])
+def test_tiled_equals_dense(mask):
+    r = _schedule([1000, 333, 200, 90, 45], 1, 256, mask)
+    lay = build_rank_work(r, 0).layout
+    q, k, v, _ = _inputs(lay.tokens, 2)
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    rows = sequence_rows(r.deps, lay.offset)
+    o1, l1 = mono_fwd(q, k, v, rows, scale, causal=(mask == "causal"))
+    o2, l2 = tiled_fwd(q, k, v, r.deps, lay.offset, scale)
+    assert torch.allclose(o1, o2, atol=1e-10)
+    assert torch.allclose(l1, l2, atol=1e-10)
+
+
+@pytest.mark.parametrize("n,lengths,block", [
+    (1, [700, 260, 130, 100, 50, 9], 256),
+    (2, [700, 260, 130, 100, 50, 9], 256),
+    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256),
+])
+def test_worklist_emulation_matches_dense(n, lengths, block):
+    """Simulated workers: per-rank work lists + in-process exchange == dense attention."""
+    r = _schedule(lengths, n, block)
+    works = [build_rank_work(r, w) for w in range(n)]
+    goff, T = global_offsets(r)
+    q, k, v, do = _inputs(T, 3)
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    rows = global_sequence_rows(r)
+    o_ref, l_ref = mono_fwd(q, k, v, rows, scale)
+    dq_ref, dk_ref, dv_ref = mono_bwd(q, k, v, o_ref, l_ref, do, rows, scale)
+
+    deps = r.deps
+    owner = chunk_placement(r.assignment, r.units)
+    o = torch.zeros_like(q)
+    lse = torch.zeros_like(l_ref)
+    dq = torch.zeros_like(q)
+    dk_loc, dv_loc, dk_recv, dv_recv = [], [], [], []
+    for w, work in enumerate(works):
+        lay = work.layout
+        ql, kl, vl, dol = (gather_rank(x, lay, goff, deps) for x in (q, k, v, do))
+        kr, vr = (gather_rank(x, lay, goff, deps, recv=True) for x in (k, v))
+        ow, lw = emulate_forward(work, ql, kl, vl, kr, vr, scale)
+        scatter_rank(ow, o, lay, goff, deps)
+        scatter_rank(lw, lse, lay, goff, deps)
+        dqw, dkw, dvw, dkrw, dvrw = emulate_backward(work, ql, kl, vl, kr, vr, ow, lw, dol, scale)
+        scatter_rank(dqw, dq, lay, goff, deps)
+        dk_loc.append(dkw)
+        dv_loc.append(dvw)
+        dk_recv.append(dkrw)
+        dv_recv.append(dvrw)
+    layouts = [wk.layout for wk in works]
+    return_partials(dk_recv, dk_loc, layouts, deps, owner)
+    return_partials(dv_recv, dv_loc, layouts, deps, owner)
+    dk = torch.zeros_like(k)
+    dv = torch.zeros_like(v)
+    for w, work in enumerate(works):
+        scatter_rank(dk_loc[w], dk, work.layout, goff, deps)
+        scatter_rank(dv_loc[w], dv, work.layout, goff, deps)
+    for a, b in ((o, o_ref), (lse, l_ref), (dq, dq_ref), (dk, dk_ref), (dv, dv_ref)):
+        assert torch.allclose(a, b, atol=1e-9), (a - b).abs().max()
+    if n > 1:
+        assert any(wk.fwd.partial_rows for wk in works)   # the merge path was exercised
+
+
+def test_worklist_pairs_match_reference_accounting():
+    """Visible pairs of all tiles == batch_token_pairs (reference costmodel.py:196-200)."""
+    from paper_2605_08524_b200.costmodel import batch_token_pairs
+    lengths = [5000, 2049, 2048, 2047, 300, 1]
+    for n in (1, 2, 4):
+        r = _schedule(lengths, n, 2048)
+        tot = sum(build_rank_work(r, w).pairs for w in range(n))
+        assert tot == batch_token_pairs(lengths, "causal")
+        tot_b = sum(b.pairs for w in range(n) for b in build_rank_work(r, w).bwd)
+        assert tot_b == tot
