@@ -1,0 +1,356 @@
+#!/usr/bin/env python3
+"""FCP block-attention fwd+bwd benchmark on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step = one attention layer forward + backward over the whole batch: FCP plan
+(computed once per batch, outside the timed region, like the paper) -> per rank:
+local tiles, staged KV exchange over NVLink overlapped with released tiles,
+LSE merge, backward with the dK/dV return.  Prints ONE JSON line on rank 0.
+
+Metric (BASELINE.json): CP attention fwd+bwd tokens/s (sum of sequence lengths /
+max-over-ranks step time) and MFU = 3.5 * 4*Hq*D*sum L(L+1)/2 / (N * peak * T).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2605_08524_b200 import configs  # noqa: E402
+from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, batch_token_pairs  # noqa: E402
+from paper_2605_08524_b200.distributor import worker_loads  # noqa: E402
+from paper_2605_08524_b200.pipeline import fcp_schedule  # noqa: E402
+from paper_2605_08524_b200.sharding import ShardingConfig  # noqa: E402
+
+METRIC = "CP attention fwd+bwd tokens/sec and MFU at 1/2/4/8 B200 (max over ranks)"
+UNIT = "tokens/s"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["bf16_tflops"]) * 1e12, float(d.get("bf16_tflops_sustained", 0)) * 1e12, \
+            float(d.get("hbm_gbs", 6555)) * 1e9, "measured"
+    except Exception:
+        return 1.59e15, 1.4e15, 6.65e12, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_workload(name: str, n: int, block: int | None):
+    w = configs.by_name(name, n, block)
+    result = fcp_schedule(w.batch(), n, ShardingConfig(block_size=w.block_size), w.model,
+                          DEFAULT_EFFICIENCY)
+    return w, result
+
+
+def rank_inputs(ex, rank, cfg, device, pin=False):
+    g = torch.Generator().manual_seed(1234 + rank)
+    T, H, Hk, D = ex.tokens, cfg.q_heads, cfg.kv_heads, cfg.head_dim
+    host = [torch.randn((T, h, D), generator=g).to(torch.bfloat16) for h in (H, Hk, Hk, H)]
+    if pin:
+        host = [x.pin_memory() for x in host]
+    return host, [x.to(device) for x in host]
+
+
+# ---------------------------------------------------------------------------- CPU legs
+def cpu_sample(w, result, budget_s=20.0, threads=None):
+    """Oracle fp32 fwd+bwd (torch CPU, all host threads) on whole sequences of the
+    workload, growing the sample until ~budget; tokens/s extrapolated by the
+    pair fraction.  Returns (tokens_per_s, info)."""
+    sys.path.insert(0, ROOT)
+    from oracle.attention_ref import mono_bwd, mono_fwd
+    threads = threads or os.cpu_count()
+    torch.set_num_threads(threads)
+    cfg = w.model
+    lengths = list(w.lengths)
+    order = sorted(range(len(lengths)), key=lambda i: lengths[i])
+    g = torch.Generator().manual_seed(1234)
+    scale = 1.0 / math.sqrt(cfg.head_dim)
+    done_pairs, spent, used = 0, 0.0, []
+    for i in order[len(order) // 2:] + order[:len(order) // 2]:
+        L = lengths[i]
+        if spent > budget_s:
+            break
+        mk = lambda h: torch.randn((L, h, cfg.head_dim), generator=g).to(torch.bfloat16).float()
+        q, k, v, do = mk(cfg.q_heads), mk(cfg.kv_heads), mk(cfg.kv_heads), mk(cfg.q_heads)
+        rows = {0: torch.arange(L)}
+        t0 = time.perf_counter()
+        o, lse = mono_fwd(q, k, v, rows, scale, True, torch.float32)
+        mono_bwd(q, k, v, o, lse, do, rows, scale, True, torch.float32)
+        spent += time.perf_counter() - t0
+        done_pairs += L * (L + 1) // 2
+        used.append(L)
+    total_pairs = batch_token_pairs(lengths, "causal")
+    t_batch = spent * total_pairs / done_pairs
+    return sum(lengths) / t_batch, {"cores": threads, "sample_seqs": used, "sample_s": round(spent, 2),
+                                    "pair_fraction": done_pairs / total_pairs}
+
+
+def run_reference(args):
+    """--impl reference: the reference path's CPU implementation (the oracle port:
+    the reference has no attention code) on the same workload, all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.gpus
+    w, result = build_workload(args.config, n, args.block)
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_sample(w, result, budget_s=args.cpu_budget / max(1, args.steps))
+        if i >= args.warmup:
+            vals.append(v)
+    value = sorted(vals)[len(vals) // 2]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": w.name, "global_batch_tokens": w.total_tokens,
+                       "block": w.block_size, "heads": [w.model.q_heads, w.model.kv_heads],
+                       "head_dim": w.model.head_dim},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                             "sample": f"oracle fp32 fwd+bwd of whole sequences {info['sample_seqs']} "
+                                       f"({info['pair_fraction']:.3f} of the batch's pairs), "
+                                       "extrapolated by pair count"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- GPU leg
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--block", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = world if world > 1 else args.gpus
+    if world == 1 and args.gpus > 1:
+        # not launched under torchrun: N independent ranks need N processes
+        raise SystemExit("run N>1 under torch.distributed.run (one process per GPU)")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2605_08524_b200.executor import FcpExecutor
+
+    peak, peak_sus, hbm, peak_kind = load_peaks()
+    t_plan = time.perf_counter()
+    w, result = build_workload(args.config, n, args.block)
+    plan_ms = (time.perf_counter() - t_plan) * 1e3
+    cfg = w.model
+    ex = FcpExecutor(result, rank, cfg, device)
+    host, (q, k, v, do) = rank_inputs(ex, rank, cfg, device, pin=not args.no_e2e)
+    stream = torch.cuda.current_stream(device)
+
+    # kernel-level events (on the launching stream) for the roofline
+    lib_launch = {"fwd": [], "bwd": []}
+    orig_fw, orig_bl = ex.op.forward_wave, ex.op.backward_launch
+    timing = {"on": False}
+
+    def timed_fw(*a, **kw):
+        if not timing["on"]:
+            return orig_fw(*a, **kw)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        orig_fw(*a, **kw)
+        e.record(stream)
+        lib_launch["fwd"].append((s, e))
+
+    def timed_bl(recv, *a, **kw):
+        if not timing["on"]:
+            return orig_bl(recv, *a, **kw)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        orig_bl(recv, *a, **kw)
+        e.record(stream)
+        lib_launch["bwd"].append((s, e))
+
+    ex.op.forward_wave, ex.op.backward_launch = timed_fw, timed_bl
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        ex.step(q, k, v, do)
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = ex.op.launches
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            ex.step(q, k, v, do)
+        end.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = ex.op.launches - launches0
+    ms = start.elapsed_time(end) / args.steps
+    # per-kernel share (separate pass so the kernel events do not perturb the step time)
+    timing["on"] = True
+    for _ in range(min(3, args.steps)):
+        ex.step(q, k, v, do)
+    torch.cuda.synchronize()
+    timing["on"] = False
+    # e2e: host buffers in, results out, through the public executor API
+    e2e = None
+    if not args.no_e2e:
+        outs_host = None
+        h2d = sum(x.numel() * x.element_size() for x in host)
+        t_e2e = []
+        for it in range(args.warmup + args.steps):
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            qd, kd, vd, dod = (x.to(device, non_blocking=True) for x in host)
+            o_, lse_, gq, gk, gv = ex.step(qd, kd, vd, dod)
+            res = [t.to("cpu", non_blocking=True) for t in (o_, lse_, gq, gk, gv)]
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                t_e2e.append(dt)
+            outs_host = res
+        d2h = sum(x.numel() * x.element_size() for x in outs_host)
+        e2e_s = sorted(t_e2e)[len(t_e2e) // 2]
+        if world > 1:
+            t = torch.tensor([e2e_s], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = t.item()
+        e2e = {"value": w.total_tokens / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3}
+
+    t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    fwd_f, bwd_f = ex.flops()
+    total_pairs = batch_token_pairs(list(w.lengths), "causal")
+    flop_total = 3.5 * cfg.flops_per_token_pair * total_pairs
+    loads = worker_loads(result.assignment, result.units, result.deps, cfg)
+    exb = ex.exchange_bytes()
+
+    if rank == 0:
+        value = w.total_tokens / (ms_max / 1e3)
+        mfu = flop_total / (n * peak * ms_max / 1e3)
+        n_fwd = len(lib_launch["fwd"]) or 1
+        n_bwd = len(lib_launch["bwd"]) or 1
+        reps = min(3, args.steps)
+        fwd_ms = sum(s.elapsed_time(e) for s, e in lib_launch["fwd"]) / reps
+        bwd_ms = sum(s.elapsed_time(e) for s, e in lib_launch["bwd"]) / reps
+        bwd_tflops = bwd_f / (bwd_ms / 1e3) / 1e12 if bwd_ms > 0 else 0.0
+        fwd_tflops = fwd_f / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else 0.0
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong" if args.config in ("c2", "c3") else "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": w.name, "global_batch_tokens": w.total_tokens,
+                       "sequences": len(w.lengths), "block": w.block_size,
+                       "q_heads": cfg.q_heads, "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim,
+                       "parallelism": f"fcp{n}", "l2": "inputs larger than L2 (no flush needed)",
+                       "plan_ms_host": round(plan_ms, 2)},
+            "mfu": mfu, "flop_total": flop_total,
+            "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel",
+                         "achieved": bwd_tflops, "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": bwd_tflops * 1e12 / peak, "peak_kind": peak_kind + " burst",
+                         "traffic": None,
+                         "per_unit": "2.5*4*Hq*D FLOP per visible (q,kv) pair; units = rank-0 pairs"},
+            "kernels": {"attn_fwd_kernel": {"ms": fwd_ms, "tflops": fwd_tflops,
+                                            "frac": fwd_tflops * 1e12 / peak, "launches": n_fwd / reps},
+                        "attn_bwd_kernel": {"ms": bwd_ms, "tflops": bwd_tflops,
+                                            "frac": bwd_tflops * 1e12 / peak, "launches": n_bwd / reps}},
+            "exchange_bytes_rank0": exb,
+            "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+        }
+        if not args.no_cpu and n == 1:
+            cv, info = cpu_sample(w, result, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                                    "sample": f"oracle fp32 fwd+bwd (torch CPU) of whole sequences "
+                                              f"{info['sample_seqs']} = {info['pair_fraction']:.3f} of the "
+                                              f"batch's pairs in {info['sample_s']} s, extrapolated"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

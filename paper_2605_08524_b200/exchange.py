@@ -1,0 +1,137 @@
+"""K5/K6: execute the coalesced Delta-matching plan as point-to-point transfers.
+
+Each coalesced stage of ``ScheduleResult.plan`` (reference ``planner.py:234-248``)
+becomes one grouped send/recv batch: this rank sends every KV chunk it owns on
+an edge ``src == rank`` and receives every chunk on an edge ``dst == rank`` into
+that chunk's receive-arena slot (``worklist.rank_layout``).  Every round of a
+stage is a matching, so within a stage each GPU sends at most ``degree`` and
+receives at most ``degree`` chunks -- over NVSwitch (uniform 900 GB/s per
+direction to every peer) this is the congestion-free schedule the reference
+models with its flat full-duplex NIC (``simulator.py:136-151``).
+
+The backward return (K6) walks the same edges reversed: the receiver sends the
+chunk's dK/dV partial back to the owner, which adds it with K4.
+
+The transport is ``torch.distributed`` P2P (NCCL on GPUs; gloo in the CPU tests),
+issued on a dedicated communication stream and ordered against compute with
+CUDA events; the ops only describe *which rows* move, so the same plan object
+drives both backends.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from .pipeline import ScheduleResult
+from .worklist import RankLayout
+
+
+@dataclass
+class Transfer:
+    peer: int
+    row: int          # first token row (local buffer for sends, receive arena for recvs)
+    tokens: int
+    chunk: tuple[int, int]
+
+
+@dataclass
+class StageOps:
+    sends: list[Transfer] = field(default_factory=list)
+    recvs: list[Transfer] = field(default_factory=list)
+
+    @property
+    def empty(self) -> bool:
+        return not self.sends and not self.recvs
+
+
+def build_stage_ops(result: ScheduleResult, lay: RankLayout, all_layouts=None) -> list[StageOps]:
+    """Per coalesced stage, this rank's sends (from its local rows) and receives
+    (into its receive arena), in plan edge order."""
+    rank = lay.rank
+    out = []
+    for s, stage in enumerate(result.plan.stages):
+        ops = StageOps()
+        for e in stage:
+            for c in e.chunks:
+                n = lay.chunk_tokens[c]
+                if e.src == rank:
+                    ops.sends.append(Transfer(e.dst, lay.offset[c], n, c))
+                if e.dst == rank and lay.recv_stage.get(c) == s:
+                    ops.recvs.append(Transfer(e.src, lay.recv_offset[c], n, c))
+        out.append(ops)
+    return out
+
+
+def _p2p(ops, group=None):
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+def run_stage(stage: StageOps, send_bufs, recv_bufs, group=None):
+    """Post one stage's grouped sends/recvs.  ``send_bufs``/``recv_bufs`` are
+    lists of [tokens, ...] tensors moved together (e.g. (K, V)); returns works."""
+    ops = []
+    for t in stage.sends:
+        for buf in send_bufs:
+            ops.append(dist.P2POp(dist.isend, buf[t.row:t.row + t.tokens], t.peer, group))
+    for t in stage.recvs:
+        for buf in recv_bufs:
+            ops.append(dist.P2POp(dist.irecv, buf[t.row:t.row + t.tokens], t.peer, group))
+    return _p2p(ops, group)
+
+
+def run_return(stages: list[StageOps], partial_bufs, staging_bufs, staging_rows, group=None):
+    """Reverse every edge of every stage in one group: receivers send their fp32
+    dK/dV partials back; owners receive them into ``staging_bufs`` at
+    ``staging_rows[(chunk, peer)]``."""
+    ops = []
+    for st in stages:
+        for t in st.recvs:          # I received chunk t.chunk from t.peer: send partial back
+            for buf in partial_bufs:
+                ops.append(dist.P2POp(dist.isend, buf[t.row:t.row + t.tokens], t.peer, group))
+        for t in st.sends:          # I sent chunk to t.peer: receive its partial
+            r = staging_rows[(t.chunk, t.peer)]
+            for buf in staging_bufs:
+                ops.append(dist.P2POp(dist.irecv, buf[r:r + t.tokens], t.peer, group))
+    return _p2p(ops, group)
+
+
+def return_staging_layout(stages: list[StageOps]):
+    """Rows of the owner-side staging buffer for returned partials, plus the
+    owner's destination row of each staged row (for the K4 reduce)."""
+    rows, dst, pos = {}, [], 0
+    for st in stages:
+        for t in st.sends:
+            rows[(t.chunk, t.peer)] = pos
+            dst.extend(range(t.row, t.row + t.tokens))
+            pos += t.tokens
+    return rows, dst, pos
+
+
+def exchange_bytes(stages: list[StageOps], bytes_per_token: int) -> tuple[int, int]:
+    sent = sum(t.tokens for st in stages for t in st.sends) * bytes_per_token
+    got = sum(t.tokens for st in stages for t in st.recvs) * bytes_per_token
+    return sent, got
+
+
+def wait_all(works):
+    for w in works:
+        w.wait()
+
+
+def sync_plan_digest(digest: str, group=None) -> None:
+    """All ranks must hold the same plan: all-gather its hash (cheap, once per batch)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    mine = torch.tensor([int(digest, 16) & ((1 << 62) - 1)], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        mine = mine.cuda()
+    got = [torch.zeros_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(got, mine, group=group)
+    if any(int(x.item()) != int(mine.item()) for x in got):
+        from .errors import ConsistencyError
+        raise ConsistencyError("ranks disagree on the FCP plan (hash mismatch)")
