@@ -87,15 +87,18 @@ typedef struct {
 
 FCPB_API int fcpb_lse_merge(const FcpbMergeArgs* args, void* stream);
 
-/* K2 preprocess: delta[t,h] = sum_d dO[t,h,d] * O[t,h,d] (fp32), and zero the
- * fp32 dQ accumulator. */
-FCPB_API int fcpb_bwd_preprocess(const void* o, const void* dout, float* delta, float* dq_accum,
-                        int64_t tokens, int32_t num_q_heads, int32_t head_dim, void* stream);
+/* K2 preprocess: delta = rowsum(dO * O) and lse2 = lse * log2(e), both written
+ * head-major [Hq, t_pad] fp32 (t_pad = tokens rounded up to 4, TMA row pitch), and
+ * zero the fp32 dQ accumulator [tokens, Hq, D]. */
+FCPB_API int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse,
+                                 float* lse2_t, float* delta_t, int64_t t_pad, float* dq_accum,
+                                 int64_t tokens, int32_t num_q_heads, int32_t head_dim,
+                                 void* stream);
 
 /* K2: backward.  Work is organised by KV tile: for each KV chunk reference (local
  * or received) the list of local Q chunks that attend to it.  dK/dV accumulate in
- * fp32 per KV arena row; dQ accumulates in fp32 (dq_accum) and is converted by
- * fcpb_dq_convert. */
+ * fp32 per KV arena row (plain stores: one CTA owns a KV block for all heads of
+ * its GQA group); dQ partials are TMA reduce-added into dq_accum (fp32). */
 typedef struct {
   int32_t kv_off, kv_len;       /* arena rows of the KV chunk                       */
   int32_t flags;                /* FCPB_KV_RECV: lives in the receive arena         */
@@ -117,7 +120,8 @@ typedef struct {
 typedef struct {
   int32_t num_q_heads, num_kv_heads, head_dim;
   float softmax_scale;
-  const void* q; const void* dout; const float* lse; const float* delta;
+  const void* q; const void* dout;
+  const float* lse2_t; const float* delta_t; int64_t t_pad;   /* from fcpb_bwd_preprocess */
   int64_t q_tokens;
   const void* k; const void* v; int64_t kv_tokens;
   const void* k_recv; const void* v_recv; int64_t kv_recv_tokens;

@@ -145,16 +145,20 @@ class BlockAttention:
             _check(v_recv, "v_recv", self.kv_shape(True))
 
     # ------------------------------------------------------------------ backward
-    def backward_prepare(self, o, do, stream=None):
-        """delta = rowsum(dO*O) and a zeroed fp32 dQ accumulator."""
+    def backward_prepare(self, o, lse, do, stream=None):
+        """delta = rowsum(dO*O) and lse*log2(e), head-major, plus a zeroed fp32 dQ
+        accumulator.  Returns the tuple the K2 launches consume."""
         H = self.cfg.q_heads
-        delta = torch.empty((self.tokens, H), dtype=torch.float32, device=self.device)
+        t_pad = (self.tokens + 3) // 4 * 4
+        lse2_t = torch.empty((H, t_pad), dtype=torch.float32, device=self.device)
+        delta_t = torch.empty((H, t_pad), dtype=torch.float32, device=self.device)
         dq = torch.empty(self.q_shape(), dtype=torch.float32, device=self.device)
-        native.check(self.lib.fcpb_bwd_preprocess(native.ptr(o), native.ptr(do), native.ptr(delta),
+        native.check(self.lib.fcpb_bwd_preprocess(native.ptr(o), native.ptr(do), native.ptr(lse),
+                                                  native.ptr(lse2_t), native.ptr(delta_t), t_pad,
                                                   native.ptr(dq), self.tokens, H, self.cfg.head_dim,
                                                   self._stream(stream)))
         self.launches += 1
-        return delta, dq
+        return (lse2_t, delta_t, t_pad), dq
 
     def alloc_dkv(self, recv: bool):
         shape = self.kv_shape(recv)
@@ -163,7 +167,7 @@ class BlockAttention:
         return (torch.empty(shape, dtype=torch.float32, device=self.device),
                 torch.empty(shape, dtype=torch.float32, device=self.device))
 
-    def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, lse, delta, do, dq,
+    def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, prep, do, dq,
                         dk, dv, dk_r, dv_r, stream=None):
         for b, kvsegs, qrefs, items in self._bwd:
             if b.recv != recv:
@@ -171,7 +175,9 @@ class BlockAttention:
             a = native.BwdArgs()
             a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
             a.softmax_scale = self.scale
-            a.q, a.dout, a.lse, a.delta = native.ptr(q), native.ptr(do), native.ptr(lse), native.ptr(delta)
+            lse2_t, delta_t, t_pad = prep
+            a.q, a.dout = native.ptr(q), native.ptr(do)
+            a.lse2_t, a.delta_t, a.t_pad = native.ptr(lse2_t), native.ptr(delta_t), t_pad
             a.q_tokens = self.tokens
             a.k, a.v, a.kv_tokens = native.ptr(k), native.ptr(v), self.tokens
             a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
@@ -203,11 +209,11 @@ class BlockAttention:
         received KV, the fp32 (dk_recv, dv_recv) partials owed to their owners."""
         self.validate(q, k, v, k_recv, v_recv)
         _check(do, "do", self.q_shape())
-        delta, dq = self.backward_prepare(o, do, stream)
+        prep, dq = self.backward_prepare(o, lse, do, stream)
         dk, dv = self.alloc_dkv(False)
         dk_r, dv_r = self.alloc_dkv(True)
-        self.backward_launch(True, q, k, v, k_recv, v_recv, lse, delta, do, dq, dk, dv, dk_r, dv_r, stream)
-        self.backward_launch(False, q, k, v, k_recv, v_recv, lse, delta, do, dq, dk, dv, dk_r, dv_r, stream)
+        self.backward_launch(True, q, k, v, k_recv, v_recv, prep, do, dq, dk, dv, dk_r, dv_r, stream)
+        self.backward_launch(False, q, k, v, k_recv, v_recv, prep, do, dq, dk, dv, dk_r, dv_r, stream)
         return (self.to_bf16(dq, stream), self.to_bf16(dk, stream), self.to_bf16(dv, stream),
                 dk_r, dv_r)
 

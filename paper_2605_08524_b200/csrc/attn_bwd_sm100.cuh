@@ -1,20 +1,24 @@
 // K2: varlen block-pair attention backward on sm_100a (tcgen05 + TMEM + TMA).
 //
-// Work item = one 128-row KV block of one KV chunk (local or received) for one
-// KV head.  The CTA loops over every (Q chunk, 128-row Q block, q-head of the
-// GQA group) that attends to it, so dK/dV accumulate in TMEM without atomics and
-// are written exactly once; dQ partials are added into an fp32 accumulator.
+// Work item = one 128-row KV block of one KV chunk (local or received) for one KV
+// head.  The CTA streams every (Q chunk, 64-row Q block, q-head of the GQA group)
+// that attends to it; dK/dV accumulate in TMEM (written once, no atomics) and dQ
+// partials leave through TMA bulk reduce-adds into an fp32 accumulator.
 //
-// Per Q tile j (all matmuls 128x128x128, bf16 in, fp32 accumulate):
-//   S^T  = K  Q_j^T      (SS)   -> TMEM [0,128)
-//   dP^T = V  dO_j^T     (SS)   -> TMEM [128,256)
-//   softmax warps (thread == kv row):  P^T = exp2(S^T*c - lse2[q]),
-//        dS^T = P^T (dP^T - delta[q]);  P^T (bf16) -> TMEM [0,64),
-//        dS^T (bf16) -> TMEM [128,192) and -> smem (MN-major, A of the dQ matmul)
-//   dV  += P^T  dO_j     (TS)   TMEM [256,384)
-//   dK  += dS^T Q_j      (TS)   TMEM [384,512)
-//   dQ_j = dS   K        (SS)   -> TMEM [128,256), drained with fp32 reductions
-// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 softmax / dQ drain / dK,dV epilogue.
+// Per Q tile j (64 query rows):
+//   S^T  = K  Q_j^T   M128 N64  K128 (SS)  -> TMEM S        (fp32)
+//   dP^T = V  dO_j^T  M128 N64  K128 (SS)  -> TMEM dP
+//   softmax WG (thread == kv row): loads S^T, dP^T rows, frees TMEM at once, then
+//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - delta[q])   -> bf16 smem
+//        (SW128 rows of 64 q, double buffered)
+//   dV  += P^T  dO_j  M128 N128 K64  (SS)  -> TMEM dV
+//   dK  += dS^T Q_j   M128 N128 K64  (SS)  -> TMEM dK
+//   dQ^T = K^T dS^T   M128 N64  K128 (SS, both MN-major) -> TMEM dQ[j&1]
+//   drain WG (thread == head-dim lane): TMEM -> smem [q][d] -> TMA reduce-add.
+// TMEM (512 cols): dV [0,128) dK [128,256) S [256,320) dP [320,384) dQ0 [384,448) dQ1 [448,512)
+// The tensor pipe computes S/dP of tile j+1 while the softmax of tile j runs, and
+// the dQ drain never sits on the matmul critical path.
+// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 softmax, w8-11 dQ drain + dK/dV store.
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -23,34 +27,37 @@ namespace fcpb {
 namespace bwd {
 
 constexpr int kD = 128;
-constexpr int kB = 128;                    // rows per Q tile and per KV tile
-constexpr int kTileBytes = kB * kD * 2;    // 32 KB
-constexpr int kHalfBytes = kTileBytes / 2;
-constexpr int kStages = 2;                 // (Q, dO) double buffer
-constexpr int kThreads = 256;
-constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+constexpr int kBK = 128;                        // kv rows per item
+constexpr int kBQ = 64;                         // q rows per tile
+constexpr int kKVBytes = kBK * kD * 2;          // 32 KB (two 16 KB SW128 panels)
+constexpr int kKVPanel = kKVBytes / 2;
+constexpr int kQBytes = kBQ * kD * 2;           // 16 KB (two 8 KB panels)
+constexpr int kQPanel = kQBytes / 2;
+constexpr int kPBytes = kBK * kBQ * 2;          // 16 KB: 128 kv rows x 64 q (one SW128 panel)
+constexpr int kStages = 2;
+constexpr int kThreads = 384;
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColDP = 320, kColDQ = 384;
 
-struct KvSeg {      // mirrors FcpbBwdKvSeg
-  int32_t kv_off, kv_len, flags, q_begin, q_end, pad_;
-};
-struct QRef {       // mirrors FcpbBwdQRef
-  int32_t q_off, q_len, diag, pad_;
-};
-struct Item {       // mirrors FcpbBwdItem
-  int32_t kvseg, nblock;
-};
+struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
+struct QRef { int32_t q_off, q_len, diag, pad_; };
+struct Item { int32_t kvseg, nblock; };
 
 struct Smem {
-  uint8_t k[kTileBytes];
-  uint8_t v[kTileBytes];
-  uint8_t q[kStages][kTileBytes];
-  uint8_t dout[kStages][kTileBytes];
-  uint8_t ds[kTileBytes];          // dS as the MN-major A operand of dQ = dS K
-  float lse2[kB];                  // lse * log2(e) of the current Q tile
-  float delta[kB];
+  uint8_t k[kKVBytes];
+  uint8_t v[kKVBytes];
+  uint8_t q[kStages][kQBytes];
+  uint8_t dout[kStages][kQBytes];
+  uint8_t p[2][kPBytes];            // P^T  (A of dV)
+  uint8_t ds[2][kPBytes];           // dS^T (A of dK, B of dQ^T)
+  float dq_stage[kBQ * kD];         // 32 KB, [q][d] fp32, source of the TMA reduce
+  float lse2[kStages][kBQ];         // lse * log2(e), per q column
+  float delta[kStages][kBQ];
   uint64_t kv_full, kv_empty;
   uint64_t qd_full[kStages], qd_empty[kStages];
-  uint64_t s_full, p_full, dq_full, dq_empty, acc_full, acc_empty;
+  uint64_t sdp_full, sdp_free;
+  uint64_t pds_full[2], pds_free[2];
+  uint64_t dq_full[2], dq_free[2];
+  uint64_t acc_full, acc_free;
   uint32_t tmem_base;
 };
 
@@ -62,31 +69,62 @@ struct Params {
   int32_t num_q_heads, num_kv_heads;
   float scale;            // softmax scale
   float scale_log2;       // scale * log2(e)
-  const float* lse;       // [Tq, Hq] natural log
-  const float* delta;     // [Tq, Hq]
-  float* dq;              // [Tq, Hq, D] fp32 accumulate
+  const float* lse2_t;    // [Hq, t_pad] lse * log2(e)
+  const float* delta_t;   // [Hq, t_pad]
+  int64_t t_pad;
+  int32_t q_tokens;
   float* dk;              // local  [Tkv, Hkv, D] fp32
   float* dv;
   float* dk_recv;         // recv   [Tr, Hkv, D] fp32
   float* dv_recv;
 };
 
-// Q blocks of `qr` that see KV block `nb`: causal diagonal -> mb >= nb.
-FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? nb : 0; }
-FCPB_DEV int q_num_blocks(const QRef& qr) { return (qr.q_len + kB - 1) / kB; }
+// Q blocks (64 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= 2nb.
+FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? 2 * nb : 0; }
+FCPB_DEV int q_num_blocks(const QRef& qr) { return (qr.q_len + kBQ - 1) / kBQ; }
 
-FCPB_DEV void red_add_v4(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
-               ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+FCPB_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem_src, int32_t c0, int32_t c1,
+                                int32_t c2) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+      " [%0, {%2, %3, %4}], [%1];"
+      ::"l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// 4-byte async copy with zero fill when !valid; completion tracked by an mbarrier.
+FCPB_DEV void cp_async_4(void* smem_dst, const float* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+               ::"r"(smem_u32(smem_dst)), "l"(src), "r"(valid ? 4 : 0) : "memory");
+}
+FCPB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+FCPB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+FCPB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+FCPB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// 32 lanes x 64 columns (two x32 loads), waits for completion.
+FCPB_DEV void tmem_ld64(uint32_t taddr, float (&out)[64]) {
+  uint32_t a[32], b[32];
+  tmem_ld32(taddr, a);
+  tmem_ld32(taddr + 32, b);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    out[i] = __uint_as_float(a[i]);
+    out[32 + i] = __uint_as_float(b[i]);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
-                const __grid_constant__ CUtensorMap tm_do,
-                const __grid_constant__ CUtensorMap tm_k,
+attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D], box (64,1,64)
+                const __grid_constant__ CUtensorMap tm_do,     // bf16 [Tq,Hq,D], box (64,1,64)
+                const __grid_constant__ CUtensorMap tm_k,      // bf16 [Tkv,Hkv,D], box (64,1,128)
                 const __grid_constant__ CUtensorMap tm_v,
                 const __grid_constant__ CUtensorMap tm_k_recv,
                 const __grid_constant__ CUtensorMap tm_v_recv,
+                const __grid_constant__ CUtensorMap tm_dq,     // fp32 [Tq,Hq,D], box (128,1,64)
                 const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(
@@ -102,20 +140,25 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_k_recv);
     tma_prefetch_desc(&tm_v_recv);
+    tma_prefetch_desc(&tm_dq);
   }
   if (warp == 1 && elect_one()) {
     mbar_init(&sm.kv_full, 1);
     mbar_init(&sm.kv_empty, 1);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.qd_full[s], 1);
+      mbar_init(&sm.qd_full[s], 1 + 32);   // TMA expect_tx arrive + 32 cp.async arrives
       mbar_init(&sm.qd_empty[s], 1);
     }
-    mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.p_full, 128);
-    mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_empty, 128);
+    mbar_init(&sm.sdp_full, 1);
+    mbar_init(&sm.sdp_free, 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.pds_full[b], 128);
+      mbar_init(&sm.pds_free[b], 1);
+      mbar_init(&sm.dq_full[b], 1);
+      mbar_init(&sm.dq_free[b], 128);
+    }
     mbar_init(&sm.acc_full, 1);
-    mbar_init(&sm.acc_empty, 128);
+    mbar_init(&sm.acc_free, 128);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -125,117 +168,151 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
   const uint32_t tmem = sm.tmem_base;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
-      uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
-        const Item it = p.items[g / p.num_kv_heads];
-        const int kvh = g % p.num_kv_heads;
-        const KvSeg ks = p.kvsegs[it.kvseg];
-        const bool recv = ks.flags & FCPB_KV_RECV;
-        const int krow = ks.kv_off + it.nblock * kB;
-        mbar_wait(&sm.kv_empty, kv_phase ^ 1);
-        kv_phase ^= 1;
-        mbar_arrive_expect_tx(&sm.kv_full, 2 * kTileBytes);
+    // ------------------------------------------------------------ TMA producer (all lanes:
+    // lane 0 issues the TMA tiles, every lane copies 2 lse2 + 2 delta values with cp.async)
+    const uint32_t lane = lane_id();
+    const uint64_t keep = policy_evict_last();
+    uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const Item it = p.items[g / p.num_kv_heads];
+      const int kvh = g % p.num_kv_heads;
+      const KvSeg ks = p.kvsegs[it.kvseg];
+      const bool recv = ks.flags & FCPB_KV_RECV;
+      const int krow = ks.kv_off + it.nblock * kBK;
+      mbar_wait(&sm.kv_empty, kv_phase ^ 1);
+      kv_phase ^= 1;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&sm.kv_full, 2 * kKVBytes);
         for (int half = 0; half < 2; ++half) {
-          tma_load_3d(&sm.k[half * kHalfBytes], recv ? &tm_k_recv : &tm_k, &sm.kv_full,
-                      half * 64, kvh, krow);
-          tma_load_3d(&sm.v[half * kHalfBytes], recv ? &tm_v_recv : &tm_v, &sm.kv_full,
-                      half * 64, kvh, krow);
+          tma_load_3d(&sm.k[half * kKVPanel], recv ? &tm_k_recv : &tm_k, &sm.kv_full, half * 64,
+                      kvh, krow);
+          tma_load_3d(&sm.v[half * kKVPanel], recv ? &tm_v_recv : &tm_v, &sm.kv_full, half * 64,
+                      kvh, krow);
         }
-        for (int r = ks.q_begin; r < ks.q_end; ++r) {
-          const QRef qr = p.qrefs[r];
-          for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
-            for (int gq = 0; gq < group; ++gq) {
-              const int h = kvh * group + gq;
-              mbar_wait(&sm.qd_empty[stage], stage_phase ^ 1);
-              mbar_arrive_expect_tx(&sm.qd_full[stage], 2 * kTileBytes);
-              const int qrow = qr.q_off + mb * kB;
+      }
+      for (int r = ks.q_begin; r < ks.q_end; ++r) {
+        const QRef qr = p.qrefs[r];
+        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
+          const int qrow = qr.q_off + mb * kBQ;
+          for (int gq = 0; gq < group; ++gq) {
+            const int h = kvh * group + gq;
+            mbar_wait(&sm.qd_empty[stage], stage_phase ^ 1);
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&sm.qd_full[stage], 2 * kQBytes);
               for (int half = 0; half < 2; ++half) {
-                tma_load_3d_hint(&sm.q[stage][half * kHalfBytes], &tm_q, &sm.qd_full[stage],
+                tma_load_3d_hint(&sm.q[stage][half * kQPanel], &tm_q, &sm.qd_full[stage],
                                  half * 64, h, qrow, keep);
-                tma_load_3d_hint(&sm.dout[stage][half * kHalfBytes], &tm_do, &sm.qd_full[stage],
+                tma_load_3d_hint(&sm.dout[stage][half * kQPanel], &tm_do, &sm.qd_full[stage],
                                  half * 64, h, qrow, keep);
               }
-              if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
             }
+            const float* lsrc = p.lse2_t + static_cast<int64_t>(h) * p.t_pad + qrow;
+            const float* dsrc = p.delta_t + static_cast<int64_t>(h) * p.t_pad + qrow;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int i = lane + 32 * u;
+              const bool ok = qrow + i < p.q_tokens;
+              cp_async_4(&sm.lse2[stage][i], ok ? lsrc + i : p.lse2_t, ok);
+              cp_async_4(&sm.delta[stage][i], ok ? dsrc + i : p.delta_t, ok);
+            }
+            cp_async_arrive_noinc(&sm.qd_full[stage]);
+            if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t id_kmaj = idesc_bf16_f32(kB, kB, false, false);  // S^T, dP^T
-    const uint32_t id_bmn = idesc_bf16_f32(kB, kD, false, true);    // dV, dK (TS)
-    const uint32_t id_dq = idesc_bf16_f32(kB, kD, true, true);      // dQ: A=dS MN-major
-    const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v), a_ds = smem_u32(sm.ds);
+    const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);  // S^T, dP^T
+    const uint32_t id_acc = idesc_bf16_f32(kBK, kD, false, true);    // dV, dK
+    const uint32_t id_dq = idesc_bf16_f32(kD, kBQ, true, true);      // dQ^T
+    const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v);
     const bool leader = elect_one();
-    uint32_t kv_phase = 0, stage = 0, stage_phase = 0, p_phase = 0, dqe_phase = 0,
-             acce_phase = 0;
+    uint32_t kv_phase = 0, stage = 0, stage_phase = 0, sdpf_phase = 0, acc_phase = 0;
+    uint32_t pds_phase[2] = {0, 0}, dqf_phase[2] = {0, 0};
+    uint32_t tile = 0;   // running Q-tile counter (selects P/dS and dQ buffers)
+
+    auto issue_sdp = [&](uint32_t st) {
+      const uint32_t a_q = smem_u32(sm.q[st]), a_do = smem_u32(sm.dout[st]);
+      if (leader) {
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32;
+          mma_ss(tmem + kColS, smem_desc_sw128(a_k + oa, 16, 1024),
+                 smem_desc_sw128(a_q + ob, 16, 1024), id_sdp, kk > 0);
+        }
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32;
+          mma_ss(tmem + kColDP, smem_desc_sw128(a_v + oa, 16, 1024),
+                 smem_desc_sw128(a_do + ob, 16, 1024), id_sdp, kk > 0);
+        }
+        mma_commit(&sm.sdp_full);
+      }
+      __syncwarp();
+    };
+
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const Item it = p.items[g / p.num_kv_heads];
       const KvSeg ks = p.kvsegs[it.kvseg];
-      mbar_wait(&sm.kv_full, kv_phase);
-      kv_phase ^= 1;
-      mbar_wait(&sm.acc_empty, acce_phase ^ 1);
-      acce_phase ^= 1;
-      tc_fence_after();
-      int j = 0;
+      int n = 0;
       for (int r = ks.q_begin; r < ks.q_end; ++r) {
         const QRef qr = p.qrefs[r];
-        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
-          for (int gq = 0; gq < group; ++gq, ++j) {
-            mbar_wait(&sm.qd_full[stage], stage_phase);
-            tc_fence_after();
-            const uint32_t a_q = smem_u32(sm.q[stage]), a_do = smem_u32(sm.dout[stage]);
-            if (leader) {
-#pragma unroll
-              for (int kk = 0; kk < kD / 16; ++kk) {
-                const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                mma_ss(tmem + kColS, smem_desc_sw128(a_k + off, 16, 1024),
-                       smem_desc_sw128(a_q + off, 16, 1024), id_kmaj, kk > 0);
-              }
-            }
-            __syncwarp();
-            mbar_wait(&sm.dq_empty, dqe_phase ^ 1);
-            dqe_phase ^= 1;
-            tc_fence_after();
-            if (leader) {
-#pragma unroll
-              for (int kk = 0; kk < kD / 16; ++kk) {
-                const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                mma_ss(tmem + kColDP, smem_desc_sw128(a_v + off, 16, 1024),
-                       smem_desc_sw128(a_do + off, 16, 1024), id_kmaj, kk > 0);
-              }
-              mma_commit(&sm.s_full);
-            }
-            __syncwarp();
-            mbar_wait(&sm.p_full, p_phase);
-            p_phase ^= 1;
-            tc_fence_after();
-            if (leader) {
-#pragma unroll
-              for (int kk = 0; kk < kB / 16; ++kk)   // dV += P^T dO
-                mma_ts(tmem + kColDV, tmem + kColS + kk * 8,
-                       smem_desc_sw128(a_do + kk * 2048, kHalfBytes, 1024), id_bmn,
-                       (j > 0 || kk > 0));
-#pragma unroll
-              for (int kk = 0; kk < kB / 16; ++kk)   // dK += dS^T Q
-                mma_ts(tmem + kColDK, tmem + kColDP + kk * 8,
-                       smem_desc_sw128(a_q + kk * 2048, kHalfBytes, 1024), id_bmn,
-                       (j > 0 || kk > 0));
-#pragma unroll
-              for (int kk = 0; kk < kB / 16; ++kk)   // dQ = dS K
-                mma_ss(tmem + kColDP, smem_desc_sw128(a_ds + kk * 2048, kHalfBytes, 1024),
-                       smem_desc_sw128(a_k + kk * 2048, kHalfBytes, 1024), id_dq, kk > 0);
-              mma_commit(&sm.dq_full);
-              mma_commit(&sm.qd_empty[stage]);
-            }
-            __syncwarp();
-            if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
-          }
+        n += (q_num_blocks(qr) - q_first_block(qr, it.nblock)) * group;
+      }
+      mbar_wait(&sm.kv_full, kv_phase);
+      kv_phase ^= 1;
+      // tile 0 of this item: S/dP region must have been read by the previous softmax
+      mbar_wait(&sm.qd_full[stage], stage_phase);
+      mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);
+      sdpf_phase ^= 1;
+      tc_fence_after();
+      issue_sdp(stage);
+      uint32_t cur_stage = stage;
+      if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
+      for (int j = 0; j < n; ++j, ++tile) {
+        const uint32_t b = tile & 1;
+        const uint32_t st_j = cur_stage;
+        if (j + 1 < n) {
+          mbar_wait(&sm.qd_full[stage], stage_phase);
+          mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);   // softmax(j) has S/dP(j) in registers
+          sdpf_phase ^= 1;
+          tc_fence_after();
+          issue_sdp(stage);
+          cur_stage = stage;
+          if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
         }
+        mbar_wait(&sm.pds_full[b], pds_phase[b]);
+        pds_phase[b] ^= 1;
+        if (j == 0) {
+          mbar_wait(&sm.acc_free, acc_phase ^ 1);
+          acc_phase ^= 1;
+        }
+        mbar_wait(&sm.dq_free[b], dqf_phase[b] ^ 1);
+        dqf_phase[b] ^= 1;
+        tc_fence_after();
+        if (leader) {
+          const uint32_t a_p = smem_u32(sm.p[b]), a_ds = smem_u32(sm.ds[b]);
+          const uint32_t a_q = smem_u32(sm.q[st_j]), a_do = smem_u32(sm.dout[st_j]);
+#pragma unroll
+          for (int kk = 0; kk < kBQ / 16; ++kk)     // dV += P^T dO
+            mma_ss(tmem + kColDV, smem_desc_sw128(a_p + kk * 32, 16, 1024),
+                   smem_desc_sw128(a_do + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
+#pragma unroll
+          for (int kk = 0; kk < kBQ / 16; ++kk)     // dK += dS^T Q
+            mma_ss(tmem + kColDK, smem_desc_sw128(a_ds + kk * 32, 16, 1024),
+                   smem_desc_sw128(a_q + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
+          mma_commit(&sm.qd_empty[st_j]);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)     // dQ^T = K^T dS^T
+            mma_ss(tmem + kColDQ + b * 64, smem_desc_sw128(a_k + kk * 2048, kKVPanel, 1024),
+                   smem_desc_sw128(a_ds + kk * 2048, kPBytes, 1024), id_dq, kk > 0);
+          mma_commit(&sm.dq_full[b]);
+          mma_commit(&sm.pds_free[b]);
+        }
+        __syncwarp();
       }
       if (leader) {
         mma_commit(&sm.acc_full);
@@ -243,106 +320,116 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
       __syncwarp();
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax / drains
-    const int tid = threadIdx.x - 128;            // 0..127 == TMEM lane
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ softmax (thread == kv row)
+    const int tid = threadIdx.x - 128;
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_bits + kColS;
     const uint32_t t_dp = tmem + lane_bits + kColDP;
-    const uint32_t ds_row = smem_u32(sm.ds) + (tid >> 3) * 1024 + (tid & 7) * 128;
+    const uint32_t row_off = (tid >> 3) * 1024 + (tid & 7) * 128;
     const float sl2 = p.scale_log2;
-    constexpr float kLog2e = 1.4426950408889634f;
-    uint32_t s_phase = 0, dq_phase = 0, acc_phase = 0;
+    uint32_t sdp_phase = 0, stage = 0, stage_phase = 0, tile = 0;
+    uint32_t pfree_phase[2] = {0, 0};
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      const Item it = p.items[g / p.num_kv_heads];
+      const KvSeg ks = p.kvsegs[it.kvseg];
+      const int kv_row = it.nblock * kBK + tid;
+      const bool kv_live = kv_row < ks.kv_len;
+      const bool kv_full_tile = it.nblock * kBK + kBK <= ks.kv_len;
+      for (int r = ks.q_begin; r < ks.q_end; ++r) {
+        const QRef qr = p.qrefs[r];
+        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
+          const int q_valid = qr.q_len - mb * kBQ;
+          // diagonal: column c (q = 64mb + c) sees kv row 128nb + tid iff c >= shift
+          const int shift0 = (it.nblock * kBK - mb * kBQ);
+          const bool plain = kv_full_tile && q_valid >= kBQ && (!qr.diag || shift0 + kBK - 1 <= 0);
+          const int shift = qr.diag ? shift0 + tid : -1;
+          for (int gq = 0; gq < group; ++gq, ++tile) {
+            const uint32_t b = tile & 1;
+            mbar_wait(&sm.sdp_full, sdp_phase);
+            sdp_phase ^= 1;
+            mbar_wait(&sm.qd_full[stage], stage_phase);   // lse2 / delta of this tile landed
+            tc_fence_after();
+            float s[kBQ], dp[kBQ];
+            tmem_ld64(t_s, s);
+            tmem_ld64(t_dp, dp);
+            tc_fence_before();
+            mbar_arrive(&sm.sdp_free);
+            mbar_wait(&sm.pds_free[b], pfree_phase[b] ^ 1);
+            pfree_phase[b] ^= 1;
+            const float* l2 = sm.lse2[stage];
+            const float* dl = sm.delta[stage];
+            const uint32_t pb = smem_u32(sm.p[b]) + row_off;
+            const uint32_t db = smem_u32(sm.ds[b]) + row_off;
+#pragma unroll
+            for (int c8 = 0; c8 < kBQ / 8; ++c8) {
+              const float4 la = *reinterpret_cast<const float4*>(l2 + c8 * 8);
+              const float4 lb = *reinterpret_cast<const float4*>(l2 + c8 * 8 + 4);
+              const float4 da = *reinterpret_cast<const float4*>(dl + c8 * 8);
+              const float4 dbv = *reinterpret_cast<const float4*>(dl + c8 * 8 + 4);
+              const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+              const float dv[8] = {da.x, da.y, da.z, da.w, dbv.x, dbv.y, dbv.z, dbv.w};
+              float pp[8], dd[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int col = c8 * 8 + u;
+                float pv = ex2(fmaf(s[col], sl2, -lv[u]));
+                if (!plain) {
+                  const bool vis = kv_live && col < q_valid && col >= shift;
+                  pv = vis ? pv : 0.f;
+                }
+                pp[u] = pv;
+                dd[u] = pv * (dp[col] - dv[u]);
+              }
+              const uint32_t chunk = (c8 ^ (tid & 7)) * 16;
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                           ::"r"(pb + chunk), "r"(pack_bf16(pp[0], pp[1])), "r"(pack_bf16(pp[2], pp[3])),
+                             "r"(pack_bf16(pp[4], pp[5])), "r"(pack_bf16(pp[6], pp[7])) : "memory");
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
+                           ::"r"(db + chunk), "r"(pack_bf16(dd[0], dd[1])), "r"(pack_bf16(dd[2], dd[3])),
+                             "r"(pack_bf16(dd[4], dd[5])), "r"(pack_bf16(dd[6], dd[7])) : "memory");
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&sm.pds_full[b]);
+            if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ dQ drain + dK/dV epilogue
+    const int tid = threadIdx.x - 256;            // head-dim lane for dQ^T, kv row for dK/dV
+    const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const bool leader = (tid == 0);
+    uint32_t tile = 0, acc_phase = 0;
+    uint32_t dq_phase[2] = {0, 0};
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const Item it = p.items[g / p.num_kv_heads];
       const int kvh = g % p.num_kv_heads;
       const KvSeg ks = p.kvsegs[it.kvseg];
-      const int kv_row = it.nblock * kB + tid;              // row inside the KV chunk
-      const bool kv_live = kv_row < ks.kv_len;
       for (int r = ks.q_begin; r < ks.q_end; ++r) {
         const QRef qr = p.qrefs[r];
         for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
-          for (int gq = 0; gq < group; ++gq) {
+          for (int gq = 0; gq < group; ++gq, ++tile) {
+            const uint32_t b = tile & 1;
             const int h = kvh * group + gq;
-            // per-column statistics of this Q tile
-            named_bar_sync(1, 128);
-            {
-              const int q = mb * kB + tid;
-              float l2 = 0.f, dl = 0.f;
-              if (q < qr.q_len) {
-                const size_t idx = static_cast<size_t>(qr.q_off + q) * p.num_q_heads + h;
-                l2 = p.lse[idx] * kLog2e;
-                dl = p.delta[idx];
-              }
-              sm.lse2[tid] = l2;
-              sm.delta[tid] = dl;
-            }
-            named_bar_sync(1, 128);
-            mbar_wait(&sm.s_full, s_phase);
-            s_phase ^= 1;
+            mbar_wait(&sm.dq_full[b], dq_phase[b]);
+            dq_phase[b] ^= 1;
             tc_fence_after();
-            const int q_valid = qr.q_len - mb * kB;            // columns < q_valid are live
-            // diagonal: column c (q row mb*128+c) sees kv row nb*128+tid iff q >= kv
-            const int diag_shift = qr.diag ? (it.nblock - mb) * kB + tid : -1;
+            float v[kBQ];
+            tmem_ld64(tmem + lane_bits + kColDQ + b * 64, v);
+            tc_fence_before();
+            mbar_arrive(&sm.dq_free[b]);
+            if (leader) bulk_wait_read0();          // previous reduce has read dq_stage
+            named_bar_sync(2, 128);
 #pragma unroll
-            for (int c = 0; c < kB / 32; ++c) {
-              uint32_t sv[32], dv[32];
-              tmem_ld32(t_s + c * 32, sv);
-              tmem_ld32(t_dp + c * 32, dv);
-              tmem_wait_ld();
-              uint32_t pk[16], dk[16];
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                float pp[2], dd[2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                  const int col = c * 32 + i + u;
-                  const bool vis = kv_live && col < q_valid && col >= diag_shift;
-                  const float pv = vis ? ex2(fmaf(__uint_as_float(sv[i + u]), sl2, -sm.lse2[col])) : 0.f;
-                  pp[u] = pv;
-                  dd[u] = pv * (__uint_as_float(dv[i + u]) - sm.delta[col]);
-                }
-                pk[i / 2] = pack_bf16(pp[0], pp[1]);
-                dk[i / 2] = pack_bf16(dd[0], dd[1]);
-              }
-              tmem_st16(t_s + c * 16, pk);
-              tmem_st16(t_dp + c * 16, dk);
-              // dS^T row `tid`, q columns [32c, 32c+32): 64 bytes into the 128-B row of
-              // M-atom (c>>1), 16-B chunks XOR-swizzled by (tid & 7).
-              const uint32_t atom = ds_row + (c >> 1) * (kB / 8) * 1024;
-#pragma unroll
-              for (int ch = 0; ch < 4; ++ch) {
-                const uint32_t chunk = ((c & 1) * 4 + ch) ^ (tid & 7);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
-                             ::"r"(atom + chunk * 16), "r"(dk[ch * 4]), "r"(dk[ch * 4 + 1]),
-                               "r"(dk[ch * 4 + 2]), "r"(dk[ch * 4 + 3]) : "memory");
-              }
-            }
-            tmem_wait_st();
+            for (int q = 0; q < kBQ; ++q) sm.dq_stage[q * kD + tid] = v[q] * p.scale;
             fence_proxy_async_smem();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full);
-            // ---- drain dQ_j (thread == q row of the tile)
-            mbar_wait(&sm.dq_full, dq_phase);
-            dq_phase ^= 1;
-            tc_fence_after();
-            const bool q_live = tid < q_valid;
-            float* dst = p.dq + (static_cast<size_t>(qr.q_off + mb * kB + tid) * p.num_q_heads + h) * kD;
-#pragma unroll
-            for (int c = 0; c < kD / 32; ++c) {
-              uint32_t v[32];
-              tmem_ld32(t_dp + c * 32, v);
-              tmem_wait_ld();
-              if (q_live) {
-#pragma unroll
-                for (int i = 0; i < 32; i += 4)
-                  red_add_v4(dst + c * 32 + i, __uint_as_float(v[i]) * p.scale,
-                             __uint_as_float(v[i + 1]) * p.scale, __uint_as_float(v[i + 2]) * p.scale,
-                             __uint_as_float(v[i + 3]) * p.scale);
-              }
+            named_bar_sync(2, 128);
+            if (leader) {
+              tma_reduce_add_3d(&tm_dq, sm.dq_stage, 0, h, qr.q_off + mb * kBQ);
+              bulk_commit();
             }
-            tc_fence_before();
-            mbar_arrive(&sm.dq_empty);
           }
         }
       }
@@ -350,15 +437,17 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&sm.acc_full, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
+      const int kv_row = it.nblock * kBK + tid;
+      const bool kv_live = kv_row < ks.kv_len;
       const bool recv = ks.flags & FCPB_KV_RECV;
       float* dkb = recv ? p.dk_recv : p.dk;
       float* dvb = recv ? p.dv_recv : p.dv;
       const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD;
 #pragma unroll
       for (int c = 0; c < kD / 32; ++c) {
-        uint32_t a[32], b[32];
+        uint32_t a[32], bb[32];
         tmem_ld32(tmem + lane_bits + kColDK + c * 32, a);
-        tmem_ld32(tmem + lane_bits + kColDV + c * 32, b);
+        tmem_ld32(tmem + lane_bits + kColDV + c * 32, bb);
         tmem_wait_ld();
         if (kv_live) {
           float4* k4 = reinterpret_cast<float4*>(dkb + row + c * 32);
@@ -367,14 +456,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           for (int i = 0; i < 32; i += 4) {
             k4[i / 4] = make_float4(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale,
                                     __uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
-            v4[i / 4] = make_float4(__uint_as_float(b[i]), __uint_as_float(b[i + 1]),
-                                    __uint_as_float(b[i + 2]), __uint_as_float(b[i + 3]));
+            v4[i / 4] = make_float4(__uint_as_float(bb[i]), __uint_as_float(bb[i + 1]),
+                                    __uint_as_float(bb[i + 2]), __uint_as_float(bb[i + 3]));
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(&sm.acc_empty);
+      mbar_arrive(&sm.acc_free);
     }
+    if (leader) bulk_wait0();
   }
 
   tc_fence_before();

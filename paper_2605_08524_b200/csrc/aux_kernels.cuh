@@ -48,11 +48,15 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
   if (lane == 0) a.lse[out] = wsum > 0.f ? mu + __logf(wsum) : -INFINITY;
 }
 
-// delta[row] = <dO[row,:], O[row,:]> and dq_accum[row,:] = 0; one warp per (token, head).
+// delta = <dO[row,:], O[row,:]>, lse2 = lse*log2(e) (both head-major [H, t_pad]) and
+// dq_accum[row,:] = 0; one warp per (token, head) row.
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                               const __nv_bfloat16* __restrict__ dout,
-                                                              float* __restrict__ delta,
-                                                              float* __restrict__ dq, int64_t rows) {
+                                                              const float* __restrict__ lse,
+                                                              float* __restrict__ lse2_t,
+                                                              float* __restrict__ delta_t,
+                                                              int64_t t_pad, float* __restrict__ dq,
+                                                              int64_t rows, int heads) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= rows) return;
@@ -70,7 +74,11 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) delta[w] = s;
+  if (lane == 0) {
+    const int64_t t = w / heads, h = w % heads;
+    delta_t[h * t_pad + t] = s;
+    lse2_t[h * t_pad + t] = lse[w] * 1.4426950408889634f;
+  }
   if (dq) reinterpret_cast<float4*>(dq + w * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 

@@ -49,20 +49,23 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// Token-major [T, H, 128] bf16 -> 3-D map (d, head, token), box (64, 1, 128), SW128.
-int make_map(CUtensorMap* m, const void* base, int64_t tokens, int heads, int d) {
+// Token-major [T, H, d] tensor -> 3-D map (d, head, token) with box (box_d, 1, box_rows).
+int make_map(CUtensorMap* m, const void* base, int64_t tokens, int heads, int d, int box_rows,
+             bool fp32 = false, int box_d = 64, bool swizzle = true) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(FCPB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(base) % 16)
     return fail(FCPB_ERR_INVALID, "tensor base must be 16-byte aligned");
+  const int esz = fp32 ? 4 : 2;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(heads),
                               static_cast<cuuint64_t>(tokens > 0 ? tokens : 1)};
-  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2,
-                                 static_cast<cuuint64_t>(heads) * d * 2};
-  const cuuint32_t box[3] = {64, 1, 128};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * esz,
+                                 static_cast<cuuint64_t>(heads) * d * esz};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_d), 1, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FCPB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return FCPB_OK;
@@ -105,15 +108,15 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   if (a->num_items <= 0) return FCPB_OK;
   CUtensorMap tq, tk, tv, tkr, tvr;
   int rc;
-  if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128))) return rc;
-  if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128))) return rc;
-  if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128, 128))) return rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128, 128))) return rc;
+  if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128, 128))) return rc;
   const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
   if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
-                     a->num_kv_heads, 128)))
+                     a->num_kv_heads, 128, 128)))
     return rc;
   if ((rc = make_map(&tvr, has_recv ? a->v_recv : a->v, has_recv ? a->kv_recv_tokens : a->kv_tokens,
-                     a->num_kv_heads, 128)))
+                     a->num_kv_heads, 128, 128)))
     return rc;
   fcpb::fwd::Params p;
   p.segs = a->segments;
@@ -149,31 +152,37 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
     return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
   if (a->num_items <= 0) return FCPB_OK;
-  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
+  CUtensorMap tq, tdo, tk, tv, tkr, tvr, tdq;
   int rc;
-  if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128))) return rc;
-  if ((rc = make_map(&tdo, a->dout, a->q_tokens, a->num_q_heads, 128))) return rc;
-  if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128))) return rc;
-  if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128))) return rc;
+  const int H = a->num_q_heads, Hk = a->num_kv_heads;
+  if ((rc = make_map(&tq, a->q, a->q_tokens, H, 128, fcpb::bwd::kBQ))) return rc;
+  if ((rc = make_map(&tdo, a->dout, a->q_tokens, H, 128, fcpb::bwd::kBQ))) return rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, Hk, 128, fcpb::bwd::kBK))) return rc;
+  if ((rc = make_map(&tv, a->v, a->kv_tokens, Hk, 128, fcpb::bwd::kBK))) return rc;
   const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
   if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
-                     a->num_kv_heads, 128)))
+                     Hk, 128, fcpb::bwd::kBK)))
     return rc;
   if ((rc = make_map(&tvr, has_recv ? a->v_recv : a->v, has_recv ? a->kv_recv_tokens : a->kv_tokens,
-                     a->num_kv_heads, 128)))
+                     Hk, 128, fcpb::bwd::kBK)))
+    return rc;
+  if (a->t_pad < a->q_tokens || !a->lse2_t || !a->delta_t)
+    return fail(FCPB_ERR_INVALID, "lse2_t/delta_t/t_pad missing (run fcpb_bwd_preprocess)");
+  if ((rc = make_map(&tdq, a->dq_accum, a->q_tokens, H, 128, fcpb::bwd::kBQ, true, 128, false)))
     return rc;
   fcpb::bwd::Params p;
   p.kvsegs = reinterpret_cast<const fcpb::bwd::KvSeg*>(a->kvsegs);
   p.qrefs = reinterpret_cast<const fcpb::bwd::QRef*>(a->qrefs);
   p.items = reinterpret_cast<const fcpb::bwd::Item*>(a->items);
   p.num_items = a->num_items;
-  p.num_q_heads = a->num_q_heads;
-  p.num_kv_heads = a->num_kv_heads;
+  p.num_q_heads = H;
+  p.num_kv_heads = Hk;
   p.scale = a->softmax_scale;
   p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
-  p.lse = a->lse;
-  p.delta = a->delta;
-  p.dq = a->dq_accum;
+  p.lse2_t = a->lse2_t;
+  p.delta_t = a->delta_t;
+  p.t_pad = a->t_pad;
+  p.q_tokens = static_cast<int32_t>(a->q_tokens);
   p.dk = a->dk_accum;
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
@@ -184,11 +193,11 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem));
     attr = true;
   }
-  const int total = a->num_items * a->num_kv_heads;
+  const int total = a->num_items * Hk;
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
   fcpb::bwd::attn_bwd_kernel<<<grid, fcpb::bwd::kThreads, kBwdSmem,
-                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, p);
+                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, tdq, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
@@ -206,17 +215,19 @@ int fcpb_lse_merge(const FcpbMergeArgs* a, void* stream) {
   return FCPB_OK;
 }
 
-int fcpb_bwd_preprocess(const void* o, const void* dout, float* delta, float* dq_accum,
-                        int64_t tokens, int32_t num_q_heads, int32_t head_dim, void* stream) {
+int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse, float* lse2_t,
+                        float* delta_t, int64_t t_pad, float* dq_accum, int64_t tokens,
+                        int32_t num_q_heads, int32_t head_dim, void* stream) {
   if (head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", head_dim);
+  if (t_pad < tokens || t_pad % 4) return fail(FCPB_ERR_INVALID, "bad t_pad %lld", (long long)t_pad);
   const int64_t rows = tokens * num_q_heads;
   if (rows == 0) return FCPB_OK;
   const int block = 256;
   const int64_t grid = (rows * 32 + block - 1) / block;
   fcpb::aux::bwd_preprocess_kernel<<<static_cast<unsigned>(grid), block, 0,
                                      static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), delta,
-      dq_accum, rows);
+      static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, lse2_t,
+      delta_t, t_pad, dq_accum, rows, num_q_heads);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }

@@ -101,10 +101,10 @@ class FcpExecutor:
     def backward(self, q, k, v, o, lse, do):
         op = self.op
         cur = torch.cuda.current_stream(self.device)
-        delta, dq = op.backward_prepare(o, do, cur)
+        prep, dq = op.backward_prepare(o, lse, do, cur)
         dk, dv = op.alloc_dkv(False)
         dk_r, dv_r = op.alloc_dkv(True)
-        args = (q, k, v, self.k_recv, self.v_recv, lse, delta, do, dq, dk, dv, dk_r, dv_r, cur)
+        args = (q, k, v, self.k_recv, self.v_recv, prep, do, dq, dk, dv, dk_r, dv_r, cur)
         staged = None
         if self.world > 1 and self.stages:
             op.backward_launch(True, *args)

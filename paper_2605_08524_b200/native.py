@@ -42,7 +42,8 @@ class MergeArgs(ctypes.Structure):
 class BwdArgs(ctypes.Structure):
     _fields_ = [("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
                 ("softmax_scale", c_f32),
-                ("q", c_vp), ("dout", c_vp), ("lse", c_vp), ("delta", c_vp), ("q_tokens", c_i64),
+                ("q", c_vp), ("dout", c_vp),
+                ("lse2_t", c_vp), ("delta_t", c_vp), ("t_pad", c_i64), ("q_tokens", c_i64),
                 ("k", c_vp), ("v", c_vp), ("kv_tokens", c_i64),
                 ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
                 ("dq_accum", c_vp), ("dk_accum", c_vp), ("dv_accum", c_vp),
@@ -72,7 +73,8 @@ def load(path: str | None = None):
     lib.fcpb_attn_fwd.argtypes = [ctypes.POINTER(FwdArgs), c_vp]
     lib.fcpb_attn_bwd.argtypes = [ctypes.POINTER(BwdArgs), c_vp]
     lib.fcpb_lse_merge.argtypes = [ctypes.POINTER(MergeArgs), c_vp]
-    lib.fcpb_bwd_preprocess.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]
+    lib.fcpb_bwd_preprocess.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32,
+                                         c_i32, c_vp]
     lib.fcpb_f32_to_bf16.argtypes = [c_vp, c_vp, c_i64, c_vp]
     lib.fcpb_dkv_reduce.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]
     lib.fcpb_last_error.restype = ctypes.c_char_p

@@ -87,12 +87,12 @@ def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True):
     acc = []
     for w, op in enumerate(ops):
         t = loc[w]
-        delta, dqa = op.backward_prepare(t["o"], t["do"])
+        prep, dqa = op.backward_prepare(t["o"], t["lse"], t["do"])
         dka, dva = op.alloc_dkv(False)
         dkr, dvr = op.alloc_dkv(True)
-        op.backward_launch(True, t["q"], t["k"], t["v"], t["kr"], t["vr"], t["lse"], delta, t["do"],
+        op.backward_launch(True, t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"],
                            dqa, dka, dva, dkr, dvr)
-        op.backward_launch(False, t["q"], t["k"], t["v"], t["kr"], t["vr"], t["lse"], delta, t["do"],
+        op.backward_launch(False, t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"],
                            dqa, dka, dva, dkr, dvr)
         acc.append((dqa, dka, dva, dkr, dvr))
     # dKV return along reversed edges + K4 reduce at the owner
