@@ -3,7 +3,7 @@
 // Work item = one 128-row KV block of one KV chunk (local or received) for one KV
 // head.  The CTA streams every (Q chunk, 64-row Q block, q-head of the GQA group)
 // that attends to it; dK/dV accumulate in TMEM (written once, no atomics) and dQ
-// partials leave through TMA bulk reduce-adds into an fp32 accumulator.
+// partials leave through coalesced fp32 reductions into an accumulator.
 //
 // Per Q tile j (64 query rows):
 //   S^T  = K  Q_j^T   M128 N64  K128 (SS)  -> TMEM S        (fp32)
@@ -14,7 +14,8 @@
 //   dV  += P^T  dO_j  M128 N128 K64  (SS)  -> TMEM dV
 //   dK  += dS^T Q_j   M128 N128 K64  (SS)  -> TMEM dK
 //   dQ^T = K^T dS^T   M128 N64  K128 (SS, both MN-major) -> TMEM dQ[j&1]
-//   drain WG (thread == head-dim lane): TMEM -> smem [q][d] -> TMA reduce-add.
+//   drain WG (thread == head-dim lane): TMEM -> registers -> warp-coalesced fp32
+//        red.global.add (one 128-B line per warp per q row).
 // TMEM (512 cols): dV [0,128) dK [128,256) S [256,320) dP [320,384) dQ0 [384,448) dQ1 [448,512)
 // The tensor pipe computes S/dP of tile j+1 while the softmax of tile j runs, and
 // the dQ drain never sits on the matmul critical path.
@@ -26,6 +27,19 @@
 namespace fcpb {
 namespace bwd {
 
+#ifdef FCPB_TRACE
+// Debug timeline of CTA 0: [event][tile] clock64 stamps (see scripts/trace_bwd.py).
+constexpr int kTraceTiles = 256;
+enum TraceEv { kTrQdIssue, kTrQdGot, kTrSdpIssue, kTrPdsGot, kTrAccIssue, kTrSdpGot, kTrLoaded,
+               kTrPfreeGot, kTrPdsArrive, kTrDqGot, kTrDqDone, kTrEvents };
+__device__ unsigned long long g_trace[kTrEvents * kTraceTiles];
+#define FCPB_TR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
+    ((ev) < kTrSdpGot || (ev) >= kTrDqGot ? true : threadIdx.x == 128)) \
+    g_trace[(ev) * kTraceTiles + (j)] = clock64(); } while (0)
+#else
+#define FCPB_TR(ev, j) do {} while (0)
+#endif
+
 constexpr int kD = 128;
 constexpr int kBK = 128;                        // kv rows per item
 constexpr int kBQ = 64;                         // q rows per tile
@@ -34,7 +48,7 @@ constexpr int kKVPanel = kKVBytes / 2;
 constexpr int kQBytes = kBQ * kD * 2;           // 16 KB (two 8 KB panels)
 constexpr int kQPanel = kQBytes / 2;
 constexpr int kPBytes = kBK * kBQ * 2;          // 16 KB: 128 kv rows x 64 q (one SW128 panel)
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 constexpr int kThreads = 384;
 constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColDP = 320, kColDQ = 384;
 
@@ -49,7 +63,6 @@ struct Smem {
   uint8_t dout[kStages][kQBytes];
   uint8_t p[2][kPBytes];            // P^T  (A of dV)
   uint8_t ds[2][kPBytes];           // dS^T (A of dK, B of dQ^T)
-  float dq_stage[kBQ * kD];         // 32 KB, [q][d] fp32, source of the TMA reduce
   float lse2[kStages][kBQ];         // lse * log2(e), per q column
   float delta[kStages][kBQ];
   uint64_t kv_full, kv_empty;
@@ -73,6 +86,7 @@ struct Params {
   const float* delta_t;   // [Hq, t_pad]
   int64_t t_pad;
   int32_t q_tokens;
+  float* dq;              // [Tq, Hq, D] fp32 accumulator
   float* dk;              // local  [Tkv, Hkv, D] fp32
   float* dv;
   float* dk_recv;         // recv   [Tr, Hkv, D] fp32
@@ -100,6 +114,9 @@ FCPB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+FCPB_DEV void red_add_f32(float* addr, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
 FCPB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 FCPB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 FCPB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -117,6 +134,54 @@ FCPB_DEV void tmem_ld64(uint32_t taddr, float (&out)[64]) {
   }
 }
 
+FCPB_DEV float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+FCPB_DEV void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d) : "memory");
+}
+
+// One kv row of one Q tile:  P = exp2(S*c + nlse2[q]),  dS = P (dP + ndelta[q])  -> bf16
+// rows of the SW128 P^T / dS^T panels.  nlse2 = -lse*log2(e), ndelta = -delta (preprocess).
+// kMask: ragged kv row / ragged q columns / causal diagonal (col >= shift) masking.
+template <bool kMask>
+FCPB_DEV void softmax_rows(const float (&s)[kBQ], const float (&dp)[kBQ], uint32_t l2, uint32_t dl,
+                           float sl2, uint32_t pb, uint32_t db, int tid, bool kv_live, int q_valid,
+                           int shift) {
+  const float2 c2 = make_float2(sl2, sl2);
+#pragma unroll
+  for (int c8 = 0; c8 < kBQ / 8; ++c8) {
+    const float4 la = lds128(l2 + c8 * 32), lb = lds128(l2 + c8 * 32 + 16);
+    const float4 da = lds128(dl + c8 * 32), dbv = lds128(dl + c8 * 32 + 16);
+    const float2 nl[4] = {make_float2(la.x, la.y), make_float2(la.z, la.w), make_float2(lb.x, lb.y),
+                          make_float2(lb.z, lb.w)};
+    const float2 nd[4] = {make_float2(da.x, da.y), make_float2(da.z, da.w),
+                          make_float2(dbv.x, dbv.y), make_float2(dbv.z, dbv.w)};
+    uint32_t pk[4], dk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int col = c8 * 8 + 2 * u;
+      const float2 x = __ffma2_rn(make_float2(s[col], s[col + 1]), c2, nl[u]);
+      float p0 = ex2(x.x), p1 = ex2(x.y);
+      if (kMask) {
+        p0 = (kv_live && col < q_valid && col >= shift) ? p0 : 0.f;
+        p1 = (kv_live && col + 1 < q_valid && col + 1 >= shift) ? p1 : 0.f;
+      }
+      const float2 pp = make_float2(p0, p1);
+      const float2 dd = __fmul2_rn(pp, __fadd2_rn(make_float2(dp[col], dp[col + 1]), nd[u]));
+      pk[u] = pack_bf16(pp.x, pp.y);
+      dk[u] = pack_bf16(dd.x, dd.y);
+    }
+    const uint32_t chunk = (c8 ^ (tid & 7)) * 16;
+    sts128(pb + chunk, pk[0], pk[1], pk[2], pk[3]);
+    sts128(db + chunk, dk[0], dk[1], dk[2], dk[3]);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D], box (64,1,64)
                 const __grid_constant__ CUtensorMap tm_do,     // bf16 [Tq,Hq,D], box (64,1,64)
@@ -124,7 +189,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
                 const __grid_constant__ CUtensorMap tm_v,
                 const __grid_constant__ CUtensorMap tm_k_recv,
                 const __grid_constant__ CUtensorMap tm_v_recv,
-                const __grid_constant__ CUtensorMap tm_dq,     // fp32 [Tq,Hq,D], box (128,1,64)
                 const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(
@@ -140,7 +204,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_k_recv);
     tma_prefetch_desc(&tm_v_recv);
-    tma_prefetch_desc(&tm_dq);
   }
   if (warp == 1 && elect_one()) {
     mbar_init(&sm.kv_full, 1);
@@ -173,6 +236,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const uint32_t lane = lane_id();
     const uint64_t keep = policy_evict_last();
     uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
+    int ptile = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
       const Item it = p.items[g / p.num_kv_heads];
       const int kvh = g % p.num_kv_heads;
@@ -216,6 +280,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               cp_async_4(&sm.delta[stage][i], ok ? dsrc + i : p.delta_t, ok);
             }
             cp_async_arrive_noinc(&sm.qd_full[stage]);
+            FCPB_TR(kTrQdIssue, ptile); ++ptile;
             if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
           }
         }
@@ -266,10 +331,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       kv_phase ^= 1;
       // tile 0 of this item: S/dP region must have been read by the previous softmax
       mbar_wait(&sm.qd_full[stage], stage_phase);
+      FCPB_TR(kTrQdGot, (int)tile);
       mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);
       sdpf_phase ^= 1;
       tc_fence_after();
       issue_sdp(stage);
+      FCPB_TR(kTrSdpIssue, (int)tile);
       uint32_t cur_stage = stage;
       if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
       for (int j = 0; j < n; ++j, ++tile) {
@@ -277,15 +344,18 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         const uint32_t st_j = cur_stage;
         if (j + 1 < n) {
           mbar_wait(&sm.qd_full[stage], stage_phase);
+          FCPB_TR(kTrQdGot, (int)tile + 1);
           mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);   // softmax(j) has S/dP(j) in registers
           sdpf_phase ^= 1;
           tc_fence_after();
           issue_sdp(stage);
+          FCPB_TR(kTrSdpIssue, (int)tile + 1);
           cur_stage = stage;
           if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
         }
         mbar_wait(&sm.pds_full[b], pds_phase[b]);
         pds_phase[b] ^= 1;
+        FCPB_TR(kTrPdsGot, (int)tile);
         if (j == 0) {
           mbar_wait(&sm.acc_free, acc_phase ^ 1);
           acc_phase ^= 1;
@@ -311,6 +381,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
                    smem_desc_sw128(a_ds + kk * 2048, kPBytes, 1024), id_dq, kk > 0);
           mma_commit(&sm.dq_full[b]);
           mma_commit(&sm.pds_free[b]);
+          FCPB_TR(kTrAccIssue, (int)tile);
         }
         __syncwarp();
       }
@@ -347,6 +418,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           for (int gq = 0; gq < group; ++gq, ++tile) {
             const uint32_t b = tile & 1;
             mbar_wait(&sm.sdp_full, sdp_phase);
+            FCPB_TR(kTrSdpGot, (int)tile);
             sdp_phase ^= 1;
             mbar_wait(&sm.qd_full[stage], stage_phase);   // lse2 / delta of this tile landed
             tc_fence_after();
@@ -355,42 +427,21 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             tmem_ld64(t_dp, dp);
             tc_fence_before();
             mbar_arrive(&sm.sdp_free);
+            FCPB_TR(kTrLoaded, (int)tile);
             mbar_wait(&sm.pds_free[b], pfree_phase[b] ^ 1);
             pfree_phase[b] ^= 1;
-            const float* l2 = sm.lse2[stage];
-            const float* dl = sm.delta[stage];
+            FCPB_TR(kTrPfreeGot, (int)tile);
+            const uint32_t l2 = smem_u32(sm.lse2[stage]);
+            const uint32_t dl = smem_u32(sm.delta[stage]);
             const uint32_t pb = smem_u32(sm.p[b]) + row_off;
             const uint32_t db = smem_u32(sm.ds[b]) + row_off;
-#pragma unroll
-            for (int c8 = 0; c8 < kBQ / 8; ++c8) {
-              const float4 la = *reinterpret_cast<const float4*>(l2 + c8 * 8);
-              const float4 lb = *reinterpret_cast<const float4*>(l2 + c8 * 8 + 4);
-              const float4 da = *reinterpret_cast<const float4*>(dl + c8 * 8);
-              const float4 dbv = *reinterpret_cast<const float4*>(dl + c8 * 8 + 4);
-              const float lv[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-              const float dv[8] = {da.x, da.y, da.z, da.w, dbv.x, dbv.y, dbv.z, dbv.w};
-              float pp[8], dd[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int col = c8 * 8 + u;
-                float pv = ex2(fmaf(s[col], sl2, -lv[u]));
-                if (!plain) {
-                  const bool vis = kv_live && col < q_valid && col >= shift;
-                  pv = vis ? pv : 0.f;
-                }
-                pp[u] = pv;
-                dd[u] = pv * (dp[col] - dv[u]);
-              }
-              const uint32_t chunk = (c8 ^ (tid & 7)) * 16;
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
-                           ::"r"(pb + chunk), "r"(pack_bf16(pp[0], pp[1])), "r"(pack_bf16(pp[2], pp[3])),
-                             "r"(pack_bf16(pp[4], pp[5])), "r"(pack_bf16(pp[6], pp[7])) : "memory");
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};"
-                           ::"r"(db + chunk), "r"(pack_bf16(dd[0], dd[1])), "r"(pack_bf16(dd[2], dd[3])),
-                             "r"(pack_bf16(dd[4], dd[5])), "r"(pack_bf16(dd[6], dd[7])) : "memory");
-            }
+            if (plain)
+              softmax_rows<false>(s, dp, l2, dl, sl2, pb, db, tid, true, kBQ, -1);
+            else
+              softmax_rows<true>(s, dp, l2, dl, sl2, pb, db, tid, kv_live, q_valid, shift);
             fence_proxy_async_smem();
             mbar_arrive(&sm.pds_full[b]);
+            FCPB_TR(kTrPdsArrive, (int)tile);
             if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
           }
         }
@@ -400,7 +451,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     // ------------------------------------------------------------ dQ drain + dK/dV epilogue
     const int tid = threadIdx.x - 256;            // head-dim lane for dQ^T, kv row for dK/dV
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const bool leader = (tid == 0);
     uint32_t tile = 0, acc_phase = 0;
     uint32_t dq_phase[2] = {0, 0};
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
@@ -415,21 +465,21 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             const int h = kvh * group + gq;
             mbar_wait(&sm.dq_full[b], dq_phase[b]);
             dq_phase[b] ^= 1;
+            FCPB_TR(kTrDqGot, (int)tile);
             tc_fence_after();
             float v[kBQ];
             tmem_ld64(tmem + lane_bits + kColDQ + b * 64, v);
             tc_fence_before();
             mbar_arrive(&sm.dq_free[b]);
-            if (leader) bulk_wait_read0();          // previous reduce has read dq_stage
-            named_bar_sync(2, 128);
+            // rows past the chunk get exact zeros (dS is masked), so no row guard is needed
+            // inside the tensor; rows past the end of the tensor are skipped.
+            float* dst = p.dq + (static_cast<size_t>(qr.q_off + mb * kBQ) * p.num_q_heads + h) * kD + tid;
+            const size_t row_stride = static_cast<size_t>(p.num_q_heads) * kD;
+            const int rows = min(kBQ, p.q_tokens - (qr.q_off + mb * kBQ));
 #pragma unroll
-            for (int q = 0; q < kBQ; ++q) sm.dq_stage[q * kD + tid] = v[q] * p.scale;
-            fence_proxy_async_smem();
-            named_bar_sync(2, 128);
-            if (leader) {
-              tma_reduce_add_3d(&tm_dq, sm.dq_stage, 0, h, qr.q_off + mb * kBQ);
-              bulk_commit();
-            }
+            for (int q = 0; q < kBQ; ++q)
+              if (q < rows) red_add_f32(dst + q * row_stride, v[q] * p.scale);
+            FCPB_TR(kTrDqDone, (int)tile);
           }
         }
       }
@@ -464,7 +514,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       tc_fence_before();
       mbar_arrive(&sm.acc_free);
     }
-    if (leader) bulk_wait0();
   }
 
   tc_fence_before();

@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   if (lane == 0) {
     const int64_t t = w / heads, h = w % heads;
-    delta_t[h * t_pad + t] = s;
-    lse2_t[h * t_pad + t] = lse[w] * 1.4426950408889634f;
+    delta_t[h * t_pad + t] = -s;                                  // negated: dP + ndelta
+    lse2_t[h * t_pad + t] = -lse[w] * 1.4426950408889634f;        // negated: S*c + nlse2
   }
   if (dq) reinterpret_cast<float4*>(dq + w * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
 }

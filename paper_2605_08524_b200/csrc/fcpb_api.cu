@@ -152,7 +152,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
     return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
   if (a->num_items <= 0) return FCPB_OK;
-  CUtensorMap tq, tdo, tk, tv, tkr, tvr, tdq;
+  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
   int rc;
   const int H = a->num_q_heads, Hk = a->num_kv_heads;
   if ((rc = make_map(&tq, a->q, a->q_tokens, H, 128, fcpb::bwd::kBQ))) return rc;
@@ -168,8 +168,6 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
     return rc;
   if (a->t_pad < a->q_tokens || !a->lse2_t || !a->delta_t)
     return fail(FCPB_ERR_INVALID, "lse2_t/delta_t/t_pad missing (run fcpb_bwd_preprocess)");
-  if ((rc = make_map(&tdq, a->dq_accum, a->q_tokens, H, 128, fcpb::bwd::kBQ, true, 128, false)))
-    return rc;
   fcpb::bwd::Params p;
   p.kvsegs = reinterpret_cast<const fcpb::bwd::KvSeg*>(a->kvsegs);
   p.qrefs = reinterpret_cast<const fcpb::bwd::QRef*>(a->qrefs);
@@ -183,6 +181,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.delta_t = a->delta_t;
   p.t_pad = a->t_pad;
   p.q_tokens = static_cast<int32_t>(a->q_tokens);
+  p.dq = a->dq_accum;
   p.dk = a->dk_accum;
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
@@ -197,7 +196,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
   fcpb::bwd::attn_bwd_kernel<<<grid, fcpb::bwd::kThreads, kBwdSmem,
-                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, tdq, p);
+                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
@@ -261,5 +260,13 @@ int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
+
+#ifdef FCPB_TRACE
+// Debug builds only (not part of include/fcpb.h): copy the bwd timeline of CTA 0.
+__attribute__((visibility("default"))) int fcpb_debug_bwd_trace(unsigned long long* host, int n) {
+  FCPB_CUDA(cudaMemcpyFromSymbol(host, fcpb::bwd::g_trace, sizeof(unsigned long long) * n));
+  return FCPB_OK;
+}
+#endif
 
 }  // extern "C"
