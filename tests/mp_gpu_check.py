@@ -1,0 +1,61 @@
+"""Multi-GPU executor check, run under torchrun (one process per GPU, NCCL):
+the FcpExecutor's fwd+bwd with the real NVLink exchange vs the fp64 oracle.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \\
+        --master-port P tests/mp_gpu_check.py [lengths] [block]
+"""
+import json
+import math
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle.attention_ref import mono_bwd, mono_fwd  # noqa: E402
+from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows  # noqa: E402
+from paper_2605_08524_b200.costmodel import ModelConfig  # noqa: E402
+from paper_2605_08524_b200.executor import FcpExecutor  # noqa: E402
+from tests.gpu_harness import REL_L2, LSE_ABS, err, make_inputs, schedule  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    lengths = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3523,2702,2219,1292,1438,413,544,319").split(",")]
+    block = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    model = ModelConfig(q_heads=8, kv_heads=2, head_dim=128)
+    r = schedule(lengths, world, block, model)
+    goff, T = global_offsets(r)
+    q, k, v, do = make_inputs(T, model)
+    ex = FcpExecutor(r, rank, model, dev)
+    lay = ex.layout
+    loc = [gather_rank(x, lay, goff, r.deps).to(dev) for x in (q, k, v, do)]
+    for _ in range(2):   # twice: the executor is reused across layers
+        o, lse, dq, dk, dv = ex.step(*loc)
+    torch.cuda.synchronize()
+    rows = global_sequence_rows(r)
+    scale = 1 / math.sqrt(model.head_dim)
+    qf, kf, vf, dof = (x.double() for x in (q, k, v, do))
+    ro, rl = mono_fwd(qf, kf, vf, rows, scale)
+    rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
+    rep = {}
+    for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))
+    ok = all((e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2) for n, e in rep.items())
+    print(json.dumps({"rank": rank, "world": world, "recv_tokens": lay.recv_tokens,
+                      "stages": len(ex.stages), "ok": ok, "errors": rep}), flush=True)
+    flag = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    dist.destroy_process_group()
+    sys.exit(0 if flag.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
