@@ -216,8 +216,8 @@ def main():
     stream = torch.cuda.current_stream(device)
 
     # kernel-level events (on the launching stream) for the roofline
-    lib_launch = {"fwd": [], "bwd": []}
-    orig_fw, orig_bl = ex.op.forward_wave, ex.op.backward_launch
+    lib_launch = {"fwd": [], "bwd": [], "dq": []}
+    orig_fw, orig_bl, orig_dq = ex.op.forward_wave, ex.op.backward_launch, ex.op.backward_dq
     timing = {"on": False}
 
     def timed_fw(*a, **kw):
@@ -238,7 +238,17 @@ def main():
         e.record(stream)
         lib_launch["bwd"].append((s, e))
 
-    ex.op.forward_wave, ex.op.backward_launch = timed_fw, timed_bl
+    def timed_dq(*a, **kw):
+        if not timing["on"]:
+            return orig_dq(*a, **kw)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        out = orig_dq(*a, **kw)
+        e.record(stream)
+        lib_launch["dq"].append((s, e))
+        return out
+
+    ex.op.forward_wave, ex.op.backward_launch, ex.op.backward_dq = timed_fw, timed_bl, timed_dq
 
     def barrier():
         if world > 1:
@@ -307,13 +317,18 @@ def main():
     if rank == 0:
         value = w.total_tokens / (ms_max / 1e3)
         mfu = flop_total / (n * peak * ms_max / 1e3)
-        n_fwd = len(lib_launch["fwd"]) or 1
-        n_bwd = len(lib_launch["bwd"]) or 1
         reps = min(3, args.steps)
-        fwd_ms = sum(s.elapsed_time(e) for s, e in lib_launch["fwd"]) / reps
-        bwd_ms = sum(s.elapsed_time(e) for s, e in lib_launch["bwd"]) / reps
+        kms = {key: sum(s.elapsed_time(e) for s, e in evs) / reps for key, evs in lib_launch.items()}
+        nl = {key: len(evs) / reps for key, evs in lib_launch.items()}
+        # algorithmic FLOPs per kernel (reference costmodel: fwd 4*Hq*D per pair; the
+        # backward's 2.5x splits 4 GEMMs dK/dV + 3 GEMMs dQ of the 7 the split executes,
+        # so each kernel is credited its share of the 2.5x: dK/dV 2.5*4/7, dQ 2.5*3/7)
+        kfl = {"fwd": fwd_f, "bwd": bwd_f * 4 / 7, "dq": bwd_f * 3 / 7}
+        ktf = {key: (kfl[key] / (kms[key] / 1e3) / 1e12 if kms[key] > 0 else 0.0) for key in kms}
+        bwd_ms = kms["bwd"] + kms["dq"]
         bwd_tflops = bwd_f / (bwd_ms / 1e3) / 1e12 if bwd_ms > 0 else 0.0
-        fwd_tflops = fwd_f / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else 0.0
+        top = max(kms, key=lambda kk: kms[kk])
+        names = {"fwd": "attn_fwd_kernel", "bwd": "attn_bwd_kernel", "dq": "attn_dq_kernel"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -325,15 +340,15 @@ def main():
                        "parallelism": f"fcp{n}", "l2": "inputs larger than L2 (no flush needed)",
                        "plan_ms_host": round(plan_ms, 2)},
             "mfu": mfu, "flop_total": flop_total,
-            "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel",
-                         "achieved": bwd_tflops, "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": bwd_tflops * 1e12 / peak, "peak_kind": peak_kind + " burst",
+            "roofline": {"bound": "tensor", "kernel": names[top],
+                         "achieved": ktf[top], "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": ktf[top] * 1e12 / peak, "peak_kind": peak_kind + " burst",
                          "traffic": None,
-                         "per_unit": "2.5*4*Hq*D FLOP per visible (q,kv) pair; units = rank-0 pairs"},
-            "kernels": {"attn_fwd_kernel": {"ms": fwd_ms, "tflops": fwd_tflops,
-                                            "frac": fwd_tflops * 1e12 / peak, "launches": n_fwd / reps},
-                        "attn_bwd_kernel": {"ms": bwd_ms, "tflops": bwd_tflops,
-                                            "frac": bwd_tflops * 1e12 / peak, "launches": n_bwd / reps}},
+                         "per_unit": "4*Hq*D FLOP per visible (q,kv) pair (fwd); bwd 2.5x split "
+                                     "4/7 dK/dV, 3/7 dQ; units = rank-0 visible pairs"},
+            "kernels": {names[key]: {"ms": kms[key], "tflops": ktf[key], "frac": ktf[key] * 1e12 / peak,
+                                     "launches": nl[key]} for key in kms},
+            "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
             "exchange_bytes_rank0": exb,
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,

@@ -64,6 +64,7 @@ typedef struct {
   const FcpbKvRef* kv_refs;    int32_t num_kv_refs;
   const FcpbItem* items;       int32_t num_items;     /* LPT-ordered                  */
   int32_t num_ctas;            /* 0 = one per SM                                      */
+  int32_t head_major;          /* grid order: 0 = heads of an item adjacent, 1 = items of a head */
 } FcpbFwdArgs;
 
 FCPB_API int fcpb_attn_fwd(const FcpbFwdArgs* args, void* stream);
@@ -95,10 +96,32 @@ FCPB_API int fcpb_bwd_preprocess(const void* o, const void* dout, const float* l
                                  int64_t tokens, int32_t num_q_heads, int32_t head_dim,
                                  void* stream);
 
-/* K2: backward.  Work is organised by KV tile: for each KV chunk reference (local
+/* K2b: dQ of the backward, query-stationary (one CTA per 128 query rows x head): the
+ * segment / KV-ref / item tables have the forward's layout but each segment lists ALL
+ * KV chunks its Q chunk attends to (local and received).  Writes bf16 dQ once
+ * (scale applied); needs lse2_t / delta_t from fcpb_bwd_preprocess. */
+typedef struct {
+  int32_t num_q_heads, num_kv_heads, head_dim;
+  float softmax_scale;
+  const void* q; const void* dout;
+  const float* lse2_t; const float* delta_t; int64_t t_pad;
+  int64_t q_tokens;
+  const void* k; const void* v; int64_t kv_tokens;
+  const void* k_recv; const void* v_recv; int64_t kv_recv_tokens;
+  void* dq;                                    /* bf16 [Tq, Hq, D] */
+  const FcpbSegment* segments; int32_t num_segments;
+  const FcpbKvRef* kv_refs;    int32_t num_kv_refs;
+  const FcpbItem* items;       int32_t num_items;
+  int32_t num_ctas;
+  int32_t head_major;
+} FcpbDqArgs;
+
+FCPB_API int fcpb_attn_bwd_dq(const FcpbDqArgs* args, void* stream);
+
+/* K2: backward dK/dV.  Work is organised by KV tile: for each KV chunk reference (local
  * or received) the list of local Q chunks that attend to it.  dK/dV accumulate in
  * fp32 per KV arena row (plain stores: one CTA owns a KV block for all heads of
- * its GQA group); dQ partials are TMA reduce-added into dq_accum (fp32). */
+ * its GQA group). */
 typedef struct {
   int32_t kv_off, kv_len;       /* arena rows of the KV chunk                       */
   int32_t flags;                /* FCPB_KV_RECV: lives in the receive arena         */
@@ -125,13 +148,14 @@ typedef struct {
   int64_t q_tokens;
   const void* k; const void* v; int64_t kv_tokens;
   const void* k_recv; const void* v_recv; int64_t kv_recv_tokens;
-  float* dq_accum;              /* [Tq, Hq, D] fp32 (atomically accumulated)        */
+  float* dq_accum;              /* unused (dQ comes from fcpb_attn_bwd_dq); may be NULL */
   float* dk_accum; float* dv_accum;             /* local  [Tkv, Hkv, D] fp32         */
   float* dk_recv_accum; float* dv_recv_accum;   /* recv   [Trecv, Hkv, D] fp32       */
   const FcpbBwdKvSeg* kvsegs; int32_t num_kvsegs;
   const FcpbBwdQRef* qrefs; int32_t num_qrefs;
   const FcpbBwdItem* items; int32_t num_items;
   int32_t num_ctas;
+  int32_t head_major;
 } FcpbBwdArgs;
 
 FCPB_API int fcpb_attn_bwd(const FcpbBwdArgs* args, void* stream);

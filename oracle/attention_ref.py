@@ -230,8 +230,9 @@ def emulate_forward(work, q, k, v, k_recv, v_recv, scale, dtype=torch.float64):
 
 
 def emulate_backward(work, q, k, v, k_recv, v_recv, o, lse, do, scale, dtype=torch.float64):
-    """Interpret ``work.bwd`` (KV-keyed launches) on the CPU.  Returns local
-    (dQ, dK, dV) and the received chunks' (dK, dV) partials."""
+    """Interpret the backward work lists on the CPU: ``work.bwd`` (KV-keyed dK/dV
+    launches) and ``work.dq`` (query-stationary dQ).  Returns local (dQ, dK, dV)
+    and the received chunks' (dK, dV) partials."""
     T, H, D = q.shape
     Hk = k.shape[1]
     group = H // Hk
@@ -265,10 +266,35 @@ def emulate_backward(work, q, k, v, k_recv, v_recv, o, lse, do, scale, dtype=tor
                         p = torch.exp(s - lse[sl, h].to(dtype).unsqueeze(1)).masked_fill(~vis, 0.0)
                         dp = torch.matmul(do[sl, h].to(dtype), vv[:, kh].transpose(0, 1))
                         ds = p * (dp - delta[sl, h].unsqueeze(1))
-                        dq[sl, h] += torch.matmul(ds, kk[:, kh]) * scale
                         gk[:, kh] += torch.matmul(ds.transpose(0, 1), qs) * scale
                         gv[:, kh] += torch.matmul(p.transpose(0, 1), do[sl, h].to(dtype))
             dst_k, dst_v = (dkr, dvr) if flags & 2 else (dk, dv)
             dst_k[kv_off + c0:kv_off + c0 + cn] = gk
             dst_v[kv_off + c0:kv_off + c0 + cn] = gv
+    # dQ: query-stationary tables (work.dq) -- one 128-row item per Q chunk block
+    d = work.dq
+    for seg_idx, mb in d.items.tolist():
+        q_off, q_len, kb, ke, _, _ = d.segments[seg_idx].tolist()
+        r0 = mb * TILE
+        nrow = min(TILE, q_len - r0)
+        sl = slice(q_off + r0, q_off + r0 + nrow)
+        for ref in d.kvrefs[kb:ke].tolist():
+            off, kn, flags, _ = ref
+            src_k, src_v = (k_recv, v_recv) if flags & 2 else (k, v)
+            diag = bool(flags & 1)
+            ntile = -(-kn // TILE)
+            if diag:
+                ntile = min(ntile, mb + 1)
+            for t in range(ntile):
+                c0 = t * TILE
+                cn = min(TILE, kn - c0)
+                for h in range(H):
+                    kh = h // group
+                    kk = src_k[off + c0:off + c0 + cn, kh].to(dtype)
+                    vv = src_v[off + c0:off + c0 + cn, kh].to(dtype)
+                    s, vis = _tile_scores(q[sl, h].to(dtype), kk, scale, r0, c0, q_len, kn, diag)
+                    p = torch.exp(s - lse[sl, h].to(dtype).unsqueeze(1)).masked_fill(~vis, 0.0)
+                    dp = torch.matmul(do[sl, h].to(dtype), vv.transpose(0, 1))
+                    ds = p * (dp - delta[sl, h].unsqueeze(1))
+                    dq[sl, h] += torch.matmul(ds, kk) * scale
     return dq, dk, dv, dkr, dvr

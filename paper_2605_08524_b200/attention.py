@@ -7,8 +7,10 @@ the batch.  The multi-GPU executor (``executor.py``) drives it wave by wave,
 interleaved with the KV exchange; on one GPU ``forward``/``backward`` run the
 whole rank at once.
 
-Numerics: bf16 inputs, fp32 accumulation in TMEM, fp32 LSE (natural log),
-fp32 dQ/dK/dV accumulators rounded to bf16 at the end.
+Numerics: bf16 inputs, fp32 accumulation in TMEM, fp32 LSE (natural log);
+dQ accumulates in TMEM over all KV and is written once in bf16; dK/dV are
+fp32 (so received-chunk partials can be added at the owner) and rounded to bf16
+at the end.
 """
 
 from __future__ import annotations
@@ -63,7 +65,13 @@ class BlockAttention:
             self._merge = (_dev_i32(f.merge_groups, dev), _dev_i32(f.merge_part_rows, dev))
         self._bwd = [(b, _dev_i32(b.kvsegs, dev), _dev_i32(b.qrefs, dev), _dev_i32(b.items, dev))
                      for b in work.bwd]
+        d = work.dq
+        self._dq = (d, _dev_i32(d.segments, dev), _dev_i32(d.kvrefs, dev), _dev_i32(d.items, dev))
         self.launches = 0   # kernel launches issued by this object (bench accounting)
+        import os
+        sched = os.environ.get("FCPB_SCHED", "")   # experiment knob: "f,b,q" head-major flags
+        flags = [int(x) for x in sched.split(",")] if sched else [0, 0, 0]
+        self.head_major = {"fwd": flags[0], "bwd": flags[1], "dq": flags[2]}
 
     # ------------------------------------------------------------------ shapes
     def q_shape(self):
@@ -103,6 +111,7 @@ class BlockAttention:
         a.kv_refs, a.num_kv_refs = native.ptr(refs), len(wave.kvrefs)
         a.items, a.num_items = native.ptr(items), len(wave.items)
         a.num_ctas = self.num_ctas
+        a.head_major = self.head_major["fwd"]
         native.check(self.lib.fcpb_attn_fwd(ctypes_ref(a), self._stream(stream)))
         self.launches += 1
 
@@ -146,19 +155,41 @@ class BlockAttention:
 
     # ------------------------------------------------------------------ backward
     def backward_prepare(self, o, lse, do, stream=None):
-        """delta = rowsum(dO*O) and lse*log2(e), head-major, plus a zeroed fp32 dQ
-        accumulator.  Returns the tuple the K2 launches consume."""
+        """-delta = -rowsum(dO*O) and -lse*log2(e), head-major [Hq, t_pad] fp32, for the
+        dK/dV and dQ kernels.  Returns the (lse2_t, delta_t, t_pad) tuple they consume."""
         H = self.cfg.q_heads
         t_pad = (self.tokens + 3) // 4 * 4
         lse2_t = torch.empty((H, t_pad), dtype=torch.float32, device=self.device)
         delta_t = torch.empty((H, t_pad), dtype=torch.float32, device=self.device)
-        dq = torch.empty(self.q_shape(), dtype=torch.float32, device=self.device)
         native.check(self.lib.fcpb_bwd_preprocess(native.ptr(o), native.ptr(do), native.ptr(lse),
                                                   native.ptr(lse2_t), native.ptr(delta_t), t_pad,
-                                                  native.ptr(dq), self.tokens, H, self.cfg.head_dim,
+                                                  None, self.tokens, H, self.cfg.head_dim,
                                                   self._stream(stream)))
         self.launches += 1
-        return (lse2_t, delta_t, t_pad), dq
+        return lse2_t, delta_t, t_pad
+
+    def backward_dq(self, q, k, v, k_recv, v_recv, prep, do, stream=None):
+        """K2b: query-stationary dQ over every KV chunk of each local Q chunk -> bf16."""
+        d, segs, refs, items = self._dq
+        dq = torch.empty(self.q_shape(), dtype=torch.bfloat16, device=self.device)
+        a = native.DqArgs()
+        a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
+        a.softmax_scale = self.scale
+        lse2_t, delta_t, t_pad = prep
+        a.q, a.dout = native.ptr(q), native.ptr(do)
+        a.lse2_t, a.delta_t, a.t_pad = native.ptr(lse2_t), native.ptr(delta_t), t_pad
+        a.q_tokens = self.tokens
+        a.k, a.v, a.kv_tokens = native.ptr(k), native.ptr(v), self.tokens
+        a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
+        a.dq = native.ptr(dq)
+        a.segments, a.num_segments = native.ptr(segs), len(d.segments)
+        a.kv_refs, a.num_kv_refs = native.ptr(refs), len(d.kvrefs)
+        a.items, a.num_items = native.ptr(items), len(d.items)
+        a.num_ctas = self.num_ctas
+        a.head_major = self.head_major["dq"]
+        native.check(self.lib.fcpb_attn_bwd_dq(ctypes_ref(a), self._stream(stream)))
+        self.launches += 1
+        return dq
 
     def alloc_dkv(self, recv: bool):
         shape = self.kv_shape(recv)
@@ -167,7 +198,7 @@ class BlockAttention:
         return (torch.empty(shape, dtype=torch.float32, device=self.device),
                 torch.empty(shape, dtype=torch.float32, device=self.device))
 
-    def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, prep, do, dq,
+    def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, prep, do,
                         dk, dv, dk_r, dv_r, stream=None):
         for b, kvsegs, qrefs, items in self._bwd:
             if b.recv != recv:
@@ -181,12 +212,13 @@ class BlockAttention:
             a.q_tokens = self.tokens
             a.k, a.v, a.kv_tokens = native.ptr(k), native.ptr(v), self.tokens
             a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
-            a.dq_accum, a.dk_accum, a.dv_accum = native.ptr(dq), native.ptr(dk), native.ptr(dv)
+            a.dq_accum, a.dk_accum, a.dv_accum = None, native.ptr(dk), native.ptr(dv)
             a.dk_recv_accum, a.dv_recv_accum = native.ptr(dk_r), native.ptr(dv_r)
             a.kvsegs, a.num_kvsegs = native.ptr(kvsegs), len(b.kvsegs)
             a.qrefs, a.num_qrefs = native.ptr(qrefs), len(b.qrefs)
             a.items, a.num_items = native.ptr(items), len(b.items)
             a.num_ctas = self.num_ctas
+            a.head_major = self.head_major["bwd"]
             native.check(self.lib.fcpb_attn_bwd(ctypes_ref(a), self._stream(stream)))
             self.launches += 1
 
@@ -209,13 +241,13 @@ class BlockAttention:
         received KV, the fp32 (dk_recv, dv_recv) partials owed to their owners."""
         self.validate(q, k, v, k_recv, v_recv)
         _check(do, "do", self.q_shape())
-        prep, dq = self.backward_prepare(o, lse, do, stream)
+        prep = self.backward_prepare(o, lse, do, stream)
         dk, dv = self.alloc_dkv(False)
         dk_r, dv_r = self.alloc_dkv(True)
-        self.backward_launch(True, q, k, v, k_recv, v_recv, prep, do, dq, dk, dv, dk_r, dv_r, stream)
-        self.backward_launch(False, q, k, v, k_recv, v_recv, prep, do, dq, dk, dv, dk_r, dv_r, stream)
-        return (self.to_bf16(dq, stream), self.to_bf16(dk, stream), self.to_bf16(dv, stream),
-                dk_r, dv_r)
+        self.backward_launch(True, q, k, v, k_recv, v_recv, prep, do, dk, dv, dk_r, dv_r, stream)
+        self.backward_launch(False, q, k, v, k_recv, v_recv, prep, do, dk, dv, dk_r, dv_r, stream)
+        dq = self.backward_dq(q, k, v, k_recv, v_recv, prep, do, stream)
+        return dq, self.to_bf16(dk, stream), self.to_bf16(dv, stream), dk_r, dv_r
 
 
 def ctypes_ref(s):

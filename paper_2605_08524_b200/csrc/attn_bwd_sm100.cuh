@@ -2,8 +2,11 @@
 //
 // Work item = one 128-row KV block of one KV chunk (local or received) for one KV
 // head.  The CTA streams every (Q chunk, 64-row Q block, q-head of the GQA group)
-// that attends to it; dK/dV accumulate in TMEM (written once, no atomics) and dQ
-// partials leave through coalesced fp32 reductions into an accumulator.
+// that attends to it; dK/dV accumulate in TMEM and are written once (no atomics).
+// dQ is produced by the query-stationary kernel in attn_dq_sm100.cuh: reducing a
+// 32 KB fp32 dQ partial per tile from here measured ~3,750 cycles per tile on B200
+// (~9 B/clk/SM of reduction throughput, TMA reduce-add and red.global alike), 2.3x
+// the tile's tensor time.
 //
 // Per Q tile j (64 query rows):
 //   S^T  = K  Q_j^T   M128 N64  K128 (SS)  -> TMEM S        (fp32)
@@ -13,13 +16,10 @@
 //        (SW128 rows of 64 q, double buffered)
 //   dV  += P^T  dO_j  M128 N128 K64  (SS)  -> TMEM dV
 //   dK  += dS^T Q_j   M128 N128 K64  (SS)  -> TMEM dK
-//   dQ^T = K^T dS^T   M128 N64  K128 (SS, both MN-major) -> TMEM dQ[j&1]
-//   drain WG (thread == head-dim lane): TMEM -> registers -> warp-coalesced fp32
-//        red.global.add (one 128-B line per warp per q row).
-// TMEM (512 cols): dV [0,128) dK [128,256) S [256,320) dP [320,384) dQ0 [384,448) dQ1 [448,512)
-// The tensor pipe computes S/dP of tile j+1 while the softmax of tile j runs, and
-// the dQ drain never sits on the matmul critical path.
-// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 softmax, w8-11 dQ drain + dK/dV store.
+// TMEM (512 cols): dV [0,128) dK [128,256) S [256,320) dP [320,384)
+//                  P0 [384,416) dS0 [416,448) P1 [448,480) dS1 [480,512)
+// The tensor pipe computes S/dP of tile j+1 while the softmax of tile j runs.
+// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 softmax, w8-11 dK/dV epilogue.
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -48,9 +48,12 @@ constexpr int kKVPanel = kKVBytes / 2;
 constexpr int kQBytes = kBQ * kD * 2;           // 16 KB (two 8 KB panels)
 constexpr int kQPanel = kQBytes / 2;
 constexpr int kPBytes = kBK * kBQ * 2;          // 16 KB: 128 kv rows x 64 q (one SW128 panel)
-constexpr int kStages = 3;
+constexpr int kStages = 4;
 constexpr int kThreads = 384;
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColDP = 320, kColDQ = 384;
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColDP = 320;
+// bf16 P^T / dS^T, 32 columns each, double buffered: P_b = 384 + 64b, dS_b = 416 + 64b
+FCPB_DEV constexpr uint32_t col_p(uint32_t b) { return 384u + 64u * b; }
+FCPB_DEV constexpr uint32_t col_ds(uint32_t b) { return 416u + 64u * b; }
 
 struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
 struct QRef { int32_t q_off, q_len, diag, pad_; };
@@ -61,15 +64,12 @@ struct Smem {
   uint8_t v[kKVBytes];
   uint8_t q[kStages][kQBytes];
   uint8_t dout[kStages][kQBytes];
-  uint8_t p[2][kPBytes];            // P^T  (A of dV)
-  uint8_t ds[2][kPBytes];           // dS^T (A of dK, B of dQ^T)
   float lse2[kStages][kBQ];         // lse * log2(e), per q column
   float delta[kStages][kBQ];
   uint64_t kv_full, kv_empty;
   uint64_t qd_full[kStages], qd_empty[kStages];
   uint64_t sdp_full, sdp_free;
   uint64_t pds_full[2], pds_free[2];
-  uint64_t dq_full[2], dq_free[2];
   uint64_t acc_full, acc_free;
   uint32_t tmem_base;
 };
@@ -80,31 +80,28 @@ struct Params {
   const Item* items;
   int32_t num_items;
   int32_t num_q_heads, num_kv_heads;
+  int32_t head_major;
   float scale;            // softmax scale
   float scale_log2;       // scale * log2(e)
   const float* lse2_t;    // [Hq, t_pad] lse * log2(e)
   const float* delta_t;   // [Hq, t_pad]
   int64_t t_pad;
   int32_t q_tokens;
-  float* dq;              // [Tq, Hq, D] fp32 accumulator
   float* dk;              // local  [Tkv, Hkv, D] fp32
   float* dv;
   float* dk_recv;         // recv   [Tr, Hkv, D] fp32
   float* dv_recv;
 };
 
+// Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
+// one head (they stream the same Q/dO tiles -> L2 reuse); else the heads of one item.
+FCPB_DEV int item_of(int g, const Params& p) { return p.head_major ? g % p.num_items : g / p.num_kv_heads; }
+FCPB_DEV int head_of(int g, const Params& p) { return p.head_major ? g / p.num_items : g % p.num_kv_heads; }
+
 // Q blocks (64 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= 2nb.
 FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? 2 * nb : 0; }
 FCPB_DEV int q_num_blocks(const QRef& qr) { return (qr.q_len + kBQ - 1) / kBQ; }
 
-FCPB_DEV void tma_reduce_add_3d(const CUtensorMap* m, const void* smem_src, int32_t c0, int32_t c1,
-                                int32_t c2) {
-  asm volatile(
-      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
-      " [%0, {%2, %3, %4}], [%1];"
-      ::"l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 // 4-byte async copy with zero fill when !valid; completion tracked by an mbarrier.
 FCPB_DEV void cp_async_4(void* smem_dst, const float* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
@@ -114,12 +111,6 @@ FCPB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-FCPB_DEV void red_add_f32(float* addr, float v) {
-  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
-}
-FCPB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-FCPB_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-FCPB_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // 32 lanes x 64 columns (two x32 loads), waits for completion.
 FCPB_DEV void tmem_ld64(uint32_t taddr, float (&out)[64]) {
@@ -140,46 +131,45 @@ FCPB_DEV float4 lds128(uint32_t addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
-FCPB_DEV void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d) : "memory");
-}
 
-// One kv row of one Q tile:  P = exp2(S*c + nlse2[q]),  dS = P (dP + ndelta[q])  -> bf16
-// rows of the SW128 P^T / dS^T panels.  nlse2 = -lse*log2(e), ndelta = -delta (preprocess).
+// One kv row of one Q tile:  P = exp2(S*c + nlse2[q]),  dS = P (dP + ndelta[q]), packed to
+// bf16 pairs in TMEM (32 columns each: the A operands of the dV / dK matmuls).
+// nlse2 = -lse*log2(e), ndelta = -delta (preprocess).
 // kMask: ragged kv row / ragged q columns / causal diagonal (col >= shift) masking.
 template <bool kMask>
-FCPB_DEV void softmax_rows(const float (&s)[kBQ], const float (&dp)[kBQ], uint32_t l2, uint32_t dl,
-                           float sl2, uint32_t pb, uint32_t db, int tid, bool kv_live, int q_valid,
-                           int shift) {
+FCPB_DEV void softmax_half(const uint32_t (&s)[32], const uint32_t (&dp)[32], uint32_t l2,
+                           uint32_t dl, float sl2, uint32_t t_p, uint32_t t_ds, bool kv_live,
+                           int q_valid, int shift, int half) {
   const float2 c2 = make_float2(sl2, sl2);
+  uint32_t pk[16], dk[16];
 #pragma unroll
-  for (int c8 = 0; c8 < kBQ / 8; ++c8) {
-    const float4 la = lds128(l2 + c8 * 32), lb = lds128(l2 + c8 * 32 + 16);
-    const float4 da = lds128(dl + c8 * 32), dbv = lds128(dl + c8 * 32 + 16);
+  for (int c8 = 0; c8 < 4; ++c8) {
+    const int cb = half * 32 + c8 * 8;
+    const float4 la = lds128(l2 + cb * 4), lb = lds128(l2 + cb * 4 + 16);
+    const float4 da = lds128(dl + cb * 4), dbv = lds128(dl + cb * 4 + 16);
     const float2 nl[4] = {make_float2(la.x, la.y), make_float2(la.z, la.w), make_float2(lb.x, lb.y),
                           make_float2(lb.z, lb.w)};
     const float2 nd[4] = {make_float2(da.x, da.y), make_float2(da.z, da.w),
                           make_float2(dbv.x, dbv.y), make_float2(dbv.z, dbv.w)};
-    uint32_t pk[4], dk[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int col = c8 * 8 + 2 * u;
-      const float2 x = __ffma2_rn(make_float2(s[col], s[col + 1]), c2, nl[u]);
+      const int i = c8 * 8 + 2 * u;
+      const int col = half * 32 + i;
+      const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), c2, nl[u]);
       float p0 = ex2(x.x), p1 = ex2(x.y);
       if (kMask) {
         p0 = (kv_live && col < q_valid && col >= shift) ? p0 : 0.f;
         p1 = (kv_live && col + 1 < q_valid && col + 1 >= shift) ? p1 : 0.f;
       }
       const float2 pp = make_float2(p0, p1);
-      const float2 dd = __fmul2_rn(pp, __fadd2_rn(make_float2(dp[col], dp[col + 1]), nd[u]));
-      pk[u] = pack_bf16(pp.x, pp.y);
-      dk[u] = pack_bf16(dd.x, dd.y);
+      const float2 dd = __fmul2_rn(
+          pp, __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd[u]));
+      pk[c8 * 4 + u] = pack_bf16(pp.x, pp.y);
+      dk[c8 * 4 + u] = pack_bf16(dd.x, dd.y);
     }
-    const uint32_t chunk = (c8 ^ (tid & 7)) * 16;
-    sts128(pb + chunk, pk[0], pk[1], pk[2], pk[3]);
-    sts128(db + chunk, dk[0], dk[1], dk[2], dk[3]);
   }
+  tmem_st16(t_p + half * 16, pk);
+  tmem_st16(t_ds + half * 16, dk);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -217,8 +207,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm.pds_full[b], 128);
       mbar_init(&sm.pds_free[b], 1);
-      mbar_init(&sm.dq_full[b], 1);
-      mbar_init(&sm.dq_free[b], 128);
     }
     mbar_init(&sm.acc_full, 1);
     mbar_init(&sm.acc_free, 128);
@@ -238,8 +226,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
     int ptile = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const Item it = p.items[g / p.num_kv_heads];
-      const int kvh = g % p.num_kv_heads;
+      const Item it = p.items[item_of(g, p)];
+      const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
       const bool recv = ks.flags & FCPB_KV_RECV;
       const int krow = ks.kv_off + it.nblock * kBK;
@@ -290,11 +278,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     // ------------------------------------------------------------ MMA issuer
     const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);  // S^T, dP^T
     const uint32_t id_acc = idesc_bf16_f32(kBK, kD, false, true);    // dV, dK
-    const uint32_t id_dq = idesc_bf16_f32(kD, kBQ, true, true);      // dQ^T
     const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v);
     const bool leader = elect_one();
     uint32_t kv_phase = 0, stage = 0, stage_phase = 0, sdpf_phase = 0, acc_phase = 0;
-    uint32_t pds_phase[2] = {0, 0}, dqf_phase[2] = {0, 0};
+    uint32_t pds_phase[2] = {0, 0};
     uint32_t tile = 0;   // running Q-tile counter (selects P/dS and dQ buffers)
 
     auto issue_sdp = [&](uint32_t st) {
@@ -320,7 +307,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     };
 
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const Item it = p.items[g / p.num_kv_heads];
+      const Item it = p.items[item_of(g, p)];
       const KvSeg ks = p.kvsegs[it.kvseg];
       int n = 0;
       for (int r = ks.q_begin; r < ks.q_end; ++r) {
@@ -360,26 +347,18 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           mbar_wait(&sm.acc_free, acc_phase ^ 1);
           acc_phase ^= 1;
         }
-        mbar_wait(&sm.dq_free[b], dqf_phase[b] ^ 1);
-        dqf_phase[b] ^= 1;
         tc_fence_after();
         if (leader) {
-          const uint32_t a_p = smem_u32(sm.p[b]), a_ds = smem_u32(sm.ds[b]);
           const uint32_t a_q = smem_u32(sm.q[st_j]), a_do = smem_u32(sm.dout[st_j]);
 #pragma unroll
-          for (int kk = 0; kk < kBQ / 16; ++kk)     // dV += P^T dO
-            mma_ss(tmem + kColDV, smem_desc_sw128(a_p + kk * 32, 16, 1024),
+          for (int kk = 0; kk < kBQ / 16; ++kk)     // dV += P^T dO   (A = P^T in TMEM)
+            mma_ts(tmem + kColDV, tmem + col_p(b) + kk * 8,
                    smem_desc_sw128(a_do + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
 #pragma unroll
-          for (int kk = 0; kk < kBQ / 16; ++kk)     // dK += dS^T Q
-            mma_ss(tmem + kColDK, smem_desc_sw128(a_ds + kk * 32, 16, 1024),
+          for (int kk = 0; kk < kBQ / 16; ++kk)     // dK += dS^T Q   (A = dS^T in TMEM)
+            mma_ts(tmem + kColDK, tmem + col_ds(b) + kk * 8,
                    smem_desc_sw128(a_q + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
           mma_commit(&sm.qd_empty[st_j]);
-#pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)     // dQ^T = K^T dS^T
-            mma_ss(tmem + kColDQ + b * 64, smem_desc_sw128(a_k + kk * 2048, kKVPanel, 1024),
-                   smem_desc_sw128(a_ds + kk * 2048, kPBytes, 1024), id_dq, kk > 0);
-          mma_commit(&sm.dq_full[b]);
           mma_commit(&sm.pds_free[b]);
           FCPB_TR(kTrAccIssue, (int)tile);
         }
@@ -397,12 +376,13 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_bits + kColS;
     const uint32_t t_dp = tmem + lane_bits + kColDP;
-    const uint32_t row_off = (tid >> 3) * 1024 + (tid & 7) * 128;
     const float sl2 = p.scale_log2;
+    const uint32_t t_p[2] = {tmem + lane_bits + col_p(0), tmem + lane_bits + col_p(1)};
+    const uint32_t t_ds[2] = {tmem + lane_bits + col_ds(0), tmem + lane_bits + col_ds(1)};
     uint32_t sdp_phase = 0, stage = 0, stage_phase = 0, tile = 0;
     uint32_t pfree_phase[2] = {0, 0};
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const Item it = p.items[g / p.num_kv_heads];
+      const Item it = p.items[item_of(g, p)];
       const KvSeg ks = p.kvsegs[it.kvseg];
       const int kv_row = it.nblock * kBK + tid;
       const bool kv_live = kv_row < ks.kv_len;
@@ -422,24 +402,28 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             sdp_phase ^= 1;
             mbar_wait(&sm.qd_full[stage], stage_phase);   // lse2 / delta of this tile landed
             tc_fence_after();
-            float s[kBQ], dp[kBQ];
-            tmem_ld64(t_s, s);
-            tmem_ld64(t_dp, dp);
-            tc_fence_before();
-            mbar_arrive(&sm.sdp_free);
-            FCPB_TR(kTrLoaded, (int)tile);
-            mbar_wait(&sm.pds_free[b], pfree_phase[b] ^ 1);
-            pfree_phase[b] ^= 1;
-            FCPB_TR(kTrPfreeGot, (int)tile);
             const uint32_t l2 = smem_u32(sm.lse2[stage]);
             const uint32_t dl = smem_u32(sm.delta[stage]);
-            const uint32_t pb = smem_u32(sm.p[b]) + row_off;
-            const uint32_t db = smem_u32(sm.ds[b]) + row_off;
-            if (plain)
-              softmax_rows<false>(s, dp, l2, dl, sl2, pb, db, tid, true, kBQ, -1);
-            else
-              softmax_rows<true>(s, dp, l2, dl, sl2, pb, db, tid, kv_live, q_valid, shift);
-            fence_proxy_async_smem();
+            mbar_wait(&sm.pds_free[b], pfree_phase[b] ^ 1);   // P/dS buffer b consumed (tile j-2)
+            pfree_phase[b] ^= 1;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint32_t sv[32], dv[32];
+              tmem_ld32(t_s + half * 32, sv);
+              tmem_ld32(t_dp + half * 32, dv);
+              tmem_wait_ld();
+              if (half == 1) {
+                tc_fence_before();
+                mbar_arrive(&sm.sdp_free);                  // S/dP(j) fully read
+                FCPB_TR(kTrLoaded, (int)tile);
+              }
+              if (plain)
+                softmax_half<false>(sv, dv, l2, dl, sl2, t_p[b], t_ds[b], true, kBQ, -1, half);
+              else
+                softmax_half<true>(sv, dv, l2, dl, sl2, t_p[b], t_ds[b], kv_live, q_valid, shift, half);
+            }
+            tmem_wait_st();
+            tc_fence_before();
             mbar_arrive(&sm.pds_full[b]);
             FCPB_TR(kTrPdsArrive, (int)tile);
             if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
@@ -448,41 +432,14 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       }
     }
   } else if (warp >= 8) {
-    // ------------------------------------------------------------ dQ drain + dK/dV epilogue
-    const int tid = threadIdx.x - 256;            // head-dim lane for dQ^T, kv row for dK/dV
+    // ------------------------------------------------------------ dK/dV epilogue
+    const int tid = threadIdx.x - 256;            // kv row
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint32_t tile = 0, acc_phase = 0;
-    uint32_t dq_phase[2] = {0, 0};
+    uint32_t acc_phase = 0;
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const Item it = p.items[g / p.num_kv_heads];
-      const int kvh = g % p.num_kv_heads;
+      const Item it = p.items[item_of(g, p)];
+      const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
-      for (int r = ks.q_begin; r < ks.q_end; ++r) {
-        const QRef qr = p.qrefs[r];
-        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
-          for (int gq = 0; gq < group; ++gq, ++tile) {
-            const uint32_t b = tile & 1;
-            const int h = kvh * group + gq;
-            mbar_wait(&sm.dq_full[b], dq_phase[b]);
-            dq_phase[b] ^= 1;
-            FCPB_TR(kTrDqGot, (int)tile);
-            tc_fence_after();
-            float v[kBQ];
-            tmem_ld64(tmem + lane_bits + kColDQ + b * 64, v);
-            tc_fence_before();
-            mbar_arrive(&sm.dq_free[b]);
-            // rows past the chunk get exact zeros (dS is masked), so no row guard is needed
-            // inside the tensor; rows past the end of the tensor are skipped.
-            float* dst = p.dq + (static_cast<size_t>(qr.q_off + mb * kBQ) * p.num_q_heads + h) * kD + tid;
-            const size_t row_stride = static_cast<size_t>(p.num_q_heads) * kD;
-            const int rows = min(kBQ, p.q_tokens - (qr.q_off + mb * kBQ));
-#pragma unroll
-            for (int q = 0; q < kBQ; ++q)
-              if (q < rows) red_add_f32(dst + q * row_stride, v[q] * p.scale);
-            FCPB_TR(kTrDqDone, (int)tile);
-          }
-        }
-      }
       // ---- dK, dV epilogue (thread == kv row)
       mbar_wait(&sm.acc_full, acc_phase);
       acc_phase ^= 1;

@@ -48,6 +48,7 @@ struct Params {
   int32_t num_items;
   int32_t num_q_heads;
   int32_t num_kv_heads;
+  int32_t head_major;    // grid index -> (item, head pair) mapping
   float scale_log2;      // softmax_scale * log2(e)
   float scale;           // softmax_scale
   __nv_bfloat16* o;      // [Tq, Hq, D]
@@ -55,6 +56,9 @@ struct Params {
   float* o_part;         // [P, Hq, D]
   float* lse_part;       // [P, Hq]
 };
+
+FCPB_DEV int item_of(int g, int hp, const Params& p) { return p.head_major ? g % p.num_items : g / hp; }
+FCPB_DEV int pair_of(int g, int hp, const Params& p) { return p.head_major ? g / p.num_items : g % hp; }
 
 // Number of 128-row KV tiles a Q tile at m-block `mb` visits in `ref`.
 FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
@@ -112,8 +116,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       const uint64_t keep = policy_evict_last();
       uint32_t q_phase = 0, slot = 0, slot_phase = 0;
       for (int g = blockIdx.x; g < total; g += gridDim.x) {
-        const FcpbItem it = p.items[g / head_pairs];
-        const int hp = g % head_pairs;
+        const FcpbItem it = p.items[item_of(g, head_pairs, p)];
+        const int hp = pair_of(g, head_pairs, p);
         const FcpbSegment seg = p.segs[it.seg];
         const int h0 = 2 * hp;
         const int kvh = h0 / group;
@@ -191,7 +195,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     };
 
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const FcpbItem it = p.items[g / head_pairs];
+      const FcpbItem it = p.items[item_of(g, head_pairs, p)];
       const FcpbSegment seg = p.segs[it.seg];
       int n = 0;
       for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
@@ -245,8 +249,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     const float sl2 = p.scale_log2;
 
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
-      const FcpbItem it = p.items[g / head_pairs];
-      const int head = 2 * (g % head_pairs) + h;
+      const FcpbItem it = p.items[item_of(g, head_pairs, p)];
+      const int head = 2 * pair_of(g, head_pairs, p) + h;
       const FcpbSegment seg = p.segs[it.seg];
       float m_run = -INFINITY, l_run = 0.f;
       bool first = true;

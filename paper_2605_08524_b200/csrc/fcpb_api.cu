@@ -8,6 +8,7 @@
 
 #include "../../include/fcpb.h"
 #include "attn_bwd_sm100.cuh"
+#include "attn_dq_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
 #include "aux_kernels.cuh"
 
@@ -80,6 +81,8 @@ int sm_count() {
 
 constexpr size_t kFwdSmem = sizeof(fcpb::fwd::Smem) + 1024;
 constexpr size_t kBwdSmem = sizeof(fcpb::bwd::Smem) + 1024;
+constexpr size_t kDqSmem = sizeof(fcpb::dq::Smem) + 1024;
+static_assert(kDqSmem <= 232448, "dq smem budget");
 static_assert(kFwdSmem <= 232448, "fwd smem budget");
 static_assert(kBwdSmem <= 232448, "bwd smem budget");
 
@@ -131,6 +134,7 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   p.lse = a->lse;
   p.o_part = a->o_partial;
   p.lse_part = a->lse_partial;
+  p.head_major = a->head_major;
   static bool attr = false;
   if (!attr) {
     FCPB_CUDA(cudaFuncSetAttribute(fcpb::fwd::attn_fwd_kernel,
@@ -181,7 +185,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.delta_t = a->delta_t;
   p.t_pad = a->t_pad;
   p.q_tokens = static_cast<int32_t>(a->q_tokens);
-  p.dq = a->dq_accum;
+  p.head_major = a->head_major;
   p.dk = a->dk_accum;
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
@@ -197,6 +201,57 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   if (grid > total) grid = total;
   fcpb::bwd::attn_bwd_kernel<<<grid, fcpb::bwd::kThreads, kBwdSmem,
                                static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, p);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
+  if (!a) return fail(FCPB_ERR_INVALID, "null args");
+  if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d (need 128)", a->head_dim);
+  if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
+    return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
+  if (a->num_items <= 0) return FCPB_OK;
+  if (a->t_pad < a->q_tokens || !a->lse2_t || !a->delta_t)
+    return fail(FCPB_ERR_INVALID, "lse2_t/delta_t/t_pad missing (run fcpb_bwd_preprocess)");
+  const int H = a->num_q_heads, Hk = a->num_kv_heads;
+  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
+  int rc;
+  if ((rc = make_map(&tq, a->q, a->q_tokens, H, 128, fcpb::dq::kBM))) return rc;
+  if ((rc = make_map(&tdo, a->dout, a->q_tokens, H, 128, fcpb::dq::kBM))) return rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, Hk, 128, fcpb::dq::kBN))) return rc;
+  if ((rc = make_map(&tv, a->v, a->kv_tokens, Hk, 128, fcpb::dq::kBN))) return rc;
+  const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
+  if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     Hk, 128, fcpb::dq::kBN)))
+    return rc;
+  if ((rc = make_map(&tvr, has_recv ? a->v_recv : a->v, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     Hk, 128, fcpb::dq::kBN)))
+    return rc;
+  fcpb::dq::Params p;
+  p.segs = a->segments;
+  p.kvrefs = a->kv_refs;
+  p.items = a->items;
+  p.num_items = a->num_items;
+  p.num_q_heads = H;
+  p.num_kv_heads = Hk;
+  p.scale = a->softmax_scale;
+  p.scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  p.lse2_t = a->lse2_t;
+  p.delta_t = a->delta_t;
+  p.t_pad = a->t_pad;
+  p.dq = static_cast<__nv_bfloat16*>(a->dq);
+  p.head_major = a->head_major;
+  static bool attr = false;
+  if (!attr) {
+    FCPB_CUDA(cudaFuncSetAttribute(fcpb::dq::attn_dq_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqSmem));
+    attr = true;
+  }
+  const int total = a->num_items * H;
+  int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
+  if (grid > total) grid = total;
+  fcpb::dq::attn_dq_kernel<<<grid, fcpb::dq::kThreads, kDqSmem, static_cast<cudaStream_t>(stream)>>>(
+      tq, tdo, tk, tv, tkr, tvr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
@@ -265,6 +320,10 @@ int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64
 // Debug builds only (not part of include/fcpb.h): copy the bwd timeline of CTA 0.
 __attribute__((visibility("default"))) int fcpb_debug_bwd_trace(unsigned long long* host, int n) {
   FCPB_CUDA(cudaMemcpyFromSymbol(host, fcpb::bwd::g_trace, sizeof(unsigned long long) * n));
+  return FCPB_OK;
+}
+__attribute__((visibility("default"))) int fcpb_debug_dq_trace(unsigned long long* host, int n) {
+  FCPB_CUDA(cudaMemcpyFromSymbol(host, fcpb::dq::g_trace, sizeof(unsigned long long) * n));
   return FCPB_OK;
 }
 #endif

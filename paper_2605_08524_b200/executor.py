@@ -10,8 +10,9 @@ forward   compute stream: wave -1 (local tiles, no dependency) is launched first
                           arrived with stage s), ... then K3 merges the partials.
           All received KV stays resident (it is reused by the backward), so the
           transfer pipeline is never throttled by buffer reuse.
-backward  compute: preprocess -> K2 over *received* KV chunks (their dK/dV partials
-          are owed to the owners) -> event -> K2 over local KV chunks;
+backward  compute: preprocess -> K2 dK/dV over *received* KV chunks (their partials
+          are owed to the owners) -> event -> K2 dK/dV over local KV chunks ->
+          K2b query-stationary dQ over all resident KV;
           comm:    after the event, every edge reversed: partials go back to the
           owners (K6), who add them with K4 once their local K2 finished.
 
@@ -101,10 +102,10 @@ class FcpExecutor:
     def backward(self, q, k, v, o, lse, do):
         op = self.op
         cur = torch.cuda.current_stream(self.device)
-        prep, dq = op.backward_prepare(o, lse, do, cur)
+        prep = op.backward_prepare(o, lse, do, cur)
         dk, dv = op.alloc_dkv(False)
         dk_r, dv_r = op.alloc_dkv(True)
-        args = (q, k, v, self.k_recv, self.v_recv, prep, do, dq, dk, dv, dk_r, dv_r, cur)
+        args = (q, k, v, self.k_recv, self.v_recv, prep, do, dk, dv, dk_r, dv_r, cur)
         staged = None
         if self.world > 1 and self.stages:
             op.backward_launch(True, *args)
@@ -117,12 +118,13 @@ class FcpExecutor:
                                                       self.ret_rows, self.group))
             staged = (sk, sv)
         op.backward_launch(False, *args)
+        dq = op.backward_dq(q, k, v, self.k_recv, self.v_recv, prep, do, cur)
         if staged is not None:
             cur.wait_stream(self.comm)
             if self.ret_tokens:
                 op.reduce_dkv(dk, staged[0], self.ret_dst, cur)
                 op.reduce_dkv(dv, staged[1], self.ret_dst, cur)
-        return op.to_bf16(dq, cur), op.to_bf16(dk, cur), op.to_bf16(dv, cur)
+        return dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur)
 
     def step(self, q, k, v, do):
         """One attention layer fwd+bwd; returns (o, lse, dq, dk, dv)."""

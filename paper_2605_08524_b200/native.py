@@ -28,7 +28,7 @@ class FwdArgs(ctypes.Structure):
                 ("segments", c_vp), ("num_segments", c_i32),
                 ("kv_refs", c_vp), ("num_kv_refs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
-                ("num_ctas", c_i32)]
+                ("num_ctas", c_i32), ("head_major", c_i32)]
 
 
 class MergeArgs(ctypes.Structure):
@@ -51,10 +51,24 @@ class BwdArgs(ctypes.Structure):
                 ("kvsegs", c_vp), ("num_kvsegs", c_i32),
                 ("qrefs", c_vp), ("num_qrefs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
-                ("num_ctas", c_i32)]
+                ("num_ctas", c_i32), ("head_major", c_i32)]
 
 
-EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_lse_merge", "fcpb_bwd_preprocess",
+class DqArgs(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
+                ("softmax_scale", c_f32),
+                ("q", c_vp), ("dout", c_vp),
+                ("lse2_t", c_vp), ("delta_t", c_vp), ("t_pad", c_i64), ("q_tokens", c_i64),
+                ("k", c_vp), ("v", c_vp), ("kv_tokens", c_i64),
+                ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
+                ("dq", c_vp),
+                ("segments", c_vp), ("num_segments", c_i32),
+                ("kv_refs", c_vp), ("num_kv_refs", c_i32),
+                ("items", c_vp), ("num_items", c_i32),
+                ("num_ctas", c_i32), ("head_major", c_i32)]
+
+
+EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_lse_merge", "fcpb_bwd_preprocess",
            "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_last_error", "fcpb_version",
            "fcpb_device_supported")
 
@@ -72,6 +86,7 @@ def load(path: str | None = None):
     lib = ctypes.CDLL(p)
     lib.fcpb_attn_fwd.argtypes = [ctypes.POINTER(FwdArgs), c_vp]
     lib.fcpb_attn_bwd.argtypes = [ctypes.POINTER(BwdArgs), c_vp]
+    lib.fcpb_attn_bwd_dq.argtypes = [ctypes.POINTER(DqArgs), c_vp]
     lib.fcpb_lse_merge.argtypes = [ctypes.POINTER(MergeArgs), c_vp]
     lib.fcpb_bwd_preprocess.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32,
                                          c_i32, c_vp]

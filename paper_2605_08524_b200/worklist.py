@@ -14,10 +14,11 @@ times (``simulator.py:73-109``).  For rank ``r``:
   with coalesced stage s.  A Q chunk whose tiles span several waves writes one
   fp32 partial (O, LSE) per wave, merged by K3 afterwards; a Q chunk served by
   a single wave writes its final bf16 O directly.
-* **Backward.**  Work is keyed by KV chunk (local or received): the KV block
-  iterates over every local Q chunk attending to it.  Received chunks form
+* **Backward.**  dK/dV work is keyed by KV chunk (local or received): the KV
+  block iterates over every local Q chunk attending to it.  Received chunks form
   their own launch so their dK/dV partials can travel back along the reversed
-  plan edges while the local chunks compute.
+  plan edges while the local chunks compute.  dQ is query-stationary: one
+  segment per local Q chunk over all of its (by then resident) KV chunks.
 
 Work items are sorted longest-first (LPT over the persistent grid).
 """
@@ -86,11 +87,22 @@ class BwdLaunch:
 
 
 @dataclass
+class DqPlan:
+    """Query-stationary dQ launch: one segment per local Q chunk listing ALL its KV
+    chunks (local and received), same record layout as the forward tables."""
+    segments: np.ndarray         # int32 [S, 6]
+    kvrefs: np.ndarray           # int32 [R, 4]
+    items: np.ndarray            # int32 [I, 2]: seg mblock (LPT order)
+    pairs: int
+
+
+@dataclass
 class RankWork:
     layout: RankLayout
     fwd: FwdPlan
     bwd: list[BwdLaunch] = field(default_factory=list)
     pairs: int = 0
+    dq: DqPlan | None = None
 
 
 def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
@@ -140,6 +152,12 @@ def _lpt_order(items):
     grouped order was measured slower on B200: more dQ reduce contention, worse
     tail balance.)
     """
+    import os
+    if os.environ.get("FCPB_ORDER", "lpt") == "seq":     # experiment knob
+        seq_cost: dict[int, int] = {}
+        for cost, _, _, seq in items:
+            seq_cost[seq] = seq_cost.get(seq, 0) + cost
+        return sorted(items, key=lambda t: (-seq_cost[t[3]], t[3], -t[0], t[1], t[2]))
     return sorted(items, key=lambda t: (-t[0], t[1], t[2]))
 
 
@@ -249,8 +267,36 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
     return launches
 
 
+def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
+    deps = result.deps
+    causal = deps.mask == CAUSAL
+    segs, refs, items, pairs = [], [], [], 0
+    for q in lay.chunks:
+        qn = deps.chunk_tokens[q]
+        begin = len(refs)
+        for kv in deps.q_to_kv[q]:
+            _, off, flags = _kv_location(lay, kv)
+            if causal and kv == q:
+                flags |= KV_DIAG
+            refs.append((off, deps.chunk_tokens[kv], flags, 0))
+            pairs += tile_token_pairs(qn, deps.chunk_tokens[kv], bool(flags & KV_DIAG))
+        sidx = len(segs)
+        segs.append((lay.offset[q], qn, begin, len(refs), -1, 0))
+        for mb in range(_cdiv(qn, TILE)):
+            cost = 0
+            for off, kn, flags, _ in refs[begin:]:
+                nt = _cdiv(kn, TILE)
+                cost += min(nt, mb + 1) if flags & KV_DIAG else nt
+            items.append((cost, sidx, mb, q[0]))
+    items = _lpt_order(items)
+    return DqPlan(np.asarray(segs, dtype=np.int32).reshape(-1, 6),
+                  np.asarray(refs, dtype=np.int32).reshape(-1, 4),
+                  np.asarray([(s_, m) for _, s_, m, _ in items], dtype=np.int32).reshape(-1, 2),
+                  pairs)
+
+
 def build_rank_work(result: ScheduleResult, rank: int) -> RankWork:
     lay = rank_layout(result, rank)
     fwd = build_forward(result, lay)
     bwd = build_backward(result, lay)
-    return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves))
+    return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves), build_dq(result, lay))

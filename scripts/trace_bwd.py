@@ -4,7 +4,7 @@ import numpy as np
 import torch
 sys.path.insert(0, ".")
 from paper_2605_08524_b200 import native
-native._LIB_PATH = os.path.abspath("dbg/libfcpb_trace.so")
+native._LIB_PATH = os.path.abspath(os.environ.get("FCPB_LIB", "dbg/libfcpb_trace.so"))
 import bench
 from paper_2605_08524_b200.executor import FcpExecutor
 w, r = bench.build_workload("c2", 1, None)
@@ -22,7 +22,28 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(len(EV), T).astype(np.int64)
 t0 = a[a > 0].min()
 a = np.where(a > 0, a - t0, -1)
 print("tile " + " ".join(f"{e:>9s}" for e in EV))
-for j in range(0, 120):
+for j in range(0, int(os.environ.get("NPRINT", "120"))):
     print(f"{j:4d} " + " ".join(f"{a[e, j]:9d}" for e in range(len(EV))))
 d = np.diff(a[EV.index("AccIssue"), 20:120])
 print("median AccIssue period (cycles):", np.median(d))
+dd = a[EV.index("DqDone"), 20:120] - a[EV.index("DqGot"), 20:120]
+print("median drain (cycles):", np.median(dd))
+import time
+s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s0.record()
+for _ in range(5):
+    ex.step(q, k, v, do)
+e0.record(); torch.cuda.synchronize()
+print("step ms:", s0.elapsed_time(e0) / 5)
+
+EV2 = ["KIssue", "KGot", "SdpIssue", "DsGot", "DqIssue", "SdpGot", "Freed", "DsArrive"]
+buf2 = (ctypes.c_ulonglong * (len(EV2) * T))()
+lib.fcpb_debug_dq_trace(buf2, len(EV2) * T)
+b = np.frombuffer(buf2, dtype=np.uint64).reshape(len(EV2), T).astype(np.int64)
+t0 = b[b > 0].min()
+b = np.where(b > 0, b - t0, -1)
+print("dq tile " + " ".join(f"{e:>9s}" for e in EV2))
+for j in range(0, int(os.environ.get("NPRINT2", "30"))):
+    print(f"{j:4d} " + " ".join(f"{b[e, j]:9d}" for e in range(len(EV2))))
+d2 = np.diff(b[EV2.index("DqIssue"), 10:100])
+print("dq median DqIssue period (cycles):", np.median(d2))

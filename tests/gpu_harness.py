@@ -87,13 +87,14 @@ def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True):
     acc = []
     for w, op in enumerate(ops):
         t = loc[w]
-        prep, dqa = op.backward_prepare(t["o"], t["lse"], t["do"])
+        prep = op.backward_prepare(t["o"], t["lse"], t["do"])
         dka, dva = op.alloc_dkv(False)
         dkr, dvr = op.alloc_dkv(True)
         op.backward_launch(True, t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"],
-                           dqa, dka, dva, dkr, dvr)
+                           dka, dva, dkr, dvr)
         op.backward_launch(False, t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"],
-                           dqa, dka, dva, dkr, dvr)
+                           dka, dva, dkr, dvr)
+        dqa = op.backward_dq(t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"])
         acc.append((dqa, dka, dva, dkr, dvr))
     # dKV return along reversed edges + K4 reduce at the owner
     for w, work in enumerate(works):
@@ -109,7 +110,7 @@ def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True):
             ops[o_rank].reduce_dkv(acc[o_rank][2], dvr[a:a + m].contiguous(), rows)
     for w, (work, op) in enumerate(zip(works, ops)):
         lay = work.layout
-        dq_b = op.to_bf16(acc[w][0])
+        dq_b = acc[w][0]
         for c in lay.chunks:
             a, m = lay.offset[c], deps.chunk_tokens[c]
             dq[goff[c]:goff[c] + m] = dq_b[a:a + m].cpu()

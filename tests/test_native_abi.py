@@ -37,7 +37,28 @@ def test_missing_library_fails_loudly(tmp_path):
         native.load(str(tmp_path / "nope.so"))
 
 
-def test_struct_sizes_match_c_layout():
-    # 8-byte aligned pointers / int64 in the same order as include/fcpb.h
-    assert ctypes.sizeof(native.FwdArgs) == 4 * 4 + 8 * 13 + 4 * 2 + 8 + 4 * 2 + 8 + 4 * 2 + 8 - 0 or True
-    assert ctypes.alignment(native.FwdArgs) == 8
+def test_struct_layouts_match_header(tmp_path):
+    """Compile a probe against include/fcpb.h and compare sizeof/offsetof with ctypes."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    fields = {"FcpbFwdArgs": native.FwdArgs, "FcpbMergeArgs": native.MergeArgs,
+              "FcpbBwdArgs": native.BwdArgs}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
+    for cname, py in fields.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0;}")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run([cc, "-std=c11", "-o", str(exe), str(src)], check=True)
+    out = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                       check=True).stdout.splitlines())
+    for cname, py in fields.items():
+        assert int(out[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(out[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
