@@ -17,9 +17,10 @@
 // TMEM: S [0,128) dP [128,256) dQ [256,384) dS0 [384,448) dS1 [448,512).
 // Shared memory holds only TMA-fed operands: Q, dO, a 3-deep K ring and a 2-deep V ring
 // (K(j) stays until dQ(j) has read it; the ring depth hides the ~1,300-cycle TMA latency).
-// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 and w8-11: two softmax/epilogue
-// warpgroups, each owning one 64-column half of every tile (and of dQ) for all 128 rows
-// (a warp reaches TMEM lanes 32*(warp%4)..+31, so both warpgroups cover every row).
+// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, then four softmax/epilogue warpgroups,
+// each owning 32 columns of every tile (and of dQ) for all 128 rows (a warp reaches TMEM
+// lanes 32*(warp%4)..+31, so every warpgroup covers every row).  Four warps per SMSP hide
+// the exp/convert dependency chains that left two warpgroups latency-bound.
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -44,7 +45,9 @@ constexpr int kTile = kBN * kD * 2;          // 32 KB (two SW128 panels of 64 co
 constexpr int kPanel = kTile / 2;
 constexpr int kKSlots = 3;
 constexpr int kVSlots = 2;
-constexpr int kThreads = 384;
+constexpr int kSoftmaxWGs = 4;                   // each owns 128/kSoftmaxWGs columns of a tile
+constexpr int kCols = kBN / kSoftmaxWGs;         // 32
+constexpr int kThreads = 128 + 128 * kSoftmaxWGs;
 constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
 FCPB_DEV constexpr uint32_t col_ds(uint32_t b) { return 384u + 64u * b; }   // bf16 dS, 64 cols
 
@@ -89,28 +92,25 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
 // 64 columns of one query row: dS = exp2(S*c + nlse) * (dP + ndelta) -> 32 bf16 pairs in TMEM
 // (this row's lane, columns t_ds..t_ds+31).  kMask: column validity and causal diagonal.
 template <bool kMask>
-FCPB_DEV void ds_half(const uint32_t (&s)[64], const uint32_t (&dp)[64], float c, float nlse,
+FCPB_DEV void ds_cols(const uint32_t (&s)[kCols], const uint32_t (&dp)[kCols], float c, float nlse,
                       float ndelta, uint32_t t_ds, int col0, int valid, int diag_row) {
   const float2 c2 = make_float2(c, c), nl = make_float2(nlse, nlse), nd = make_float2(ndelta, ndelta);
+  uint32_t pk[kCols / 2];
 #pragma unroll
-  for (int q32 = 0; q32 < 2; ++q32) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int i = q32 * 32 + 2 * u;
-      const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), c2, nl);
-      float p0 = ex2(x.x), p1 = ex2(x.y);
-      if (kMask) {
-        const int cg = col0 + i;
-        p0 = (cg < valid && cg <= diag_row) ? p0 : 0.f;
-        p1 = (cg + 1 < valid && cg + 1 <= diag_row) ? p1 : 0.f;
-      }
-      const float2 d = __fmul2_rn(make_float2(p0, p1),
-                                  __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd));
-      pk[u] = pack_bf16(d.x, d.y);
+  for (int u = 0; u < kCols / 2; ++u) {
+    const int i = 2 * u;
+    const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), c2, nl);
+    float p0 = ex2(x.x), p1 = ex2(x.y);
+    if (kMask) {
+      const int cg = col0 + i;
+      p0 = (cg < valid && cg <= diag_row) ? p0 : 0.f;
+      p1 = (cg + 1 < valid && cg + 1 <= diag_row) ? p1 : 0.f;
     }
-    tmem_st16(t_ds + q32 * 16, pk);
+    const float2 d = __fmul2_rn(make_float2(p0, p1),
+                                __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd));
+    pk[u] = pack_bf16(d.x, d.y);
   }
+  tmem_st16(t_ds, pk);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -146,13 +146,13 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       mbar_init(&sm.v_empty[s], 1);
     }
     mbar_init(&sm.sdp_full, 1);
-    mbar_init(&sm.sdp_free, 256);
+    mbar_init(&sm.sdp_free, 128 * kSoftmaxWGs);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.ds_full[b], 256);
+      mbar_init(&sm.ds_full[b], 128 * kSoftmaxWGs);
       mbar_init(&sm.ds_free[b], 1);
     }
     mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_free, 256);
+    mbar_init(&sm.dq_free, 128 * kSoftmaxWGs);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -284,12 +284,12 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax + epilogue
-    const int half = (warp - 4) >> 2;                      // which 64-column half of the tile
+    const int part = (warp - 4) >> 2;                      // which 32-column slice of the tile
     const int row = (warp & 3) * 32 + lane_id();
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t t_s = tmem + lane_bits + kColS + half * 64;
-    const uint32_t t_dp = tmem + lane_bits + kColDP + half * 64;
-    const uint32_t t_ds0 = tmem + lane_bits + col_ds(0) + half * 32;
+    const uint32_t t_s = tmem + lane_bits + kColS + part * kCols;
+    const uint32_t t_dp = tmem + lane_bits + kColDP + part * kCols;
+    const uint32_t t_ds0 = tmem + lane_bits + col_ds(0) + part * (kCols / 2);
     uint32_t sdp_phase = 0, dq_phase = 0, tile = 0;
     uint32_t dsf_phase[2] = {0, 0};
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
@@ -309,24 +309,17 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           const uint32_t b = tile & 1;
           const int valid = live ? ref.len - t * kBN : 0;    // dead rows contribute nothing
           const bool on_diag = diag && t == it.mblock;
-          // tcgen05.st inside ds_half is .sync.aligned: the path must be warp-uniform
+          // tcgen05.st inside ds_cols is .sync.aligned: the path must be warp-uniform
           const bool plain = __all_sync(0xffffffffu, valid >= kBN && !on_diag);
           const int diag_row = on_diag ? row : kBN;           // col <= row on the diagonal tile
           mbar_wait(&sm.sdp_full, sdp_phase);
           sdp_phase ^= 1;
           FCPB_DQTR(kDqSdpGot, (int)tile);
           tc_fence_after();
-          uint32_t sv[64], dv[64];
-          {
-            uint32_t a0[32], a1[32], b0[32], b1[32];
-            tmem_ld32(t_s, a0);
-            tmem_ld32(t_s + 32, a1);
-            tmem_ld32(t_dp, b0);
-            tmem_ld32(t_dp + 32, b1);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) { sv[i] = a0[i]; sv[32 + i] = a1[i]; dv[i] = b0[i]; dv[32 + i] = b1[i]; }
-          }
+          uint32_t sv[kCols], dv[kCols];
+          tmem_ld32(t_s, sv);
+          tmem_ld32(t_dp, dv);
+          tmem_wait_ld();
           tc_fence_before();
           mbar_arrive(&sm.sdp_free);                          // S/dP(j) in registers
           FCPB_DQTR(kDqFreed, (int)tile);
@@ -334,27 +327,26 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
           dsf_phase[b] ^= 1;
           const uint32_t t_ds = t_ds0 + b * 64;
           if (plain)
-            ds_half<false>(sv, dv, p.scale_log2, nlse, ndel, t_ds, half * 64, kBN, kBN);
+            ds_cols<false>(sv, dv, p.scale_log2, nlse, ndel, t_ds, part * kCols, kBN, kBN);
           else
-            ds_half<true>(sv, dv, p.scale_log2, nlse, ndel, t_ds, half * 64, valid, diag_row);
+            ds_cols<true>(sv, dv, p.scale_log2, nlse, ndel, t_ds, part * kCols, valid, diag_row);
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&sm.ds_full[b]);
           FCPB_DQTR(kDqDsArrive, (int)tile);
         }
       }
-      // ---- epilogue: this warpgroup's 64 columns of dQ * scale -> bf16
+      // ---- epilogue: this warpgroup's 32 columns of dQ * scale -> bf16
       mbar_wait(&sm.dq_full, dq_phase);
       dq_phase ^= 1;
       tc_fence_after();
-      __nv_bfloat16* dst = p.dq + (static_cast<size_t>(seg.q_off + (live ? qpos : 0)) * H + h) * kD + half * 64;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      {
         uint32_t v[32];
-        tmem_ld32(tmem + lane_bits + kColDQ + half * 64 + c * 32, v);
+        tmem_ld32(tmem + lane_bits + kColDQ + part * kCols, v);
         tmem_wait_ld();
         if (live) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+          __nv_bfloat16* dst = p.dq + (static_cast<size_t>(seg.q_off + qpos) * H + h) * kD + part * kCols;
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
             uint4 w;
