@@ -65,6 +65,7 @@ typedef struct {
   const FcpbItem* items;       int32_t num_items;     /* LPT-ordered                  */
   int32_t num_ctas;            /* 0 = one per SM                                      */
   int32_t head_major;          /* grid order: 0 = heads of an item adjacent, 1 = items of a head */
+  int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbFwdArgs;
 
 FCPB_API int fcpb_attn_fwd(const FcpbFwdArgs* args, void* stream);
@@ -114,6 +115,7 @@ typedef struct {
   const FcpbItem* items;       int32_t num_items;
   int32_t num_ctas;
   int32_t head_major;
+  int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbDqArgs;
 
 FCPB_API int fcpb_attn_bwd_dq(const FcpbDqArgs* args, void* stream);
@@ -156,6 +158,7 @@ typedef struct {
   const FcpbBwdItem* items; int32_t num_items;
   int32_t num_ctas;
   int32_t head_major;
+  int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbBwdArgs;
 
 FCPB_API int fcpb_attn_bwd(const FcpbBwdArgs* args, void* stream);

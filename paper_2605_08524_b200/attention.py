@@ -72,6 +72,8 @@ class BlockAttention:
         sched = os.environ.get("FCPB_SCHED", "")   # experiment knob: "f,b,q" head-major flags
         flags = [int(x) for x in sched.split(",")] if sched else [0, 0, 0]
         self.head_major = {"fwd": flags[0], "bwd": flags[1], "dq": flags[2]}
+        # one dynamic-scheduler counter per kernel kind (zeroed by the C ABI before each launch)
+        self._sched = torch.zeros(4, dtype=torch.int32, device=self.device)
 
     # ------------------------------------------------------------------ shapes
     def q_shape(self):
@@ -112,6 +114,7 @@ class BlockAttention:
         a.items, a.num_items = native.ptr(items), len(wave.items)
         a.num_ctas = self.num_ctas
         a.head_major = self.head_major["fwd"]
+        a.sched_counter = self._sched.data_ptr()
         native.check(self.lib.fcpb_attn_fwd(ctypes_ref(a), self._stream(stream)))
         self.launches += 1
 
@@ -187,6 +190,7 @@ class BlockAttention:
         a.items, a.num_items = native.ptr(items), len(d.items)
         a.num_ctas = self.num_ctas
         a.head_major = self.head_major["dq"]
+        a.sched_counter = self._sched.data_ptr() + 8
         native.check(self.lib.fcpb_attn_bwd_dq(ctypes_ref(a), self._stream(stream)))
         self.launches += 1
         return dq
@@ -219,6 +223,7 @@ class BlockAttention:
             a.items, a.num_items = native.ptr(items), len(b.items)
             a.num_ctas = self.num_ctas
             a.head_major = self.head_major["bwd"]
+            a.sched_counter = self._sched.data_ptr() + 4
             native.check(self.lib.fcpb_attn_bwd(ctypes_ref(a), self._stream(stream)))
             self.launches += 1
 

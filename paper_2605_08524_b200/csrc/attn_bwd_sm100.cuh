@@ -71,10 +71,12 @@ struct Smem {
   uint64_t sdp_full, sdp_free;
   uint64_t pds_full[2], pds_free[2];
   uint64_t acc_full, acc_free;
+  SchedRing sched;
   uint32_t tmem_base;
 };
 
 struct Params {
+  int* sched_counter;      // dynamic tile scheduler (zeroed before launch)
   const KvSeg* kvsegs;
   const QRef* qrefs;
   const Item* items;
@@ -210,6 +212,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     }
     mbar_init(&sm.acc_full, 1);
     mbar_init(&sm.acc_free, 128);
+    sched_init(sm.sched, 1 + 8);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -225,7 +228,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const uint64_t keep = policy_evict_last();
     uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
     int ptile = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = __shfl_sync(0xffffffffu, lane == 0 ? sched_produce(sm.sched, sc, p.sched_counter) : 0, 0)) < total;) {
       const Item it = p.items[item_of(g, p)];
       const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
@@ -306,7 +310,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       __syncwarp();
     };
 
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
       const KvSeg ks = p.kvsegs[it.kvseg];
       int n = 0;
@@ -381,7 +386,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const uint32_t t_ds[2] = {tmem + lane_bits + col_ds(0), tmem + lane_bits + col_ds(1)};
     uint32_t sdp_phase = 0, stage = 0, stage_phase = 0, tile = 0;
     uint32_t pfree_phase[2] = {0, 0};
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
       const KvSeg ks = p.kvsegs[it.kvseg];
       const int kv_row = it.nblock * kBK + tid;
@@ -436,7 +442,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const int tid = threadIdx.x - 256;            // kv row
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     uint32_t acc_phase = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
       const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];

@@ -62,10 +62,12 @@ struct Smem {
   uint64_t sdp_full, sdp_free;
   uint64_t ds_full[2], ds_free[2];
   uint64_t dq_full, dq_free;
+  SchedRing sched;
   uint32_t tmem_base;
 };
 
 struct Params {
+  int* sched_counter;      // dynamic tile scheduler (zeroed before launch)
   const FcpbSegment* segs;
   const FcpbKvRef* kvrefs;
   const FcpbItem* items;
@@ -153,6 +155,7 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     }
     mbar_init(&sm.dq_full, 1);
     mbar_init(&sm.dq_free, 128 * kSoftmaxWGs);
+    sched_init(sm.sched, 1 + 4 * kSoftmaxWGs);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -167,7 +170,8 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
       const uint64_t keep = policy_evict_last();
       uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0;
       int ptile = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      SchedCursor sc;
+      for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
         const FcpbItem it = p.items[item_of(g, p)];
         const int h = head_of(g, p);
         const int kvh = h / group;
@@ -212,7 +216,8 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0, sdpf_phase = 0,
              dqf_phase = 0;
     uint32_t ds_phase[2] = {0, 0}, tile = 0;
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const FcpbItem it = p.items[item_of(g, p)];
       const FcpbSegment seg = p.segs[it.seg];
       int n = 0;
@@ -292,7 +297,8 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
     const uint32_t t_ds0 = tmem + lane_bits + col_ds(0) + part * (kCols / 2);
     uint32_t sdp_phase = 0, dq_phase = 0, tile = 0;
     uint32_t dsf_phase[2] = {0, 0};
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const FcpbItem it = p.items[item_of(g, p)];
       const int h = head_of(g, p);
       const FcpbSegment seg = p.segs[it.seg];

@@ -38,10 +38,12 @@ struct Smem {
   uint64_t q_full, q_empty;
   uint64_t kv_full[kSlots], kv_empty[kSlots];
   uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  SchedRing sched;
   uint32_t tmem_base;
 };
 
 struct Params {
+  int* sched_counter;      // dynamic tile scheduler (zeroed before launch)
   const FcpbSegment* segs;
   const FcpbKvRef* kvrefs;
   const FcpbItem* items;
@@ -102,6 +104,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_init(&sm.o_full[h], 1);
       mbar_init(&sm.o_empty[h], 128);
     }
+    sched_init(sm.sched, 1 + 8);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -115,7 +118,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (elect_one()) {
       const uint64_t keep = policy_evict_last();
       uint32_t q_phase = 0, slot = 0, slot_phase = 0;
-      for (int g = blockIdx.x; g < total; g += gridDim.x) {
+      SchedCursor sc;
+      for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
         const FcpbItem it = p.items[item_of(g, head_pairs, p)];
         const int hp = pair_of(g, head_pairs, p);
         const FcpbSegment seg = p.segs[it.seg];
@@ -194,7 +198,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       return cur;
     };
 
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const FcpbItem it = p.items[item_of(g, head_pairs, p)];
       const FcpbSegment seg = p.segs[it.seg];
       int n = 0;
@@ -248,7 +253,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     uint32_t s_phase = 0, o_phase = 0;
     const float sl2 = p.scale_log2;
 
-    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    SchedCursor sc;
+    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const FcpbItem it = p.items[item_of(g, head_pairs, p)];
       const int head = 2 * pair_of(g, head_pairs, p) + h;
       const FcpbSegment seg = p.segs[it.seg];

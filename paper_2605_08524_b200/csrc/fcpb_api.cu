@@ -135,6 +135,9 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   p.o_part = a->o_partial;
   p.lse_part = a->lse_partial;
   p.head_major = a->head_major;
+  if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
+  p.sched_counter = a->sched_counter;
+  FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
   static bool attr = false;
   if (!attr) {
     FCPB_CUDA(cudaFuncSetAttribute(fcpb::fwd::attn_fwd_kernel,
@@ -190,6 +193,9 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
   p.dv_recv = a->dv_recv_accum;
+  if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
+  p.sched_counter = a->sched_counter;
+  FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
   static bool attr = false;
   if (!attr) {
     FCPB_CUDA(cudaFuncSetAttribute(fcpb::bwd::attn_bwd_kernel,
@@ -241,6 +247,9 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   p.t_pad = a->t_pad;
   p.dq = static_cast<__nv_bfloat16*>(a->dq);
   p.head_major = a->head_major;
+  if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
+  p.sched_counter = a->sched_counter;
+  FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
   static bool attr = false;
   if (!attr) {
     FCPB_CUDA(cudaFuncSetAttribute(fcpb::dq::attn_dq_kernel,

@@ -231,6 +231,48 @@ FCPB_DEV void mma_commit(uint64_t* bar) {
                ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ----------------------------------------------------------------------------- dynamic scheduler
+// Persistent CTAs take work items from a global counter (zeroed before the launch), so
+// CTAs that start late -- e.g. while NCCL kernels hold SMs during the exchange -- simply
+// take fewer items.  The producer warp fetches; consumer warps read the item index from
+// a small smem ring.  Index >= total means "no more work".
+constexpr int kSchedSlots = 4;
+struct SchedRing {
+  int32_t item[kSchedSlots];
+  uint64_t full[kSchedSlots];
+  uint64_t empty[kSchedSlots];
+};
+FCPB_DEV void sched_init(SchedRing& r, uint32_t consumer_warps) {
+  for (int i = 0; i < kSchedSlots; ++i) {
+    mbar_init(&r.full[i], 1);
+    mbar_init(&r.empty[i], consumer_warps);
+  }
+}
+struct SchedCursor {
+  uint32_t slot = 0, phase = 0;
+  FCPB_DEV void advance() {
+    if (++slot == kSchedSlots) { slot = 0; phase ^= 1; }
+  }
+};
+// producer (one thread): claim the next item and publish it
+FCPB_DEV int sched_produce(SchedRing& r, SchedCursor& c, int* counter) {
+  mbar_wait(&r.empty[c.slot], c.phase ^ 1);
+  const int g = atomicAdd(counter, 1);
+  r.item[c.slot] = g;
+  mbar_arrive(&r.full[c.slot]);
+  c.advance();
+  return g;
+}
+// consumer (whole warp): read the next item, release the slot once per warp
+FCPB_DEV int sched_consume(SchedRing& r, SchedCursor& c) {
+  mbar_wait(&r.full[c.slot], c.phase);
+  const int g = *reinterpret_cast<volatile int32_t*>(&r.item[c.slot]);
+  __syncwarp();
+  if (lane_id() == 0) mbar_arrive(&r.empty[c.slot]);
+  c.advance();
+  return g;
+}
+
 // ----------------------------------------------------------------------------- math
 FCPB_DEV float ex2(float x) {
   float y;

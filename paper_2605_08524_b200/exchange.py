@@ -101,15 +101,28 @@ def run_return(stages: list[StageOps], partial_bufs, staging_bufs, staging_rows,
 
 
 def return_staging_layout(stages: list[StageOps]):
-    """Rows of the owner-side staging buffer for returned partials, plus the
-    owner's destination row of each staged row (for the K4 reduce)."""
-    rows, dst, pos = {}, [], 0
+    """Owner-side staging for returned dK/dV partials.
+
+    Returns (rows, rounds, total): ``rows[(chunk, peer)]`` is the first staging row of
+    that peer's partial; ``rounds`` is a list of (src_rows, dst_rows) pairs where round
+    k holds the k-th receiver of every chunk, so within a round every destination row
+    appears once (K4 launches per round are race-free and sum in a fixed order).
+    """
+    rows, pos = {}, 0
+    per_chunk: dict = {}
     for st in stages:
         for t in st.sends:
             rows[(t.chunk, t.peer)] = pos
-            dst.extend(range(t.row, t.row + t.tokens))
+            per_chunk.setdefault(t.chunk, []).append((t.row, pos, t.tokens))
             pos += t.tokens
-    return rows, dst, pos
+    rounds: list[tuple[list[int], list[int]]] = []
+    for parts in per_chunk.values():
+        for k, (dst0, src0, n) in enumerate(parts):
+            while len(rounds) <= k:
+                rounds.append(([], []))
+            rounds[k][0].extend(range(src0, src0 + n))
+            rounds[k][1].extend(range(dst0, dst0 + n))
+    return rows, rounds, pos
 
 
 def exchange_bytes(stages: list[StageOps], bytes_per_token: int) -> tuple[int, int]:

@@ -47,8 +47,10 @@ class FcpExecutor:
         self.layout = self.work.layout
         self.op = BlockAttention(self.work, cfg, self.device, softmax_scale, num_ctas)
         self.stages = exchange.build_stage_ops(result, self.layout)
-        self.ret_rows, ret_dst, self.ret_tokens = exchange.return_staging_layout(self.stages)
-        self.ret_dst = torch.tensor(ret_dst, dtype=torch.int32, device=self.device)
+        self.ret_rows, rounds, self.ret_tokens = exchange.return_staging_layout(self.stages)
+        self.ret_rounds = [(torch.tensor(src, dtype=torch.int64, device=self.device),
+                            torch.tensor(dst, dtype=torch.int32, device=self.device))
+                           for src, dst in rounds]
         self.comm = torch.cuda.Stream(device=self.device, priority=-1)
         # wave index by stage
         self.wave_of_stage = {self.op.wave_stage(i): i for i in range(self.op.num_waves)}
@@ -121,9 +123,9 @@ class FcpExecutor:
         dq = op.backward_dq(q, k, v, self.k_recv, self.v_recv, prep, do, cur)
         if staged is not None:
             cur.wait_stream(self.comm)
-            if self.ret_tokens:
-                op.reduce_dkv(dk, staged[0], self.ret_dst, cur)
-                op.reduce_dkv(dv, staged[1], self.ret_dst, cur)
+            for src, dst in self.ret_rounds:        # K4, one race-free round per receiver rank
+                op.reduce_dkv(dk, staged[0].index_select(0, src), dst, cur)
+                op.reduce_dkv(dv, staged[1].index_select(0, src), dst, cur)
         return dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur)
 
     def step(self, q, k, v, do):

@@ -61,7 +61,7 @@ def _worker(rank, world, port, errq):
         assert torch.equal(vr, gather_rank(vg, lay, goff, r.deps, recv=True))
         # reverse: each receiver returns (its rank + chunk data) as the "partial"
         part = kr + 1000.0 * (rank + 1)
-        rows, dst, n_stage = exchange.return_staging_layout(stages)
+        rows, rounds, n_stage = exchange.return_staging_layout(stages)
         staged = torch.zeros((n_stage, MODEL.kv_heads, MODEL.head_dim))
         exchange.wait_all(exchange.run_return(stages, (part,), (staged,), rows))
         for st in stages:
@@ -69,7 +69,11 @@ def _worker(rank, world, port, errq):
                 got = staged[rows[(t.chunk, t.peer)]:rows[(t.chunk, t.peer)] + t.tokens]
                 want = k[t.row:t.row + t.tokens] + 1000.0 * (t.peer + 1)
                 assert torch.equal(got, want), (rank, t)
-        assert len(dst) == n_stage
+        # rounds: every staged row used once; destinations unique within a round
+        srcs = sorted(x for src, _ in rounds for x in src)
+        assert srcs == list(range(n_stage))
+        for _, dst in rounds:
+            assert len(dst) == len(set(dst))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as exc:  # surface the failure in the parent
