@@ -277,6 +277,11 @@ def main():
         ex.step(q, k, v, do)
     torch.cuda.synchronize()
     timing["on"] = False
+    ex.timeline(True)
+    for _ in range(3):
+        ex.step(q, k, v, do)
+    phases = ex.phases()
+    ex.timeline(False)
     # e2e: host buffers in, results out, through the public executor API
     e2e = None
     if not args.no_e2e:
@@ -350,6 +355,7 @@ def main():
                                      "launches": nl[key]} for key in kms},
             "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
             "exchange_bytes_rank0": exb,
+            "phases_ms_rank0": {kk: round(vv, 3) for kk, vv in phases.items()},
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,
             "clocks": clocks.summary(),

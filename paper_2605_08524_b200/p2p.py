@@ -1,0 +1,112 @@
+"""K5/K6 transport: copy-engine pulls from symmetric (IPC-mapped) peer memory over NVLink.
+
+Measured on the B200 box: NCCL grouped send/recv moved the FCP stages at ~45 GB/s
+(2 MB messages, and its kernels compete with the persistent attention kernels for
+SMs), while ``cudaMemcpyAsync`` pulls from a peer's mapped buffer reach ~250 GB/s
+per direction for the same 2 MB chunks with *no* SM use.  Per the north star
+("NCCL grouped send/recv, or in-kernel P2P, whichever measures faster") the executor
+uses the pulls; ``exchange.run_stage`` (torch.distributed P2P) stays as the
+transport-agnostic reference of the same plan that the gloo CPU tests exercise.
+
+Buffers (torch symmetric memory, same size on every rank):
+
+* ``kv``   bf16 [2, T_max, Hkv, D] -- each rank's own K and V (copied in at step start)
+* ``part`` fp32 [2, R_max, Hkv, D] -- dK/dV partials of the chunks a rank *received*
+  (written directly by the dK/dV kernel), pulled back by the chunk owners.
+
+Ordering: a symmetric-memory device barrier after the K/V copy (everyone's K/V is
+readable), after the forward pulls (K/V may be overwritten next step), after the
+partials are written, and after the return pulls.  Each plan edge (reference
+``planner.py:81-102``) becomes exactly one pull of K and one of V in its coalesced
+stage; the Delta-matching guarantees each GPU reads from at most ``degree`` peers
+and is read by at most ``degree`` peers per stage.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+import torch.distributed._symmetric_memory as symm
+
+from .worklist import rank_layout
+
+
+def _append_merged(pulls, pull):
+    """Append (peer, src, dst, n), coalescing with the previous pull when both ranges
+    continue contiguously on the same peer (fewer, larger copy-engine transfers)."""
+    if pulls:
+        pp, ps, pd, pn = pulls[-1]
+        peer, src, dst, n = pull
+        if pp == peer and ps + pn == src and pd + pn == dst:
+            pulls[-1] = (pp, ps, pd, pn + n)
+            return
+    pulls.append(pull)
+
+
+class SymmetricExchange:
+    def __init__(self, result, rank: int, cfg, device, group=None, layouts=None):
+        self.rank = rank
+        self.world = result.assignment.n_workers
+        self.device = device
+        self.group = group or dist.group.WORLD
+        H, D = cfg.kv_heads, cfg.head_dim
+        layouts = layouts or [rank_layout(result, r) for r in range(self.world)]
+        self.layouts = layouts
+        me = layouts[rank]
+        t_max = max(l.tokens for l in layouts)
+        r_max = max(max(l.recv_tokens for l in layouts), 1)
+        self.kv = symm.empty(2 * t_max * H * D, dtype=torch.bfloat16, device=device).view(2, t_max, H, D)
+        self.part = symm.empty(2 * r_max * H * D, dtype=torch.float32, device=device).view(2, r_max, H, D)
+        self.h_kv = symm.rendezvous(self.kv, self.group)
+        self.h_part = symm.rendezvous(self.part, self.group)
+        self.peer_kv = [self.h_kv.get_buffer(p, (2, t_max, H, D), torch.bfloat16)
+                        for p in range(self.world)]
+        self.peer_part = [self.h_part.get_buffer(p, (2, r_max, H, D), torch.float32)
+                          for p in range(self.world)]
+        self.t_local = me.tokens
+        self.r_local = me.recv_tokens
+        # forward pulls, per coalesced stage: (peer, src_row in peer's K/V, dst_row in my arena, n)
+        self.stage_pulls: list[list[tuple[int, int, int, int]]] = []
+        for s, stage in enumerate(result.plan.stages):
+            pulls: list[tuple[int, int, int, int]] = []
+            for e in stage:
+                if e.dst != rank:
+                    continue
+                for c in e.chunks:
+                    if me.recv_stage.get(c) == s:
+                        _append_merged(pulls, (e.src, layouts[e.src].offset[c],
+                                               me.recv_offset[c], me.chunk_tokens[c]))
+            self.stage_pulls.append(pulls)
+
+    # ------------------------------------------------------------------ forward (K5)
+    def publish_kv(self, k, v):
+        """Copy this rank's K/V into its symmetric buffer (compute stream)."""
+        self.kv[0, :self.t_local].copy_(k, non_blocking=True)
+        self.kv[1, :self.t_local].copy_(v, non_blocking=True)
+
+    def barrier(self, which: str = "kv", channel: int = 0):
+        (self.h_kv if which == "kv" else self.h_part).barrier(channel=channel)
+
+    def pull_stage(self, s: int, k_recv, v_recv):
+        """Copy-engine pulls of stage s's KV chunks into the receive arena (current stream)."""
+        for peer, src, dst, n in self.stage_pulls[s]:
+            pk = self.peer_kv[peer]
+            k_recv[dst:dst + n].copy_(pk[0, src:src + n], non_blocking=True)
+            v_recv[dst:dst + n].copy_(pk[1, src:src + n], non_blocking=True)
+
+    # ------------------------------------------------------------------ backward (K6)
+    def partial_views(self):
+        """dK/dV partial buffers for the received chunks (the dK/dV kernel writes them)."""
+        if self.r_local == 0:
+            return None, None
+        return self.part[0, :self.r_local], self.part[1, :self.r_local]
+
+    def pull_returns(self, stages, staging_k, staging_v, staging_rows):
+        """Owner side: pull every receiver's partial of my chunks into staging rows."""
+        for st in stages:
+            for t in st.sends:          # I sent chunk t.chunk to t.peer
+                src = self.layouts[t.peer].recv_offset[t.chunk]
+                r = staging_rows[(t.chunk, t.peer)]
+                pp = self.peer_part[t.peer]
+                staging_k[r:r + t.tokens].copy_(pp[0, src:src + t.tokens], non_blocking=True)
+                staging_v[r:r + t.tokens].copy_(pp[1, src:src + t.tokens], non_blocking=True)
