@@ -105,12 +105,14 @@ def build_workload(name: str, n: int, block: int | None):
 
 
 def rank_inputs(ex, rank, cfg, device, pin=False):
-    g = torch.Generator().manual_seed(1234 + rank)
+    """Q, K, V, dO ~ N(0,1) rounded to bf16, drawn on the device from a generator seeded
+    1234 + rank; pinned host copies only when the e2e leg needs them."""
+    g = torch.Generator(device=device).manual_seed(1234 + rank)
     T, H, Hk, D = ex.tokens, cfg.q_heads, cfg.kv_heads, cfg.head_dim
-    host = [torch.randn((T, h, D), generator=g).to(torch.bfloat16) for h in (H, Hk, Hk, H)]
-    if pin:
-        host = [x.pin_memory() for x in host]
-    return host, [x.to(device) for x in host]
+    dev = [torch.randn((T, h, D), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+           for h in (H, Hk, Hk, H)]
+    host = [x.cpu().pin_memory() for x in dev] if pin else None
+    return host, dev
 
 
 # ---------------------------------------------------------------------------- CPU legs
