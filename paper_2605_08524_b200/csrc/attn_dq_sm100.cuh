@@ -48,6 +48,12 @@ constexpr int kVSlots = 2;
 constexpr int kSoftmaxWGs = 4;                   // each owns 128/kSoftmaxWGs columns of a tile
 constexpr int kCols = kBN / kSoftmaxWGs;         // 32
 constexpr int kThreads = 128 + 128 * kSoftmaxWGs;
+// setmaxnreg split. setmaxnreg.inc can only take registers the CTA was given at launch
+// (kThreads x kRegsLaunch, the __launch_bounds__ allocation: 65536/640 rounded down to 8),
+// so the warpgroup budgets must sum to at most (1 + kSoftmaxWGs) * kRegsLaunch.
+constexpr uint32_t kRegsLaunch = 96, kRegsCtl = 64, kRegsSoftmax = 104;
+static_assert(kRegsCtl + kSoftmaxWGs * kRegsSoftmax <= (1 + kSoftmaxWGs) * kRegsLaunch,
+              "setmaxnreg.inc would wait forever for registers that were never allocated");
 constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256;
 FCPB_DEV constexpr uint32_t col_ds(uint32_t b) { return 384u + 64u * b; }   // bf16 dS, 64 cols
 
@@ -164,131 +170,136 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
-      uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0;
-      int ptile = 0;
+  if (warp < 4) {
+    // producer / MMA warpgroup: few registers, the rest go to the softmax warpgroups
+    reg_dealloc<kRegsCtl>();
+    if (warp == 0) {
+      // ------------------------------------------------------------ TMA producer
+      if (elect_one()) {
+        const uint64_t keep = policy_evict_last();
+        uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0;
+        int ptile = 0;
+        SchedCursor sc;
+        for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
+          const FcpbItem it = p.items[item_of(g, p)];
+          const int h = head_of(g, p);
+          const int kvh = h / group;
+          const FcpbSegment seg = p.segs[it.seg];
+          const int row0 = seg.q_off + it.mblock * kBM;
+          mbar_wait(&sm.qd_empty, q_phase ^ 1);
+          q_phase ^= 1;
+          mbar_arrive_expect_tx(&sm.qd_full, 2 * kTile);
+          for (int half = 0; half < 2; ++half) {
+            tma_load_3d(&sm.q[half * kPanel], &tm_q, &sm.qd_full, half * 64, h, row0);
+            tma_load_3d(&sm.dout[half * kPanel], &tm_do, &sm.qd_full, half * 64, h, row0);
+          }
+          for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
+            const FcpbKvRef ref = p.kvrefs[r];
+            const bool recv = ref.flags & FCPB_KV_RECV;
+            const int nt = kv_tiles(ref, it.mblock);
+            for (int t = 0; t < nt; ++t) {
+              const int krow = ref.off + t * kBN;
+              mbar_wait(&sm.k_empty[kslot], k_phase ^ 1);
+              mbar_arrive_expect_tx(&sm.k_full[kslot], kTile);
+              for (int half = 0; half < 2; ++half)
+                tma_load_3d_hint(&sm.k[kslot][half * kPanel], recv ? &tm_k_recv : &tm_k,
+                                 &sm.k_full[kslot], half * 64, kvh, krow, keep);
+              if (++kslot == kKSlots) { kslot = 0; k_phase ^= 1; }
+              mbar_wait(&sm.v_empty[vslot], v_phase ^ 1);
+              mbar_arrive_expect_tx(&sm.v_full[vslot], kTile);
+              for (int half = 0; half < 2; ++half)
+                tma_load_3d_hint(&sm.v[vslot][half * kPanel], recv ? &tm_v_recv : &tm_v,
+                                 &sm.v_full[vslot], half * 64, kvh, krow, keep);
+              if (++vslot == kVSlots) { vslot = 0; v_phase ^= 1; }
+              FCPB_DQTR(kDqKIssue, ptile); ++ptile;
+            }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ------------------------------------------------------------ MMA issuer
+      const uint32_t id_kk = idesc_bf16_f32(kBM, kBN, false, false);   // S, dP
+      const uint32_t id_dq = idesc_bf16_f32(kBM, kD, false, true);     // dQ += dS K (K MN-major)
+      const uint32_t a_q = smem_u32(sm.q), a_do = smem_u32(sm.dout);
+      const bool leader = elect_one();
+      uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0, sdpf_phase = 0,
+               dqf_phase = 0;
+      uint32_t ds_phase[2] = {0, 0}, tile = 0;
       SchedCursor sc;
-      for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
+      for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
         const FcpbItem it = p.items[item_of(g, p)];
-        const int h = head_of(g, p);
-        const int kvh = h / group;
         const FcpbSegment seg = p.segs[it.seg];
-        const int row0 = seg.q_off + it.mblock * kBM;
-        mbar_wait(&sm.qd_empty, q_phase ^ 1);
+        int n = 0;
+        for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
+        mbar_wait(&sm.qd_full, q_phase);
         q_phase ^= 1;
-        mbar_arrive_expect_tx(&sm.qd_full, 2 * kTile);
-        for (int half = 0; half < 2; ++half) {
-          tma_load_3d(&sm.q[half * kPanel], &tm_q, &sm.qd_full, half * 64, h, row0);
-          tma_load_3d(&sm.dout[half * kPanel], &tm_do, &sm.qd_full, half * 64, h, row0);
-        }
-        for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
-          const FcpbKvRef ref = p.kvrefs[r];
-          const bool recv = ref.flags & FCPB_KV_RECV;
-          const int nt = kv_tiles(ref, it.mblock);
-          for (int t = 0; t < nt; ++t) {
-            const int krow = ref.off + t * kBN;
-            mbar_wait(&sm.k_empty[kslot], k_phase ^ 1);
-            mbar_arrive_expect_tx(&sm.k_full[kslot], kTile);
-            for (int half = 0; half < 2; ++half)
-              tma_load_3d_hint(&sm.k[kslot][half * kPanel], recv ? &tm_k_recv : &tm_k,
-                               &sm.k_full[kslot], half * 64, kvh, krow, keep);
-            if (++kslot == kKSlots) { kslot = 0; k_phase ^= 1; }
-            mbar_wait(&sm.v_empty[vslot], v_phase ^ 1);
-            mbar_arrive_expect_tx(&sm.v_full[vslot], kTile);
-            for (int half = 0; half < 2; ++half)
-              tma_load_3d_hint(&sm.v[vslot][half * kPanel], recv ? &tm_v_recv : &tm_v,
-                               &sm.v_full[vslot], half * 64, kvh, krow, keep);
-            if (++vslot == kVSlots) { vslot = 0; v_phase ^= 1; }
-            FCPB_DQTR(kDqKIssue, ptile); ++ptile;
+        uint32_t prev_k = 0;
+        // dQ(j) += dS(j) K(j), issued once the softmax has formed dS(j)
+        auto issue_dq = [&](bool first_dq, bool last) {
+          const uint32_t bb = (tile - 1) & 1;
+          mbar_wait(&sm.ds_full[bb], ds_phase[bb]);
+          ds_phase[bb] ^= 1;
+          FCPB_DQTR(kDqDsGot, (int)tile - 1);
+          if (first_dq) {                     // the epilogue has drained the previous item's dQ
+            mbar_wait(&sm.dq_free, dqf_phase ^ 1);
+            dqf_phase ^= 1;
           }
+          tc_fence_after();
+          if (leader) {
+            const uint32_t b_k = smem_u32(sm.k[prev_k]);
+  #pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk)
+              mma_ts(tmem + kColDQ, tmem + col_ds(bb) + kk * 8,
+                     smem_desc_sw128(b_k + kk * 2048, kPanel, 1024), id_dq, (!first_dq || kk > 0));
+            mma_commit(&sm.ds_free[bb]);
+            mma_commit(&sm.k_empty[prev_k]);
+            if (last) mma_commit(&sm.dq_full);
+          }
+          __syncwarp();
+          FCPB_DQTR(kDqDqIssue, (int)tile - 1);
+        };
+        for (int j = 0; j < n; ++j) {
+          // S(j), dP(j): the softmax must hold S/dP(j-1) in registers already
+          const uint32_t ks = kslot;
+          mbar_wait(&sm.k_full[ks], k_phase);
+          if (++kslot == kKSlots) { kslot = 0; k_phase ^= 1; }
+          const uint32_t vs = vslot;
+          mbar_wait(&sm.v_full[vs], v_phase);
+          if (++vslot == kVSlots) { vslot = 0; v_phase ^= 1; }
+          FCPB_DQTR(kDqKGot, (int)tile);
+          mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);
+          sdpf_phase ^= 1;
+          tc_fence_after();
+          if (leader) {
+            const uint32_t a_k = smem_u32(sm.k[ks]), a_v = smem_u32(sm.v[vs]);
+  #pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
+              mma_ss(tmem + kColS, smem_desc_sw128(a_q + off, 16, 1024),
+                     smem_desc_sw128(a_k + off, 16, 1024), id_kk, kk > 0);
+            }
+  #pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk) {
+              const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
+              mma_ss(tmem + kColDP, smem_desc_sw128(a_do + off, 16, 1024),
+                     smem_desc_sw128(a_v + off, 16, 1024), id_kk, kk > 0);
+            }
+            mma_commit(&sm.sdp_full);
+            mma_commit(&sm.v_empty[vs]);
+            if (j == n - 1) mma_commit(&sm.qd_empty);   // Q / dO no longer read by this item
+          }
+          __syncwarp();
+          FCPB_DQTR(kDqSdpIssue, (int)tile);
+          if (j > 0) issue_dq(j == 1, false);           // dQ(j-1) overlaps softmax(j)
+          prev_k = ks;
+          ++tile;
         }
+        issue_dq(n == 1, true);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t id_kk = idesc_bf16_f32(kBM, kBN, false, false);   // S, dP
-    const uint32_t id_dq = idesc_bf16_f32(kBM, kD, false, true);     // dQ += dS K (K MN-major)
-    const uint32_t a_q = smem_u32(sm.q), a_do = smem_u32(sm.dout);
-    const bool leader = elect_one();
-    uint32_t q_phase = 0, vslot = 0, v_phase = 0, kslot = 0, k_phase = 0, sdpf_phase = 0,
-             dqf_phase = 0;
-    uint32_t ds_phase[2] = {0, 0}, tile = 0;
-    SchedCursor sc;
-    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
-      const FcpbItem it = p.items[item_of(g, p)];
-      const FcpbSegment seg = p.segs[it.seg];
-      int n = 0;
-      for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
-      mbar_wait(&sm.qd_full, q_phase);
-      q_phase ^= 1;
-      uint32_t prev_k = 0;
-      // dQ(j) += dS(j) K(j), issued once the softmax has formed dS(j)
-      auto issue_dq = [&](bool first_dq, bool last) {
-        const uint32_t bb = (tile - 1) & 1;
-        mbar_wait(&sm.ds_full[bb], ds_phase[bb]);
-        ds_phase[bb] ^= 1;
-        FCPB_DQTR(kDqDsGot, (int)tile - 1);
-        if (first_dq) {                     // the epilogue has drained the previous item's dQ
-          mbar_wait(&sm.dq_free, dqf_phase ^ 1);
-          dqf_phase ^= 1;
-        }
-        tc_fence_after();
-        if (leader) {
-          const uint32_t b_k = smem_u32(sm.k[prev_k]);
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            mma_ts(tmem + kColDQ, tmem + col_ds(bb) + kk * 8,
-                   smem_desc_sw128(b_k + kk * 2048, kPanel, 1024), id_dq, (!first_dq || kk > 0));
-          mma_commit(&sm.ds_free[bb]);
-          mma_commit(&sm.k_empty[prev_k]);
-          if (last) mma_commit(&sm.dq_full);
-        }
-        __syncwarp();
-        FCPB_DQTR(kDqDqIssue, (int)tile - 1);
-      };
-      for (int j = 0; j < n; ++j) {
-        // S(j), dP(j): the softmax must hold S/dP(j-1) in registers already
-        const uint32_t ks = kslot;
-        mbar_wait(&sm.k_full[ks], k_phase);
-        if (++kslot == kKSlots) { kslot = 0; k_phase ^= 1; }
-        const uint32_t vs = vslot;
-        mbar_wait(&sm.v_full[vs], v_phase);
-        if (++vslot == kVSlots) { vslot = 0; v_phase ^= 1; }
-        FCPB_DQTR(kDqKGot, (int)tile);
-        mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);
-        sdpf_phase ^= 1;
-        tc_fence_after();
-        if (leader) {
-          const uint32_t a_k = smem_u32(sm.k[ks]), a_v = smem_u32(sm.v[vs]);
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
-            mma_ss(tmem + kColS, smem_desc_sw128(a_q + off, 16, 1024),
-                   smem_desc_sw128(a_k + off, 16, 1024), id_kk, kk > 0);
-          }
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kPanel + (kk & 3) * 32;
-            mma_ss(tmem + kColDP, smem_desc_sw128(a_do + off, 16, 1024),
-                   smem_desc_sw128(a_v + off, 16, 1024), id_kk, kk > 0);
-          }
-          mma_commit(&sm.sdp_full);
-          mma_commit(&sm.v_empty[vs]);
-          if (j == n - 1) mma_commit(&sm.qd_empty);   // Q / dO no longer read by this item
-        }
-        __syncwarp();
-        FCPB_DQTR(kDqSdpIssue, (int)tile);
-        if (j > 0) issue_dq(j == 1, false);           // dQ(j-1) overlaps softmax(j)
-        prev_k = ks;
-        ++tile;
-      }
-      issue_dq(n == 1, true);
-    }
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------ softmax + epilogue
+    reg_alloc<kRegsSoftmax>();
     const int part = (warp - 4) >> 2;                      // which 32-column slice of the tile
     const int row = (warp & 3) * 32 + lane_id();
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;

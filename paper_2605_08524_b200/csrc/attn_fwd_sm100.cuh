@@ -23,6 +23,18 @@
 namespace fcpb {
 namespace fwd {
 
+#ifdef FCPB_TRACE
+constexpr int kTraceTiles = 256;
+enum FwdEv { kFwKGot, kFwS0Issue, kFwP0Got, kFwPv0Issue, kFwP1Got, kFwPv1Issue, kFwS0Got, kFwP0Arrive,
+             kFwS1Got, kFwP1Arrive, kFwEvents };
+__device__ unsigned long long g_trace[kFwEvents * kTraceTiles];
+#define FCPB_FWTR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
+    ((ev) < kFwS0Got ? true : (threadIdx.x == 128 || threadIdx.x == 256))) \
+    g_trace[(ev) * kTraceTiles + (j)] = clock64(); } while (0)
+#else
+#define FCPB_FWTR(ev, j) do {} while (0)
+#endif
+
 constexpr int kD = 128;          // head dim
 constexpr int kBM = 128;         // query rows per tile
 constexpr int kBN = 128;         // kv rows per tile
@@ -69,6 +81,13 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
   return n;
 }
 
+// setmaxnreg split: one producer/MMA warpgroup, two softmax warpgroups.  setmaxnreg.inc can
+// only take registers the CTA was given at launch (384 threads x 168, the __launch_bounds__
+// allocation), so the budgets must sum to at most 3 * kRegsLaunch.
+constexpr uint32_t kRegsLaunch = 168, kRegsCtl = 104, kRegsSoftmax = 200;
+static_assert(kRegsCtl + 2 * kRegsSoftmax <= 3 * kRegsLaunch,
+              "setmaxnreg.inc would wait forever for registers that were never allocated");
+
 __global__ void __launch_bounds__(kThreads, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                 const __grid_constant__ CUtensorMap tm_k,
@@ -113,144 +132,160 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
-      uint32_t q_phase = 0, slot = 0, slot_phase = 0;
-      SchedCursor sc;
-      for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
-        const FcpbItem it = p.items[item_of(g, head_pairs, p)];
-        const int hp = pair_of(g, head_pairs, p);
-        const FcpbSegment seg = p.segs[it.seg];
-        const int h0 = 2 * hp;
-        const int kvh = h0 / group;
-        const int row0 = seg.q_off + it.mblock * kBM;
-        mbar_wait(&sm.q_empty, q_phase ^ 1);
-        q_phase ^= 1;
-        mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
-        for (int h = 0; h < 2; ++h)
-          for (int half = 0; half < 2; ++half)
-            tma_load_3d(&sm.q[h][half * kHalfBytes], &tm_q, &sm.q_full, half * 64, h0 + h, row0);
-        for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
-          const FcpbKvRef ref = p.kvrefs[r];
-          const bool recv = ref.flags & FCPB_KV_RECV;
-          const CUtensorMap* mk = recv ? &tm_k_recv : &tm_k;
-          const CUtensorMap* mv = recv ? &tm_v_recv : &tm_v;
-          const int nt = kv_tiles(ref, it.mblock);
-          for (int t = 0; t < nt; ++t) {
-            const int krow = ref.off + t * kBN;
-            for (int kv = 0; kv < 2; ++kv) {
-              mbar_wait(&sm.kv_empty[slot], slot_phase ^ 1);
-              mbar_arrive_expect_tx(&sm.kv_full[slot], kTileBytes);
-              const CUtensorMap* m = kv ? mv : mk;
-              for (int half = 0; half < 2; ++half)
-                tma_load_3d_hint(&sm.kv[slot][half * kHalfBytes], m, &sm.kv_full[slot], half * 64,
-                                 kvh, krow, keep);
-              if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+  if (warp < 4) {
+    // producer / MMA warpgroup: few registers, the rest go to the softmax warpgroups
+    reg_dealloc<kRegsCtl>();
+    if (warp == 0) {
+      // ------------------------------------------------------------ TMA producer
+      if (elect_one()) {
+        const uint64_t keep = policy_evict_last();
+        uint32_t q_phase = 0, slot = 0, slot_phase = 0;
+        SchedCursor sc;
+        for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
+          const FcpbItem it = p.items[item_of(g, head_pairs, p)];
+          const int hp = pair_of(g, head_pairs, p);
+          const FcpbSegment seg = p.segs[it.seg];
+          const int h0 = 2 * hp;
+          const int kvh = h0 / group;
+          const int row0 = seg.q_off + it.mblock * kBM;
+          mbar_wait(&sm.q_empty, q_phase ^ 1);
+          q_phase ^= 1;
+          mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
+          for (int h = 0; h < 2; ++h)
+            for (int half = 0; half < 2; ++half)
+              tma_load_3d(&sm.q[h][half * kHalfBytes], &tm_q, &sm.q_full, half * 64, h0 + h, row0);
+          for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
+            const FcpbKvRef ref = p.kvrefs[r];
+            const bool recv = ref.flags & FCPB_KV_RECV;
+            const CUtensorMap* mk = recv ? &tm_k_recv : &tm_k;
+            const CUtensorMap* mv = recv ? &tm_v_recv : &tm_v;
+            const int nt = kv_tiles(ref, it.mblock);
+            for (int t = 0; t < nt; ++t) {
+              const int krow = ref.off + t * kBN;
+              for (int kv = 0; kv < 2; ++kv) {
+                mbar_wait(&sm.kv_empty[slot], slot_phase ^ 1);
+                mbar_arrive_expect_tx(&sm.kv_full[slot], kTileBytes);
+                const CUtensorMap* m = kv ? mv : mk;
+                for (int half = 0; half < 2; ++half)
+                  tma_load_3d_hint(&sm.kv[slot][half * kHalfBytes], m, &sm.kv_full[slot], half * 64,
+                                   kvh, krow, keep);
+                if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+              }
             }
           }
         }
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t id_s = idesc_bf16_f32(kBM, kBN, false, false);
-    const uint32_t id_o = idesc_bf16_f32(kBM, kD, false, true);
-    const uint32_t q_addr[2] = {smem_u32(sm.q[0]), smem_u32(sm.q[1])};
-    const uint32_t col_s[2] = {kColS0, kColS1};
-    const uint32_t col_o[2] = {kColO0, kColO1};
-    uint32_t q_phase = 0, slot = 0, slot_phase = 0, p_phase = 0, oe_phase = 0;
-    const bool leader = elect_one();
-    auto issue_s = [&](int h, uint32_t kslot) {
-      if (leader) {
-        const uint32_t kb = smem_u32(sm.kv[kslot]);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          mma_ss(tmem + col_s[h], smem_desc_sw128(q_addr[h] + off, 16, 1024),
-                 smem_desc_sw128(kb + off, 16, 1024), id_s, kk > 0);
+    } else if (warp == 1) {
+      // ------------------------------------------------------------ MMA issuer
+      const uint32_t id_s = idesc_bf16_f32(kBM, kBN, false, false);
+      const uint32_t id_o = idesc_bf16_f32(kBM, kD, false, true);
+      const uint32_t q_addr0 = smem_u32(sm.q[0]), q_addr1 = smem_u32(sm.q[1]);
+      // selects, not arrays: a runtime-indexed array would live in local memory
+      auto q_addr = [&](int h) { return h ? q_addr1 : q_addr0; };
+      auto col_s = [](int h) { return h ? kColS1 : kColS0; };
+      auto col_o = [](int h) { return h ? kColO1 : kColO0; };
+      uint32_t q_phase = 0, slot = 0, slot_phase = 0, p_phase = 0, oe_phase = 0;
+      int trt = 0;   // trace tile counter
+      const bool leader = elect_one();
+      auto issue_s = [&](int h, uint32_t kslot) {
+        if (leader) {
+          const uint32_t kb = smem_u32(sm.kv[kslot]);
+  #pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+            mma_ss(tmem + col_s(h), smem_desc_sw128(q_addr(h) + off, 16, 1024),
+                   smem_desc_sw128(kb + off, 16, 1024), id_s, kk > 0);
+          }
+          mma_commit(&sm.s_full[h]);
         }
-        mma_commit(&sm.s_full[h]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int h, uint32_t vslot, bool acc) {
-      if (leader) {
-        const uint32_t vb = smem_u32(sm.kv[vslot]);
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          mma_ts(tmem + col_o[h], tmem + col_s[h] + kk * 8,
-                 smem_desc_sw128(vb + kk * 2048, kHalfBytes, 1024), id_o, (acc || kk > 0));
+        __syncwarp();
+      };
+      auto issue_pv = [&](int h, uint32_t vslot, bool acc) {
+        if (leader) {
+          const uint32_t vb = smem_u32(sm.kv[vslot]);
+  #pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            mma_ts(tmem + col_o(h), tmem + col_s(h) + kk * 8,
+                   smem_desc_sw128(vb + kk * 2048, kHalfBytes, 1024), id_o, (acc || kk > 0));
+          }
         }
-      }
-      __syncwarp();
-    };
-    auto commit = [&](uint64_t* bar) {
-      if (leader) mma_commit(bar);
-      __syncwarp();
-    };
-    // Take the next ring position and wait until TMA has filled it.
-    auto take_full = [&]() {
-      const uint32_t cur = slot;
-      mbar_wait(&sm.kv_full[cur], slot_phase);
-      if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
-      return cur;
-    };
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (leader) mma_commit(bar);
+        __syncwarp();
+      };
+      // Take the next ring position and wait until TMA has filled it.
+      auto take_full = [&]() {
+        const uint32_t cur = slot;
+        mbar_wait(&sm.kv_full[cur], slot_phase);
+        if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+        return cur;
+      };
 
-    SchedCursor sc;
-    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
-      const FcpbItem it = p.items[item_of(g, head_pairs, p)];
-      const FcpbSegment seg = p.segs[it.seg];
-      int n = 0;
-      for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
-      mbar_wait(&sm.q_full, q_phase);
-      q_phase ^= 1;
-      // O accumulators of the previous item must have been drained by the epilogue.
-      mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
-      mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
-      oe_phase ^= 1;
-      tc_fence_after();
-      // K(0)
-      const uint32_t ks = take_full();
-      tc_fence_after();
-      issue_s(0, ks);
-      issue_s(1, ks);
-      commit(&sm.kv_empty[ks]);
-      if (n == 1) commit(&sm.q_empty);
-      for (int j = 0; j < n; ++j) {
-        const uint32_t vs = take_full();
-        mbar_wait(&sm.p_full[0], p_phase);
+      SchedCursor sc;
+      for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
+        const FcpbItem it = p.items[item_of(g, head_pairs, p)];
+        const FcpbSegment seg = p.segs[it.seg];
+        int n = 0;
+        for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
+        mbar_wait(&sm.q_full, q_phase);
+        q_phase ^= 1;
+        // O accumulators of the previous item must have been drained by the epilogue.
+        mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
+        mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
+        oe_phase ^= 1;
         tc_fence_after();
-        issue_pv(0, vs, j > 0);
-        if (j == n - 1) commit(&sm.o_full[0]);
-        uint32_t ks2 = 0;
-        if (j + 1 < n) {
-          ks2 = take_full();
+        // K(0)
+        const uint32_t ks = take_full();
+        tc_fence_after();
+        issue_s(0, ks);
+        issue_s(1, ks);
+        commit(&sm.kv_empty[ks]);
+        if (n == 1) commit(&sm.q_empty);
+        for (int j = 0; j < n; ++j) {
+          const uint32_t vs = take_full();
+          mbar_wait(&sm.p_full[0], p_phase);
+          FCPB_FWTR(kFwP0Got, trt);
           tc_fence_after();
-          issue_s(0, ks2);
+          issue_pv(0, vs, j > 0);
+          FCPB_FWTR(kFwPv0Issue, trt);
+          if (j == n - 1) commit(&sm.o_full[0]);
+          uint32_t ks2 = 0;
+          if (j + 1 < n) {
+            ks2 = take_full();
+            FCPB_FWTR(kFwKGot, trt + 1);
+            tc_fence_after();
+            issue_s(0, ks2);
+            FCPB_FWTR(kFwS0Issue, trt + 1);
+          }
+          mbar_wait(&sm.p_full[1], p_phase);
+          FCPB_FWTR(kFwP1Got, trt);
+          tc_fence_after();
+          issue_pv(1, vs, j > 0);
+          FCPB_FWTR(kFwPv1Issue, trt);
+          commit(&sm.kv_empty[vs]);
+          if (j == n - 1) commit(&sm.o_full[1]);
+          if (j + 1 < n) {
+            issue_s(1, ks2);
+            commit(&sm.kv_empty[ks2]);
+            if (j + 2 == n) commit(&sm.q_empty);
+          }
+          p_phase ^= 1;
+          ++trt;
         }
-        mbar_wait(&sm.p_full[1], p_phase);
-        tc_fence_after();
-        issue_pv(1, vs, j > 0);
-        commit(&sm.kv_empty[vs]);
-        if (j == n - 1) commit(&sm.o_full[1]);
-        if (j + 1 < n) {
-          issue_s(1, ks2);
-          commit(&sm.kv_empty[ks2]);
-          if (j + 2 == n) commit(&sm.q_empty);
-        }
-        p_phase ^= 1;
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------ softmax + epilogue
+    reg_alloc<kRegsSoftmax>();
     const int h = (warp - 4) >> 2;           // which head of the pair
     const int row = (warp & 3) * 32 + lane_id();
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_bits + (h ? kColS1 : kColS0);
     const uint32_t t_o = tmem + lane_bits + (h ? kColO1 : kColO0);
     uint32_t s_phase = 0, o_phase = 0;
+    int trt = 0;
     const float sl2 = p.scale_log2;
 
     SchedCursor sc;
@@ -267,6 +302,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int t = 0; t < nt; ++t) {
           mbar_wait(&sm.s_full[h], s_phase);
           s_phase ^= 1;
+          if (h == 0) FCPB_FWTR(kFwS0Got, trt); else FCPB_FWTR(kFwS1Got, trt);
           tc_fence_after();
           float s[kBN];
 #pragma unroll
@@ -290,28 +326,34 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           }
           float mp[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) mp[i] = m_run;
+          for (int i = 0; i < 8; ++i) mp[i] = fmax3(m_run, s[2 * i], s[2 * i + 1]);
 #pragma unroll
-          for (int i = 0; i < kBN; ++i) mp[i & 7] = fmaxf(mp[i & 7], s[i]);
-          const float mx = fmaxf(fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3])),
-                                 fmaxf(fmaxf(mp[4], mp[5]), fmaxf(mp[6], mp[7])));
-          const float m_use = (mx == -INFINITY) ? 0.f : mx;
+          for (int i = 16; i < kBN; i += 2) mp[(i >> 1) & 7] = fmax3(mp[(i >> 1) & 7], s[i], s[i + 1]);
+          const float mx = fmax3(fmax3(mp[0], mp[1], mp[2]), fmax3(mp[3], mp[4], mp[5]),
+                                 fmaxf(mp[6], mp[7]));
+          // Lazy rescale (FA4): keep exponentiating against the running reference max
+          // until the row max grows by more than 2^8 in the exp2 domain, so O is
+          // rescaled in TMEM only rarely.  P <= 2^8 stays exact enough in bf16/fp32.
+          float m_use;
+          if (m_run == -INFINITY) m_use = (mx == -INFINITY) ? 0.f : mx;
+          else m_use = ((mx - m_run) * sl2 > 8.f) ? mx : m_run;
           const float neg = -m_use * sl2;
-          float sp[4] = {0.f, 0.f, 0.f, 0.f};
+          float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           // P (bf16 pairs) overwrites the first 64 columns of S, 16 columns per 32 scores.
 #pragma unroll
           for (int c = 0; c < kBN / 32; ++c) {
             uint32_t pk[16];
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              const float a = ex2(fmaf(s[c * 32 + i], sl2, neg));
-              const float b = ex2(fmaf(s[c * 32 + i + 1], sl2, neg));
-              sp[(i >> 1) & 3] += a + b;
-              pk[i / 2] = pack_bf16(a, b);
+              const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
+                                          make_float2(sl2, sl2), make_float2(neg, neg));
+              const float2 e = make_float2(ex2(x.x), ex2(x.y));
+              sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+              pk[i / 2] = pack_bf16(e.x, e.y);
             }
             tmem_st16(t_s + c * 16, pk);
           }
-          const float sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+          const float sum = (sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y);
           const float alpha = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_use) * sl2);
           l_run = l_run * alpha + sum;
           // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.
@@ -327,11 +369,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
               tmem_st32(t_o + c * 32, v);
             }
           }
-          m_run = mx;
+          m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&sm.p_full[h]);
+          if (h == 0) FCPB_FWTR(kFwP0Arrive, trt); else FCPB_FWTR(kFwP1Arrive, trt);
+          ++trt;
         }
       }
       // -------------------------------------------------------- epilogue

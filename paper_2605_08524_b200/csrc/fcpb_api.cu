@@ -335,6 +335,10 @@ __attribute__((visibility("default"))) int fcpb_debug_dq_trace(unsigned long lon
   FCPB_CUDA(cudaMemcpyFromSymbol(host, fcpb::dq::g_trace, sizeof(unsigned long long) * n));
   return FCPB_OK;
 }
+__attribute__((visibility("default"))) int fcpb_debug_fwd_trace(unsigned long long* host, int n) {
+  FCPB_CUDA(cudaMemcpyFromSymbol(host, fcpb::fwd::g_trace, sizeof(unsigned long long) * n));
+  return FCPB_OK;
+}
 #endif
 
 }  // extern "C"

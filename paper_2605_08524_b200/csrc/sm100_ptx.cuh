@@ -279,6 +279,32 @@ FCPB_DEV float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for a pair on the FMA/ALU pipes (x <= 127) (FA4-style MUFU offload): x = j + f, j = rint(x)
+// via the 1.5*2^23 magic add, 2^f on [-0.5, 0.5] by a degree-3 polynomial (max rel err
+// 7.7e-5, far below the bf16 rounding of P), 2^j folded into the exponent bits.
+FCPB_DEV float2 ex2_poly2(float2 x) {
+  // clamp: 2^j is folded into q's exponent (q in [0.7, 1.42], exponent 126..127), so j must
+  // stay >= -125 to remain a normal number; 2^-125 (masked entries) is numerically zero here.
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+  float2 q = __ffma2_rn(make_float2(0.055088766f, 0.055088766f), f,
+                        make_float2(0.24260466f, 0.24260466f));
+  q = __ffma2_rn(q, f, make_float2(0.6932763f, 0.6932763f));
+  q = __ffma2_rn(q, f, make_float2(0.9999289f, 0.9999289f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+
+FCPB_DEV float fmax3(float a, float b, float c) {   // FMNMX3 (sm_100)
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
 FCPB_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

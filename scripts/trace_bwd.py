@@ -47,3 +47,15 @@ for j in range(0, int(os.environ.get("NPRINT2", "30"))):
     print(f"{j:4d} " + " ".join(f"{b[e, j]:9d}" for e in range(len(EV2))))
 d2 = np.diff(b[EV2.index("DqIssue"), 10:100])
 print("dq median DqIssue period (cycles):", np.median(d2))
+
+EV3 = ["KGot", "S0Issue", "P0Got", "Pv0Issue", "P1Got", "Pv1Issue", "S0Got", "P0Arr", "S1Got", "P1Arr"]
+buf3 = (ctypes.c_ulonglong * (len(EV3) * T))()
+lib.fcpb_debug_fwd_trace(buf3, len(EV3) * T)
+c3 = np.frombuffer(buf3, dtype=np.uint64).reshape(len(EV3), T).astype(np.int64)
+t0 = c3[c3 > 0].min()
+c3 = np.where(c3 > 0, c3 - t0, -1)
+print("fwd tile " + " ".join(f"{e:>8s}" for e in EV3))
+for j in range(0, int(os.environ.get("NPRINT3", "20"))):
+    print(f"{j:4d} " + " ".join(f"{c3[e, j]:8d}" for e in range(len(EV3))))
+d3 = np.diff(c3[EV3.index("Pv1Issue"), 5:60])
+print("fwd median period (cycles):", np.median(d3))
