@@ -14,7 +14,13 @@ $(LIB): $(SRCS) $(DEPS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 	@grep -E "registers|spill|bytes stack" build_ptxas.log | head -20
 
-clean:
-	rm -f $(LIB) build_ptxas.log
+# Debug build with clock64 timelines of CTA 0 (scripts/trace_bwd.py); never shipped.
+trace: dbg/libfcpb_trace.so
+dbg/libfcpb_trace.so: $(SRCS) $(DEPS)
+	@mkdir -p dbg
+	$(NVCC) $(NVFLAGS) -DFCPB_TRACE -shared -o $@ $(SRCS) 2> dbg/ptxas.log || (cat dbg/ptxas.log; exit 1)
 
-.PHONY: all clean
+clean:
+	rm -f $(LIB) build_ptxas.log dbg/libfcpb_trace.so
+
+.PHONY: all clean trace

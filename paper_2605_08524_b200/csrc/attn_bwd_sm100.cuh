@@ -1,25 +1,28 @@
-// K2: varlen block-pair attention backward on sm_100a (tcgen05 + TMEM + TMA).
+// K2: varlen block-pair attention backward (dK, dV) on sm_100a (tcgen05 + TMEM + TMA).
 //
 // Work item = one 128-row KV block of one KV chunk (local or received) for one KV
-// head.  The CTA streams every (Q chunk, 64-row Q block, q-head of the GQA group)
+// head.  The CTA streams every (Q chunk, 128-row Q block, q-head of the GQA group)
 // that attends to it; dK/dV accumulate in TMEM and are written once (no atomics).
 // dQ is produced by the query-stationary kernel in attn_dq_sm100.cuh: reducing a
-// 32 KB fp32 dQ partial per tile from here measured ~3,750 cycles per tile on B200
-// (~9 B/clk/SM of reduction throughput, TMA reduce-add and red.global alike), 2.3x
-// the tile's tensor time.
+// fp32 dQ partial per tile from here measured ~9 B/clk/SM of reduction throughput on
+// B200 (TMA reduce-add and red.global alike), 2.3x the tile's tensor time.
 //
-// Per Q tile j (64 query rows):
-//   S^T  = K  Q_j^T   M128 N64  K128 (SS)  -> TMEM S        (fp32)
-//   dP^T = V  dO_j^T  M128 N64  K128 (SS)  -> TMEM dP
-//   softmax WG (thread == kv row): loads S^T, dP^T rows, frees TMEM at once, then
-//        P^T = exp2(S^T*c - lse2[q]),  dS^T = P^T (dP^T - delta[q])   -> bf16 smem
-//        (SW128 rows of 64 q, double buffered)
-//   dV  += P^T  dO_j  M128 N128 K64  (SS)  -> TMEM dV
-//   dK  += dS^T Q_j   M128 N128 K64  (SS)  -> TMEM dK
-// TMEM (512 cols): dV [0,128) dK [128,256) S [256,320) dP [320,384)
-//                  P0 [384,416) dS0 [416,448) P1 [448,480) dS1 [480,512)
-// The tensor pipe computes S/dP of tile j+1 while the softmax of tile j runs.
-// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-7 softmax, w8-11 dK/dV epilogue.
+// Per Q tile j (128 query rows of one q head):
+//   S^T  = K  Q_j^T   M128 N128 K128 (SS)  -> TMEM S  [0,128)    fp32
+//   dP^T = V  dO_j^T  M128 N128 K128 (SS)  -> TMEM dP [128,256)  fp32
+//   softmax (thread == kv row; warpgroup w owns q columns [64w, 64w+64)):
+//     phase 1: P^T = exp2(S^T*c - lse2[q])           -> bf16, in place over its own S columns
+//     phase 2: dS^T = P^T (dP^T - delta[q])           -> bf16, in place over its own dP columns
+//   dV  += P^T  dO_j  M128 N128 K128 (TS, A = P^T from TMEM)  -> TMEM dV [256,384)
+//   dK  += dS^T Q_j   M128 N128 K128 (TS, A = dS^T from TMEM) -> TMEM dK [384,512)
+// N=128 keeps the SS MMAs off the shared-memory operand limit (N=64 SS measured 48 vs 32
+// cycles per instruction), and writing P/dS in place frees the TMEM a second S/dP buffer
+// would need.  Issue order  dV(j), S(j+1), dK(j), dP(j+1):  the tensor pipe is in order, so
+// S(j+1) cannot overwrite P(j) before dV(j) read it, nor dP(j+1) dS(j) before dK(j); and
+// phase 1 of tile j+1 (the exp work) overlaps dK(j)/dP(j+1), phase 2 of tile j overlaps
+// dV(j)/S(j+1).
+// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 softmax (two warpgroups),
+//        w12-15 dK/dV epilogue.
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -30,11 +33,11 @@ namespace bwd {
 #ifdef FCPB_TRACE
 // Debug timeline of CTA 0: [event][tile] clock64 stamps (see scripts/trace_bwd.py).
 constexpr int kTraceTiles = 256;
-enum TraceEv { kTrQdIssue, kTrQdGot, kTrSdpIssue, kTrPdsGot, kTrAccIssue, kTrSdpGot, kTrLoaded,
-               kTrPfreeGot, kTrPdsArrive, kTrDqGot, kTrDqDone, kTrEvents };
+enum TraceEv { kTrQIssue, kTrQGot, kTrSIssue, kTrPGot, kTrDvIssue, kTrDsGot, kTrDkIssue,
+               kTrSGot, kTrPArrive, kTrDpGot, kTrDsArrive, kTrEvents };
 __device__ unsigned long long g_trace[kTrEvents * kTraceTiles];
 #define FCPB_TR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
-    ((ev) < kTrSdpGot || (ev) >= kTrDqGot ? true : threadIdx.x == 128)) \
+    ((ev) < kTrSGot ? true : threadIdx.x == 128)) \
     g_trace[(ev) * kTraceTiles + (j)] = clock64(); } while (0)
 #else
 #define FCPB_TR(ev, j) do {} while (0)
@@ -42,18 +45,28 @@ __device__ unsigned long long g_trace[kTrEvents * kTraceTiles];
 
 constexpr int kD = 128;
 constexpr int kBK = 128;                        // kv rows per item
-constexpr int kBQ = 64;                         // q rows per tile
-constexpr int kKVBytes = kBK * kD * 2;          // 32 KB (two 16 KB SW128 panels)
+constexpr int kBQ = 128;                        // q rows per tile
+constexpr int kKVBytes = kBK * kD * 2;          // 32 KB (two 16 KB SW128 panels of 64 d)
 constexpr int kKVPanel = kKVBytes / 2;
-constexpr int kQBytes = kBQ * kD * 2;           // 16 KB (two 8 KB panels)
+constexpr int kQBytes = kBQ * kD * 2;           // 32 KB (two 16 KB panels)
 constexpr int kQPanel = kQBytes / 2;
-constexpr int kPBytes = kBK * kBQ * 2;          // 16 KB: 128 kv rows x 64 q (one SW128 panel)
-constexpr int kStages = 4;
-constexpr int kThreads = 384;
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColDP = 320;
-// bf16 P^T / dS^T, 32 columns each, double buffered: P_b = 384 + 64b, dS_b = 416 + 64b
-FCPB_DEV constexpr uint32_t col_p(uint32_t b) { return 384u + 64u * b; }
-FCPB_DEV constexpr uint32_t col_ds(uint32_t b) { return 416u + 64u * b; }
+constexpr int kSlots = 2;                       // Q ring and dO ring depth
+constexpr int kSoftmaxWGs = 2;
+constexpr int kCols = kBQ / kSoftmaxWGs;        // q columns per softmax warpgroup
+constexpr int kThreads = 128 * (2 + kSoftmaxWGs);
+constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+// setmaxnreg split.  setmaxnreg.inc can only take registers the CTA was given at launch
+// (kThreads x kRegsLaunch, the __launch_bounds__ allocation), so the budgets must sum to
+// at most 4 * kRegsLaunch.
+constexpr uint32_t kRegsLaunch = 128, kRegsCtl = 96, kRegsEpi = 96, kRegsSoftmax = 160;
+static_assert(kRegsCtl + kRegsEpi + kSoftmaxWGs * kRegsSoftmax <= 4 * kRegsLaunch,
+              "setmaxnreg.inc would wait forever for registers that were never allocated");
+
+// TMEM column of the bf16 A-operand chunk kk (16 q columns = 8 TMEM columns) of P^T / dS^T:
+// warpgroup w keeps its 64 columns in the first 32 TMEM columns of its own S / dP slice.
+FCPB_DEV constexpr uint32_t a_col(uint32_t base, int kk) {
+  return base + static_cast<uint32_t>((kk >> 2) * kCols + (kk & 3) * 8);
+}
 
 struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
 struct QRef { int32_t q_off, q_len, diag, pad_; };
@@ -62,14 +75,14 @@ struct Item { int32_t kvseg, nblock; };
 struct Smem {
   uint8_t k[kKVBytes];
   uint8_t v[kKVBytes];
-  uint8_t q[kStages][kQBytes];
-  uint8_t dout[kStages][kQBytes];
-  float lse2[kStages][kBQ];         // lse * log2(e), per q column
-  float delta[kStages][kBQ];
+  uint8_t q[kSlots][kQBytes];
+  uint8_t dout[kSlots][kQBytes];
+  float lse2[kSlots][kBQ];          // -lse * log2(e), per q column (travels with the Q slot)
+  float delta[kSlots][kBQ];         // -delta (read in phase 2, freed with the Q slot)
   uint64_t kv_full, kv_empty;
-  uint64_t qd_full[kStages], qd_empty[kStages];
-  uint64_t sdp_full, sdp_free;
-  uint64_t pds_full[2], pds_free[2];
+  uint64_t q_full[kSlots], q_empty[kSlots];
+  uint64_t do_full[kSlots], do_empty[kSlots];
+  uint64_t s_full, dp_full, p_full, ds_full;
   uint64_t acc_full, acc_free;
   SchedRing sched;
   uint32_t tmem_base;
@@ -85,8 +98,8 @@ struct Params {
   int32_t head_major;
   float scale;            // softmax scale
   float scale_log2;       // scale * log2(e)
-  const float* lse2_t;    // [Hq, t_pad] lse * log2(e)
-  const float* delta_t;   // [Hq, t_pad]
+  const float* lse2_t;    // [Hq, t_pad] -lse * log2(e)
+  const float* delta_t;   // [Hq, t_pad] -delta
   int64_t t_pad;
   int32_t q_tokens;
   float* dk;              // local  [Tkv, Hkv, D] fp32
@@ -96,12 +109,12 @@ struct Params {
 };
 
 // Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
-// one head (they stream the same Q/dO tiles -> L2 reuse); else the heads of one item.
+// one head (they stream the same Q/dO tiles); else the heads of one item.
 FCPB_DEV int item_of(int g, const Params& p) { return p.head_major ? g % p.num_items : g / p.num_kv_heads; }
 FCPB_DEV int head_of(int g, const Params& p) { return p.head_major ? g / p.num_items : g % p.num_kv_heads; }
 
-// Q blocks (64 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= 2nb.
-FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? 2 * nb : 0; }
+// Q blocks (128 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= nb.
+FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? nb : 0; }
 FCPB_DEV int q_num_blocks(const QRef& qr) { return (qr.q_len + kBQ - 1) / kBQ; }
 
 // 4-byte async copy with zero fill when !valid; completion tracked by an mbarrier.
@@ -114,19 +127,6 @@ FCPB_DEV void cp_async_arrive_noinc(uint64_t* bar) {
                : "memory");
 }
 
-// 32 lanes x 64 columns (two x32 loads), waits for completion.
-FCPB_DEV void tmem_ld64(uint32_t taddr, float (&out)[64]) {
-  uint32_t a[32], b[32];
-  tmem_ld32(taddr, a);
-  tmem_ld32(taddr + 32, b);
-  tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    out[i] = __uint_as_float(a[i]);
-    out[32 + i] = __uint_as_float(b[i]);
-  }
-}
-
 FCPB_DEV float4 lds128(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -134,49 +134,69 @@ FCPB_DEV float4 lds128(uint32_t addr) {
   return v;
 }
 
-// One kv row of one Q tile:  P = exp2(S*c + nlse2[q]),  dS = P (dP + ndelta[q]), packed to
-// bf16 pairs in TMEM (32 columns each: the A operands of the dV / dK matmuls).
-// nlse2 = -lse*log2(e), ndelta = -delta (preprocess).
-// kMask: ragged kv row / ragged q columns / causal diagonal (col >= shift) masking.
+// Phase 1, 32 q columns of one kv row:  P = exp2(S*c + nlse2[q])  -> p (fp32, kept for
+// phase 2) and bf16 pairs stored at t_p.  kMask: ragged kv row / ragged q / causal diagonal.
 template <bool kMask>
-FCPB_DEV void softmax_half(const uint32_t (&s)[32], const uint32_t (&dp)[32], uint32_t l2,
-                           uint32_t dl, float sl2, uint32_t t_p, uint32_t t_ds, bool kv_live,
-                           int q_valid, int shift, int half) {
+FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p, uint32_t t_p,
+                      bool kv_live, int col0, int q_valid, int shift) {
   const float2 c2 = make_float2(sl2, sl2);
-  uint32_t pk[16], dk[16];
+  uint32_t pk[16];
 #pragma unroll
   for (int c8 = 0; c8 < 4; ++c8) {
-    const int cb = half * 32 + c8 * 8;
-    const float4 la = lds128(l2 + cb * 4), lb = lds128(l2 + cb * 4 + 16);
-    const float4 da = lds128(dl + cb * 4), dbv = lds128(dl + cb * 4 + 16);
-    const float2 nl[4] = {make_float2(la.x, la.y), make_float2(la.z, la.w), make_float2(lb.x, lb.y),
-                          make_float2(lb.z, lb.w)};
-    const float2 nd[4] = {make_float2(da.x, da.y), make_float2(da.z, da.w),
-                          make_float2(dbv.x, dbv.y), make_float2(dbv.z, dbv.w)};
+    const float4 la = lds128(l2 + c8 * 32), lb = lds128(l2 + c8 * 32 + 16);
+    const float2 nl[4] = {make_float2(la.x, la.y), make_float2(la.z, la.w),
+                          make_float2(lb.x, lb.y), make_float2(lb.z, lb.w)};
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = c8 * 8 + 2 * u;
-      const int col = half * 32 + i;
       const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), c2, nl[u]);
-      float p0 = ex2(x.x), p1 = ex2(x.y);
+      // Phase 1 is MUFU-bound (2 warps x 64 ex2 per SMSP per tile): every other pair goes
+      // to the FMA pipe (FA4-style), which measured-balances MUFU time against issue slots.
+      float p0, p1;
+      if (u & 1) {
+        const float2 e = ex2_poly2(x);
+        p0 = e.x;
+        p1 = e.y;
+      } else {
+        p0 = ex2(x.x);
+        p1 = ex2(x.y);
+      }
       if (kMask) {
+        const int col = col0 + i;
         p0 = (kv_live && col < q_valid && col >= shift) ? p0 : 0.f;
         p1 = (kv_live && col + 1 < q_valid && col + 1 >= shift) ? p1 : 0.f;
       }
-      const float2 pp = make_float2(p0, p1);
+      p[i] = p0;
+      p[i + 1] = p1;
+      pk[c8 * 4 + u] = pack_bf16(p0, p1);
+    }
+  }
+  tmem_st16(t_p, pk);
+}
+
+// Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds.
+FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, uint32_t t_ds) {
+  uint32_t dk[16];
+#pragma unroll
+  for (int c8 = 0; c8 < 4; ++c8) {
+    const float4 da = lds128(dl + c8 * 32), db = lds128(dl + c8 * 32 + 16);
+    const float2 nd[4] = {make_float2(da.x, da.y), make_float2(da.z, da.w),
+                          make_float2(db.x, db.y), make_float2(db.z, db.w)};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = c8 * 8 + 2 * u;
       const float2 dd = __fmul2_rn(
-          pp, __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd[u]));
-      pk[c8 * 4 + u] = pack_bf16(pp.x, pp.y);
+          make_float2(p[i], p[i + 1]),
+          __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd[u]));
       dk[c8 * 4 + u] = pack_bf16(dd.x, dd.y);
     }
   }
-  tmem_st16(t_p + half * 16, pk);
-  tmem_st16(t_ds + half * 16, dk);
+  tmem_st16(t_ds, dk);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D], box (64,1,64)
-                const __grid_constant__ CUtensorMap tm_do,     // bf16 [Tq,Hq,D], box (64,1,64)
+attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D], box (64,1,128)
+                const __grid_constant__ CUtensorMap tm_do,     // bf16 [Tq,Hq,D], box (64,1,128)
                 const __grid_constant__ CUtensorMap tm_k,      // bf16 [Tkv,Hkv,D], box (64,1,128)
                 const __grid_constant__ CUtensorMap tm_v,
                 const __grid_constant__ CUtensorMap tm_k_recv,
@@ -200,19 +220,19 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   if (warp == 1 && elect_one()) {
     mbar_init(&sm.kv_full, 1);
     mbar_init(&sm.kv_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&sm.qd_full[s], 1 + 32);   // TMA expect_tx arrive + 32 cp.async arrives
-      mbar_init(&sm.qd_empty[s], 1);
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&sm.q_full[s], 1 + 32);   // TMA expect_tx arrive + 32 cp.async arrives
+      mbar_init(&sm.q_empty[s], 1);
+      mbar_init(&sm.do_full[s], 1);
+      mbar_init(&sm.do_empty[s], 1);
     }
-    mbar_init(&sm.sdp_full, 1);
-    mbar_init(&sm.sdp_free, 128);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.pds_full[b], 128);
-      mbar_init(&sm.pds_free[b], 1);
-    }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.dp_full, 1);
+    mbar_init(&sm.p_full, 128 * kSoftmaxWGs);
+    mbar_init(&sm.ds_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.acc_full, 1);
     mbar_init(&sm.acc_free, 128);
-    sched_init(sm.sched, 1 + 8);
+    sched_init(sm.sched, 1 + 4 * kSoftmaxWGs + 4);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -221,171 +241,182 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (all lanes:
-    // lane 0 issues the TMA tiles, every lane copies 2 lse2 + 2 delta values with cp.async)
-    const uint32_t lane = lane_id();
-    const uint64_t keep = policy_evict_last();
-    uint32_t kv_phase = 0, stage = 0, stage_phase = 0;
-    int ptile = 0;
-    SchedCursor sc;
-    for (int g; (g = __shfl_sync(0xffffffffu, lane == 0 ? sched_produce(sm.sched, sc, p.sched_counter) : 0, 0)) < total;) {
-      const Item it = p.items[item_of(g, p)];
-      const int kvh = head_of(g, p);
-      const KvSeg ks = p.kvsegs[it.kvseg];
-      const bool recv = ks.flags & FCPB_KV_RECV;
-      const int krow = ks.kv_off + it.nblock * kBK;
-      mbar_wait(&sm.kv_empty, kv_phase ^ 1);
-      kv_phase ^= 1;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&sm.kv_full, 2 * kKVBytes);
-        for (int half = 0; half < 2; ++half) {
-          tma_load_3d(&sm.k[half * kKVPanel], recv ? &tm_k_recv : &tm_k, &sm.kv_full, half * 64,
-                      kvh, krow);
-          tma_load_3d(&sm.v[half * kKVPanel], recv ? &tm_v_recv : &tm_v, &sm.kv_full, half * 64,
-                      kvh, krow);
-        }
-      }
-      for (int r = ks.q_begin; r < ks.q_end; ++r) {
-        const QRef qr = p.qrefs[r];
-        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
-          const int qrow = qr.q_off + mb * kBQ;
-          for (int gq = 0; gq < group; ++gq) {
-            const int h = kvh * group + gq;
-            mbar_wait(&sm.qd_empty[stage], stage_phase ^ 1);
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&sm.qd_full[stage], 2 * kQBytes);
-              for (int half = 0; half < 2; ++half) {
-                tma_load_3d_hint(&sm.q[stage][half * kQPanel], &tm_q, &sm.qd_full[stage],
-                                 half * 64, h, qrow, keep);
-                tma_load_3d_hint(&sm.dout[stage][half * kQPanel], &tm_do, &sm.qd_full[stage],
-                                 half * 64, h, qrow, keep);
+  if (warp < 4) {
+    reg_dealloc<kRegsCtl>();
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer (all lanes:
+      // lane 0 issues the TMA tiles, every lane copies 4 lse2 + 4 delta values with cp.async)
+      const uint32_t lane = lane_id();
+      const uint64_t keep = policy_evict_last();
+      uint32_t kv_phase = 0, slot = 0, slot_phase = 0;
+      int ptile = 0;
+      SchedCursor sc;
+      for (int g; (g = __shfl_sync(0xffffffffu, lane == 0 ? sched_produce(sm.sched, sc, p.sched_counter) : 0, 0)) < total;) {
+        const Item it = p.items[item_of(g, p)];
+        const int kvh = head_of(g, p);
+        const KvSeg ks = p.kvsegs[it.kvseg];
+        const bool recv = ks.flags & FCPB_KV_RECV;
+        const int krow = ks.kv_off + it.nblock * kBK;
+        bool kv_issued = false;
+        auto issue_kv = [&]() {
+          mbar_wait(&sm.kv_empty, kv_phase ^ 1);
+          kv_phase ^= 1;
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&sm.kv_full, 2 * kKVBytes);
+            for (int half = 0; half < 2; ++half) {
+              tma_load_3d(&sm.k[half * kKVPanel], recv ? &tm_k_recv : &tm_k, &sm.kv_full,
+                          half * 64, kvh, krow);
+              tma_load_3d(&sm.v[half * kKVPanel], recv ? &tm_v_recv : &tm_v, &sm.kv_full,
+                          half * 64, kvh, krow);
+            }
+          }
+          kv_issued = true;
+        };
+        for (int r = ks.q_begin; r < ks.q_end; ++r) {
+          const QRef qr = p.qrefs[r];
+          for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
+            const int qrow = qr.q_off + mb * kBQ;
+            for (int gq = 0; gq < group; ++gq) {
+              const int h = kvh * group + gq;
+              mbar_wait(&sm.q_empty[slot], slot_phase ^ 1);
+              if (lane == 0) {
+                mbar_arrive_expect_tx(&sm.q_full[slot], kQBytes);
+                for (int half = 0; half < 2; ++half)
+                  tma_load_3d_hint(&sm.q[slot][half * kQPanel], &tm_q, &sm.q_full[slot],
+                                   half * 64, h, qrow, keep);
               }
-            }
-            const float* lsrc = p.lse2_t + static_cast<int64_t>(h) * p.t_pad + qrow;
-            const float* dsrc = p.delta_t + static_cast<int64_t>(h) * p.t_pad + qrow;
+              const float* lsrc = p.lse2_t + static_cast<int64_t>(h) * p.t_pad + qrow;
+              const float* dsrc = p.delta_t + static_cast<int64_t>(h) * p.t_pad + qrow;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int i = lane + 32 * u;
-              const bool ok = qrow + i < p.q_tokens;
-              cp_async_4(&sm.lse2[stage][i], ok ? lsrc + i : p.lse2_t, ok);
-              cp_async_4(&sm.delta[stage][i], ok ? dsrc + i : p.delta_t, ok);
+              for (int u = 0; u < kBQ / 32; ++u) {
+                const int i = lane + 32 * u;
+                const bool ok = qrow + i < p.q_tokens;
+                cp_async_4(&sm.lse2[slot][i], ok ? lsrc + i : p.lse2_t, ok);
+                cp_async_4(&sm.delta[slot][i], ok ? dsrc + i : p.delta_t, ok);
+              }
+              cp_async_arrive_noinc(&sm.q_full[slot]);
+              // the first Q tile of an item goes out before K/V (they only wait on the ring)
+              if (!kv_issued) issue_kv();
+              mbar_wait(&sm.do_empty[slot], slot_phase ^ 1);
+              if (lane == 0) {
+                mbar_arrive_expect_tx(&sm.do_full[slot], kQBytes);
+                for (int half = 0; half < 2; ++half)
+                  tma_load_3d_hint(&sm.dout[slot][half * kQPanel], &tm_do, &sm.do_full[slot],
+                                   half * 64, h, qrow, keep);
+              }
+              FCPB_TR(kTrQIssue, ptile); ++ptile;
+              if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
             }
-            cp_async_arrive_noinc(&sm.qd_full[stage]);
-            FCPB_TR(kTrQdIssue, ptile); ++ptile;
-            if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
           }
         }
+        if (!kv_issued) issue_kv();      // (items always have >= 1 tile; keeps phases paired)
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);  // S^T, dP^T
-    const uint32_t id_acc = idesc_bf16_f32(kBK, kD, false, true);    // dV, dK
-    const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v);
-    const bool leader = elect_one();
-    uint32_t kv_phase = 0, stage = 0, stage_phase = 0, sdpf_phase = 0, acc_phase = 0;
-    uint32_t pds_phase[2] = {0, 0};
-    uint32_t tile = 0;   // running Q-tile counter (selects P/dS and dQ buffers)
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer
+      const uint32_t id_sdp = idesc_bf16_f32(kBK, kBQ, false, false);  // S^T, dP^T
+      const uint32_t id_acc = idesc_bf16_f32(kBK, kD, false, true);    // dV, dK (B MN-major)
+      const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v);
+      const bool leader = elect_one();
+      uint32_t kv_phase = 0, slot = 0, slot_phase = 0, acc_phase = 0;
+      uint32_t p_phase = 0, ds_phase = 0;
+      uint32_t tile = 0;
 
-    auto issue_sdp = [&](uint32_t st) {
-      const uint32_t a_q = smem_u32(sm.q[st]), a_do = smem_u32(sm.dout[st]);
-      if (leader) {
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
-          const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32;
-          mma_ss(tmem + kColS, smem_desc_sw128(a_k + oa, 16, 1024),
-                 smem_desc_sw128(a_q + ob, 16, 1024), id_sdp, kk > 0);
-        }
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
-          const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32;
-          mma_ss(tmem + kColDP, smem_desc_sw128(a_v + oa, 16, 1024),
-                 smem_desc_sw128(a_do + ob, 16, 1024), id_sdp, kk > 0);
-        }
-        mma_commit(&sm.sdp_full);
-      }
-      __syncwarp();
-    };
-
-    SchedCursor sc;
-    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
-      const Item it = p.items[item_of(g, p)];
-      const KvSeg ks = p.kvsegs[it.kvseg];
-      int n = 0;
-      for (int r = ks.q_begin; r < ks.q_end; ++r) {
-        const QRef qr = p.qrefs[r];
-        n += (q_num_blocks(qr) - q_first_block(qr, it.nblock)) * group;
-      }
-      mbar_wait(&sm.kv_full, kv_phase);
-      kv_phase ^= 1;
-      // tile 0 of this item: S/dP region must have been read by the previous softmax
-      mbar_wait(&sm.qd_full[stage], stage_phase);
-      FCPB_TR(kTrQdGot, (int)tile);
-      mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);
-      sdpf_phase ^= 1;
-      tc_fence_after();
-      issue_sdp(stage);
-      FCPB_TR(kTrSdpIssue, (int)tile);
-      uint32_t cur_stage = stage;
-      if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
-      for (int j = 0; j < n; ++j, ++tile) {
-        const uint32_t b = tile & 1;
-        const uint32_t st_j = cur_stage;
-        if (j + 1 < n) {
-          mbar_wait(&sm.qd_full[stage], stage_phase);
-          FCPB_TR(kTrQdGot, (int)tile + 1);
-          mbar_wait(&sm.sdp_free, sdpf_phase ^ 1);   // softmax(j) has S/dP(j) in registers
-          sdpf_phase ^= 1;
-          tc_fence_after();
-          issue_sdp(stage);
-          FCPB_TR(kTrSdpIssue, (int)tile + 1);
-          cur_stage = stage;
-          if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
-        }
-        mbar_wait(&sm.pds_full[b], pds_phase[b]);
-        pds_phase[b] ^= 1;
-        FCPB_TR(kTrPdsGot, (int)tile);
-        if (j == 0) {
-          mbar_wait(&sm.acc_free, acc_phase ^ 1);
-          acc_phase ^= 1;
-        }
-        tc_fence_after();
+      // S^T = K Q^T (b = Q slot) or dP^T = V dO^T (b = dO slot): K-major A and B.
+      auto issue_kq = [&](uint32_t a_base, uint32_t b_base, uint32_t col, uint64_t* done) {
         if (leader) {
-          const uint32_t a_q = smem_u32(sm.q[st_j]), a_do = smem_u32(sm.dout[st_j]);
 #pragma unroll
-          for (int kk = 0; kk < kBQ / 16; ++kk)     // dV += P^T dO   (A = P^T in TMEM)
-            mma_ts(tmem + kColDV, tmem + col_p(b) + kk * 8,
-                   smem_desc_sw128(a_do + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
+            const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32;
+            mma_ss(tmem + col, smem_desc_sw128(a_base + oa, 16, 1024),
+                   smem_desc_sw128(b_base + ob, 16, 1024), id_sdp, kk > 0);
+          }
+          mma_commit(done);
+        }
+        __syncwarp();
+      };
+      // dV += P^T dO  /  dK += dS^T Q:  A from TMEM, B = the [q, d] tile (MN-major).
+      auto issue_acc = [&](uint32_t a_base, uint32_t b_base, uint32_t col, bool acc, uint64_t* done) {
+        if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < kBQ / 16; ++kk)     // dK += dS^T Q   (A = dS^T in TMEM)
-            mma_ts(tmem + kColDK, tmem + col_ds(b) + kk * 8,
-                   smem_desc_sw128(a_q + kk * 2048, kQPanel, 1024), id_acc, (j > 0 || kk > 0));
-          mma_commit(&sm.qd_empty[st_j]);
-          mma_commit(&sm.pds_free[b]);
-          FCPB_TR(kTrAccIssue, (int)tile);
+          for (int kk = 0; kk < kBQ / 16; ++kk)
+            mma_ts(tmem + col, tmem + a_col(a_base, kk),
+                   smem_desc_sw128(b_base + kk * 2048, kQPanel, 1024), id_acc, acc || kk > 0);
+          mma_commit(done);
+        }
+        __syncwarp();
+      };
+
+      SchedCursor sc;
+      for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
+        const Item it = p.items[item_of(g, p)];
+        const KvSeg ks = p.kvsegs[it.kvseg];
+        int n = 0;
+        for (int r = ks.q_begin; r < ks.q_end; ++r) {
+          const QRef qr = p.qrefs[r];
+          n += (q_num_blocks(qr) - q_first_block(qr, it.nblock)) * group;
+        }
+        mbar_wait(&sm.kv_full, kv_phase);
+        kv_phase ^= 1;
+        // prologue: S(0), dP(0).  The S/dP regions are free: the previous item's last
+        // dV/dK were issued after its softmax finished with them (in-order pipe).
+        mbar_wait(&sm.q_full[slot], slot_phase);
+        FCPB_TR(kTrQGot, (int)tile);
+        tc_fence_after();
+        issue_kq(a_k, smem_u32(sm.q[slot]), kColS, &sm.s_full);
+        FCPB_TR(kTrSIssue, (int)tile);
+        mbar_wait(&sm.do_full[slot], slot_phase);
+        tc_fence_after();
+        issue_kq(a_v, smem_u32(sm.dout[slot]), kColDP, &sm.dp_full);
+        for (int j = 0; j < n; ++j, ++tile) {
+          const uint32_t cur = slot;
+          if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+          mbar_wait(&sm.p_full, p_phase);
+          p_phase ^= 1;
+          FCPB_TR(kTrPGot, (int)tile);
+          if (j == 0) {
+            mbar_wait(&sm.acc_free, acc_phase ^ 1);   // epilogue drained the previous item
+            acc_phase ^= 1;
+          }
+          tc_fence_after();
+          issue_acc(kColS, smem_u32(sm.dout[cur]), kColDV, j > 0, &sm.do_empty[cur]);
+          FCPB_TR(kTrDvIssue, (int)tile);
+          if (j + 1 < n) {
+            mbar_wait(&sm.q_full[slot], slot_phase);
+            FCPB_TR(kTrQGot, (int)tile + 1);
+            tc_fence_after();
+            issue_kq(a_k, smem_u32(sm.q[slot]), kColS, &sm.s_full);
+            FCPB_TR(kTrSIssue, (int)tile + 1);
+          }
+          mbar_wait(&sm.ds_full, ds_phase);
+          ds_phase ^= 1;
+          FCPB_TR(kTrDsGot, (int)tile);
+          tc_fence_after();
+          issue_acc(kColDP, smem_u32(sm.q[cur]), kColDK, j > 0, &sm.q_empty[cur]);
+          FCPB_TR(kTrDkIssue, (int)tile);
+          if (j + 1 < n) {
+            mbar_wait(&sm.do_full[slot], slot_phase);
+            tc_fence_after();
+            issue_kq(a_v, smem_u32(sm.dout[slot]), kColDP, &sm.dp_full);
+          }
+        }
+        if (leader) {
+          mma_commit(&sm.acc_full);
+          mma_commit(&sm.kv_empty);
         }
         __syncwarp();
       }
-      if (leader) {
-        mma_commit(&sm.acc_full);
-        mma_commit(&sm.kv_empty);
-      }
-      __syncwarp();
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp < 4 + 4 * kSoftmaxWGs) {
     // ------------------------------------------------------------ softmax (thread == kv row)
-    const int tid = threadIdx.x - 128;
+    reg_alloc<kRegsSoftmax>();
+    const int wg = (warp - 4) >> 2;                       // q columns [64 wg, 64 wg + 64)
+    const int tid = ((warp & 3) << 5) + lane_id();        // kv row == TMEM lane
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    const uint32_t t_s = tmem + lane_bits + kColS;
-    const uint32_t t_dp = tmem + lane_bits + kColDP;
+    const uint32_t t_s = tmem + lane_bits + kColS + wg * kCols;
+    const uint32_t t_dp = tmem + lane_bits + kColDP + wg * kCols;
     const float sl2 = p.scale_log2;
-    const uint32_t t_p[2] = {tmem + lane_bits + col_p(0), tmem + lane_bits + col_p(1)};
-    const uint32_t t_ds[2] = {tmem + lane_bits + col_ds(0), tmem + lane_bits + col_ds(1)};
-    uint32_t sdp_phase = 0, stage = 0, stage_phase = 0, tile = 0;
-    uint32_t pfree_phase[2] = {0, 0};
+    uint32_t s_phase = 0, dp_phase = 0, slot = 0, slot_phase = 0, tile = 0;
     SchedCursor sc;
     for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
@@ -397,49 +428,68 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         const QRef qr = p.qrefs[r];
         for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
           const int q_valid = qr.q_len - mb * kBQ;
-          // diagonal: column c (q = 64mb + c) sees kv row 128nb + tid iff c >= shift
-          const int shift0 = (it.nblock * kBK - mb * kBQ);
+          // diagonal: column c (q = 128 mb + c) sees kv row 128 nb + tid iff c >= shift
+          const int shift0 = it.nblock * kBK - mb * kBQ;
           const bool plain = kv_full_tile && q_valid >= kBQ && (!qr.diag || shift0 + kBK - 1 <= 0);
-          const int shift = qr.diag ? shift0 + tid : -1;
+          const int shift = qr.diag ? shift0 + tid : -(1 << 30);
           for (int gq = 0; gq < group; ++gq, ++tile) {
-            const uint32_t b = tile & 1;
-            mbar_wait(&sm.sdp_full, sdp_phase);
-            FCPB_TR(kTrSdpGot, (int)tile);
-            sdp_phase ^= 1;
-            mbar_wait(&sm.qd_full[stage], stage_phase);   // lse2 / delta of this tile landed
+            float pr[kCols];
+            mbar_wait(&sm.s_full, s_phase);
+            s_phase ^= 1;
+            FCPB_TR(kTrSGot, (int)tile);
+            mbar_wait(&sm.q_full[slot], slot_phase);      // lse2 / delta of this tile landed
             tc_fence_after();
-            const uint32_t l2 = smem_u32(sm.lse2[stage]);
-            const uint32_t dl = smem_u32(sm.delta[stage]);
-            mbar_wait(&sm.pds_free[b], pfree_phase[b] ^ 1);   // P/dS buffer b consumed (tile j-2)
-            pfree_phase[b] ^= 1;
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              uint32_t sv[32], dv[32];
-              tmem_ld32(t_s + half * 32, sv);
-              tmem_ld32(t_dp + half * 32, dv);
+            const uint32_t l2 = smem_u32(&sm.lse2[slot][wg * kCols]);
+            const uint32_t dl = smem_u32(&sm.delta[slot][wg * kCols]);
+            // phase 1: P (chunk c's bf16 lands over S columns already read)
+            // chunk 1's TMEM load is in flight while chunk 0 computes
+            {
+              uint32_t s0[32], s1[32];
+              tmem_ld32(t_s, s0);
               tmem_wait_ld();
-              if (half == 1) {
-                tc_fence_before();
-                mbar_arrive(&sm.sdp_free);                  // S/dP(j) fully read
-                FCPB_TR(kTrLoaded, (int)tile);
-              }
+              tmem_ld32(t_s + 32, s1);
               if (plain)
-                softmax_half<false>(sv, dv, l2, dl, sl2, t_p[b], t_ds[b], true, kBQ, -1, half);
+                p_chunk<false>(s0, l2, sl2, pr, t_s, true, 0, 0, 0);
               else
-                softmax_half<true>(sv, dv, l2, dl, sl2, t_p[b], t_ds[b], kv_live, q_valid, shift, half);
+                p_chunk<true>(s0, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift);
+              tmem_wait_ld();
+              if (plain)
+                p_chunk<false>(s1, l2 + 128, sl2, pr + 32, t_s + 16, true, 0, 0, 0);
+              else
+                p_chunk<true>(s1, l2 + 128, sl2, pr + 32, t_s + 16, kv_live, wg * kCols + 32,
+                              q_valid, shift);
             }
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.pds_full[b]);
-            FCPB_TR(kTrPdsArrive, (int)tile);
-            if (++stage == kStages) { stage = 0; stage_phase ^= 1; }
+            mbar_arrive(&sm.p_full);
+            FCPB_TR(kTrPArrive, (int)tile);
+            // phase 2: dS
+            mbar_wait(&sm.dp_full, dp_phase);
+            dp_phase ^= 1;
+            FCPB_TR(kTrDpGot, (int)tile);
+            tc_fence_after();
+            {
+              uint32_t d0[32], d1[32];
+              tmem_ld32(t_dp, d0);
+              tmem_wait_ld();
+              tmem_ld32(t_dp + 32, d1);
+              ds_chunk(d0, dl, pr, t_dp);
+              tmem_wait_ld();
+              ds_chunk(d1, dl + 128, pr + 32, t_dp + 16);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&sm.ds_full);
+            FCPB_TR(kTrDsArrive, (int)tile);
+            if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
           }
         }
       }
     }
-  } else if (warp >= 8) {
+  } else {
     // ------------------------------------------------------------ dK/dV epilogue
-    const int tid = threadIdx.x - 256;            // kv row
+    reg_dealloc<kRegsEpi>();          // below the launch allocation: .dec
+    const int tid = ((warp & 3) << 5) + lane_id();        // kv row
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     uint32_t acc_phase = 0;
     SchedCursor sc;
@@ -447,7 +497,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       const Item it = p.items[item_of(g, p)];
       const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
-      // ---- dK, dV epilogue (thread == kv row)
       mbar_wait(&sm.acc_full, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
@@ -457,7 +506,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       float* dkb = recv ? p.dk_recv : p.dk;
       float* dvb = recv ? p.dv_recv : p.dv;
       const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD;
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < kD / 32; ++c) {
         uint32_t a[32], bb[32];
         tmem_ld32(tmem + lane_bits + kColDK + c * 32, a);

@@ -14,7 +14,7 @@ for _ in range(3):
     ex.step(q, k, v, do)
 torch.cuda.synchronize()
 lib = native.load()
-EV = ["QdIssue", "QdGot", "SdpIssue", "PdsGot", "AccIssue", "SdpGot", "Loaded", "PfreeGot", "PdsArrive", "DqGot", "DqDone"]
+EV = ["QIssue", "QGot", "SIssue", "PGot", "DvIssue", "DsGot", "DkIssue", "SGot", "PArrive", "DpGot", "DsArrive"]
 T = 256
 buf = (ctypes.c_ulonglong * (len(EV) * T))()
 lib.fcpb_debug_bwd_trace(buf, len(EV) * T)
@@ -24,10 +24,10 @@ a = np.where(a > 0, a - t0, -1)
 print("tile " + " ".join(f"{e:>9s}" for e in EV))
 for j in range(0, int(os.environ.get("NPRINT", "120"))):
     print(f"{j:4d} " + " ".join(f"{a[e, j]:9d}" for e in range(len(EV))))
-d = np.diff(a[EV.index("AccIssue"), 20:120])
-print("median AccIssue period (cycles):", np.median(d))
-dd = a[EV.index("DqDone"), 20:120] - a[EV.index("DqGot"), 20:120]
-print("median drain (cycles):", np.median(dd))
+d = np.diff(a[EV.index("DkIssue"), 20:120])
+print("median DkIssue period (cycles):", np.median(d))
+for x, y in [("SGot", "PArrive"), ("DpGot", "DsArrive"), ("SIssue", "SGot")]:
+    print(f"median {x}->{y}:", np.median(a[EV.index(y), 20:120] - a[EV.index(x), 20:120]))
 import time
 s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 s0.record()
