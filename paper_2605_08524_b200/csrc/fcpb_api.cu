@@ -220,10 +220,8 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   if (a->t_pad < a->q_tokens || !a->lse2_t || !a->delta_t)
     return fail(FCPB_ERR_INVALID, "lse2_t/delta_t/t_pad missing (run fcpb_bwd_preprocess)");
   const int H = a->num_q_heads, Hk = a->num_kv_heads;
-  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
+  CUtensorMap tk, tv, tkr, tvr;
   int rc;
-  if ((rc = make_map(&tq, a->q, a->q_tokens, H, 128, fcpb::dq::kBM))) return rc;
-  if ((rc = make_map(&tdo, a->dout, a->q_tokens, H, 128, fcpb::dq::kBM))) return rc;
   if ((rc = make_map(&tk, a->k, a->kv_tokens, Hk, 128, fcpb::dq::kBN))) return rc;
   if ((rc = make_map(&tv, a->v, a->kv_tokens, Hk, 128, fcpb::dq::kBN))) return rc;
   const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
@@ -246,6 +244,8 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   p.delta_t = a->delta_t;
   p.t_pad = a->t_pad;
   p.dq = static_cast<__nv_bfloat16*>(a->dq);
+  p.q = static_cast<const __nv_bfloat16*>(a->q);
+  p.dout = static_cast<const __nv_bfloat16*>(a->dout);
   p.head_major = a->head_major;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
@@ -260,7 +260,7 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
   fcpb::dq::attn_dq_kernel<<<grid, fcpb::dq::kThreads, kDqSmem, static_cast<cudaStream_t>(stream)>>>(
-      tq, tdo, tk, tv, tkr, tvr, p);
+      tk, tv, tkr, tvr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }

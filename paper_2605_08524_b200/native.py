@@ -12,7 +12,8 @@ import os
 
 from .errors import NativeError, ParameterError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcpb.so")
+# FCPB_LIB: A/B experiments against another build of the same ABI (scripts/); default in-tree.
+_LIB_PATH = os.environ.get("FCPB_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfcpb.so")
 
 c_i32, c_i64, c_f32, c_vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
 

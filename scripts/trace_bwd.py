@@ -36,7 +36,7 @@ for _ in range(5):
 e0.record(); torch.cuda.synchronize()
 print("step ms:", s0.elapsed_time(e0) / 5)
 
-EV2 = ["KIssue", "KGot", "SdpIssue", "DsGot", "DqIssue", "SdpGot", "Freed", "DsArrive"]
+EV2 = ["KIssue", "KGot", "SIssue", "DsGot", "DqIssue", "SGot", "Freed", "DpGot", "DsArrive"]
 buf2 = (ctypes.c_ulonglong * (len(EV2) * T))()
 lib.fcpb_debug_dq_trace(buf2, len(EV2) * T)
 b = np.frombuffer(buf2, dtype=np.uint64).reshape(len(EV2), T).astype(np.int64)
