@@ -52,31 +52,64 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock, power and clock-event reasons sampled through NVML every 20 ms during the
+    timed region (nvidia-smi as the fallback), plus the NVML energy counter around it."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []          # (sm_mhz, power_w, reasons bitmask)
         self._stop = threading.Event()
         self._t = None
+        self.nv = None
+        self.energy_mj = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            # CUDA_VISIBLE_DEVICES may remap; the bench process sees its GPU as `index`
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.limit_w = pynvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1e3
+        except Exception:
+            self.nv = None
+
+    def _energy(self):
+        try:
+            return self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h)
+        except Exception:
+            return None
 
     def _run(self):
+        nv = self.nv
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if nv is not None:
+                    self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                         nv.nvmlDeviceGetPowerUsage(self.h) / 1e3,
+                                         nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+                else:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,power.draw",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip()
+                    if out:
+                        sm, pw = (float(x) for x in out.split(",")[:2])
+                        self.samples.append((sm, pw, 0))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02 if nv is not None else 0.2)
 
     def __enter__(self):
+        e0 = self._energy() if self.nv else None
+        self._e0 = e0
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -84,17 +117,37 @@ class ClockSampler:
     def __exit__(self, *exc):
         self._stop.set()
         self._t.join(timeout=10)
+        if self.nv and self._e0 is not None:
+            e1 = self._energy()
+            self.energy_mj = None if e1 is None else e1 - self._e0
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        sm = sorted(x[0] for x in self.samples)
+        reasons = []
+        if self.nv is not None:
+            for name, attr in self.REASONS:
+                bit = getattr(self.nv, attr, 0)
+                if bit and any(x[2] & bit for x in self.samples):
+                    reasons.append(name)
+        out = {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": getattr(self, "max_mhz", None),
+               "reasons": reasons, "samples": len(self.samples), "sm_mhz_min": sm[0]}
+        if self.nv is not None:
+            out["power_limit_w"] = self.limit_w
+        return out
+
+
+def measured_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the committed
+    ncu --set full summary (profiles/traffic.json, scripts/ncu_summary.py); None if absent."""
+    try:
+        d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                        "traffic.json")))
+        k = d["kernels"][kernel]
+        return {"bytes_per_launch": k["traffic_bytes"], "source": d["source"]}
+    except Exception:
+        return None
 
 
 def build_workload(name: str, n: int, block: int | None):
@@ -182,7 +235,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--block", type=int, default=None)
@@ -311,6 +364,14 @@ def main():
         e2e = {"value": w.total_tokens / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3}
 
+    # isolated exchange bandwidth (N > 1): min over ranks of the per-rank receive GB/s
+    xbw = ex.exchange_benchmark() if world > 1 else None
+    if xbw is not None:
+        for key in ("fwd_kv_pull", "bwd_dkv_return"):
+            g = torch.tensor([xbw[key]["GBps"] or 0.0], device=device)
+            dist.all_reduce(g, op=dist.ReduceOp.MIN)
+            xbw[key]["GBps_min_over_ranks"] = g.item()
+
     t = torch.tensor([ms], device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -350,17 +411,21 @@ def main():
             "roofline": {"bound": "tensor", "kernel": names[top],
                          "achieved": ktf[top], "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": ktf[top] * 1e12 / peak, "peak_kind": peak_kind + " burst",
-                         "traffic": None,
+                         "traffic": measured_traffic(names[top]),
                          "per_unit": "4*Hq*D FLOP per visible (q,kv) pair (fwd); bwd 2.5x split "
                                      "4/7 dK/dV, 3/7 dQ; units = rank-0 visible pairs"},
             "kernels": {names[key]: {"ms": kms[key], "tflops": ktf[key], "frac": ktf[key] * 1e12 / peak,
                                      "launches": nl[key]} for key in kms},
             "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
             "exchange_bytes_rank0": exb,
+            "exchange_bw_rank0": xbw,
             "phases_ms_rank0": {kk: round(vv, 3) for kk, vv in phases.items()},
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": dict(clocks.summary(), **({} if clocks.energy_mj is None else {
+                "power_w_avg": round(clocks.energy_mj / (args.steps * ms) , 1)})),
+            "energy_j_per_step": (None if clocks.energy_mj is None
+                                  else round(clocks.energy_mj / 1e3 / args.steps, 3)),
             "e2e": e2e,
         }
         if not args.no_cpu and n == 1:

@@ -69,8 +69,13 @@ class BlockAttention:
         self._dq = (d, _dev_i32(d.segments, dev), _dev_i32(d.kvrefs, dev), _dev_i32(d.items, dev))
         self.launches = 0   # kernel launches issued by this object (bench accounting)
         import os
-        sched = os.environ.get("FCPB_SCHED", "")   # experiment knob: "f,b,q" head-major flags
-        flags = [int(x) for x in sched.split(",")] if sched else [0, 0, 0]
+        # Work order of the dynamic scheduler: head-major (all items of one head, LPT order,
+        # before the next head) keeps one head's Q/dO (or K/V) stream resident in L2.  On
+        # C2 it cut DRAM reads 17.8 -> 2.6 GB (dK/dV), 5.0 -> 1.4 GB (dQ), 3.5 -> 0.9 GB (fwd)
+        # per launch, which under the B200's 1 kW power cap is time (profiles/r01_notes.md).
+        # FCPB_SCHED="f,b,q" overrides it for experiments.
+        sched = os.environ.get("FCPB_SCHED", "")
+        flags = [int(x) for x in sched.split(",")] if sched else [1, 1, 1]
         self.head_major = {"fwd": flags[0], "bwd": flags[1], "dq": flags[2]}
         # one dynamic-scheduler counter per kernel kind (zeroed by the C ABI before each launch)
         self._sched = torch.zeros(4, dtype=torch.int32, device=self.device)

@@ -81,6 +81,34 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
   return n;
 }
 
+// One row of a 128-column S tile: P = exp2(s*sl2 + neg) as bf16 pairs into TMEM at t_s
+// (16 columns per 32 scores), returns the row sum.  kPoly: pairs 8u+8-kPolyPairs..8u+7 use
+// ex2_poly2 (finite inputs only).
+#ifndef FCPB_FWD_POLY_PAIRS
+#define FCPB_FWD_POLY_PAIRS 0    // measured: 2/3/4 pairs cost +1/+3/+6% fwd cycles (issue-bound)
+#endif
+constexpr int kPolyPairs = FCPB_FWD_POLY_PAIRS;
+template <bool kPoly>
+FCPB_DEV float exp_row(const float (&s)[kBN], float sl2, float neg, uint32_t t_s) {
+  float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int c = 0; c < kBN / 32; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
+                                  make_float2(sl2, sl2), make_float2(neg, neg));
+      float2 e;
+      if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
+      else e = make_float2(ex2(x.x), ex2(x.y));
+      sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+      pk[i / 2] = pack_bf16(e.x, e.y);
+    }
+    tmem_st16(t_s + c * 16, pk);
+  }
+  return (sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y);
+}
+
 // setmaxnreg split: one producer/MMA warpgroup, two softmax warpgroups.  setmaxnreg.inc can
 // only take registers the CTA was given at launch (384 threads x 168, the __launch_bounds__
 // allocation), so the budgets must sum to at most 3 * kRegsLaunch.
@@ -338,22 +366,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (m_run == -INFINITY) m_use = (mx == -INFINITY) ? 0.f : mx;
           else m_use = ((mx - m_run) * sl2 > 8.f) ? mx : m_run;
           const float neg = -m_use * sl2;
-          float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           // P (bf16 pairs) overwrites the first 64 columns of S, 16 columns per 32 scores.
-#pragma unroll
-          for (int c = 0; c < kBN / 32; ++c) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
-                                          make_float2(sl2, sl2), make_float2(neg, neg));
-              const float2 e = make_float2(ex2(x.x), ex2(x.y));
-              sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
-              pk[i / 2] = pack_bf16(e.x, e.y);
-            }
-            tmem_st16(t_s + c * 16, pk);
-          }
-          const float sum = (sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y);
+          // Unmasked tiles (finite scores, x <= 8) send kPolyPairs of every 8 pairs to the
+          // FMA pipe (FA4-style): two softmax warps per SMSP otherwise need 2 x 128 ex2 x 8
+          // MUFU cycles per KV tile, as long as the tile's tensor work.  Masked tiles keep
+          // exact zeros from MUFU ex2(-inf).  The choice is CTA-uniform.
+          const bool poly = !(diag && t == it.mblock) && valid >= kBN;
+          const float sum = poly ? exp_row<true>(s, sl2, neg, t_s) : exp_row<false>(s, sl2, neg, t_s);
           const float alpha = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_use) * sl2);
           l_run = l_run * alpha + sum;
           // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.

@@ -191,6 +191,43 @@ class FcpExecutor:
         self._mark("bwd_reduce_convert", cur)
         return out
 
+    def exchange_benchmark(self, reps: int = 5) -> dict | None:
+        """Isolated copy-engine exchange bandwidth of this rank (no attention running):
+        the forward K/V pulls of every stage and the backward partial-dKV returns, each
+        bracketed by the same symmetric-memory barriers the step uses and timed with CUDA
+        events on the comm stream.  GB/s = bytes this rank receives / time (the read
+        direction of its NVLink ports; B200 NVLink 5: 900 GB/s per direction)."""
+        x = self.xchg
+        if x is None or not self.stages:
+            return None
+        Hk, D = self.cfg.kv_heads, self.cfg.head_dim
+        sk = torch.empty((max(self.ret_tokens, 1), Hk, D), dtype=torch.float32, device=self.device)
+        sv = torch.empty_like(sk)
+        b = self.exchange_bytes()
+        out = {}
+        for name, nbytes in (("fwd_kv_pull", b["fwd_recv"]), ("bwd_dkv_return", b["bwd_recv"])):
+            times = []
+            for _ in range(reps + 1):
+                torch.cuda.synchronize(self.device)
+                s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(self.comm):
+                    which = "kv" if name == "fwd_kv_pull" else "part"
+                    x.barrier(which, 0)
+                    s0.record(self.comm)
+                    if which == "kv":
+                        for s_idx in range(len(self.stages)):
+                            x.pull_stage(s_idx, self.k_recv, self.v_recv)
+                    else:
+                        x.pull_returns(self.stages, sk, sv, self.ret_rows)
+                    e0.record(self.comm)
+                    x.barrier(which, 1)
+                torch.cuda.synchronize(self.device)
+                times.append(s0.elapsed_time(e0))
+            t = sorted(times[1:])[len(times[1:]) // 2]
+            out[name] = {"bytes": nbytes, "ms": t, "GBps": nbytes / (t * 1e-3) / 1e9 if t > 0 else None}
+        out["peak_GBps_per_direction"] = 900.0
+        return out
+
     def step(self, q, k, v, do):
         """One attention layer fwd+bwd; returns (o, lse, dq, dk, dv)."""
         o, lse = self.forward(q, k, v)
