@@ -10,7 +10,7 @@
 // Per Q tile j (128 query rows of one q head):
 //   S^T  = K  Q_j^T   M128 N128 K128 (SS)  -> TMEM S  [0,128)    fp32
 //   dP^T = V  dO_j^T  M128 N128 K128 (SS)  -> TMEM dP [128,256)  fp32
-//   softmax (thread == kv row; warpgroup w owns q columns [64w, 64w+64)):
+//   softmax (thread == kv row; warpgroup w owns q columns [32w, 32w+32)):
 //     phase 1: P^T = exp2(S^T*c - lse2[q])           -> bf16, in place over its own S columns
 //     phase 2: dS^T = P^T (dP^T - delta[q])           -> bf16, in place over its own dP columns
 //   dV  += P^T  dO_j  M128 N128 K128 (TS, A = P^T from TMEM)  -> TMEM dV [256,384)
@@ -21,8 +21,9 @@
 // S(j+1) cannot overwrite P(j) before dV(j) read it, nor dP(j+1) dS(j) before dK(j); and
 // phase 1 of tile j+1 (the exp work) overlaps dK(j)/dP(j+1), phase 2 of tile j overlaps
 // dV(j)/S(j+1).
-// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-11 softmax (two warpgroups),
-//        w12-15 dK/dV epilogue.
+// Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-19 four softmax warpgroups, which
+//        also drain dK/dV at the end of each item (four warps per SMSP hide the exp
+//        phase's dependency latency; with two it ran at ~40% issue efficiency).
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -34,7 +35,7 @@ namespace bwd {
 // Debug timeline of CTA 0: [event][tile] clock64 stamps (see scripts/trace_bwd.py).
 constexpr int kTraceTiles = 256;
 enum TraceEv { kTrQIssue, kTrQGot, kTrSIssue, kTrPGot, kTrDvIssue, kTrDsGot, kTrDkIssue,
-               kTrSGot, kTrPArrive, kTrDpGot, kTrDsArrive, kTrEvents };
+               kTrSGot, kTrPArrive, kTrDpGot, kTrDsArrive, kTrSLd, kTrPSt, kTrEvents };
 __device__ unsigned long long g_trace[kTrEvents * kTraceTiles];
 #define FCPB_TR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
     ((ev) < kTrSGot ? true : threadIdx.x == 128)) \
@@ -51,21 +52,18 @@ constexpr int kKVPanel = kKVBytes / 2;
 constexpr int kQBytes = kBQ * kD * 2;           // 32 KB (two 16 KB panels)
 constexpr int kQPanel = kQBytes / 2;
 constexpr int kSlots = 2;                       // Q ring and dO ring depth
-constexpr int kSoftmaxWGs = 2;
+constexpr int kSoftmaxWGs = 4;
 constexpr int kCols = kBQ / kSoftmaxWGs;        // q columns per softmax warpgroup
-constexpr int kThreads = 128 * (2 + kSoftmaxWGs);
+constexpr int kThreads = 128 * (1 + kSoftmaxWGs);
 constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
-// setmaxnreg split.  setmaxnreg.inc can only take registers the CTA was given at launch
-// (kThreads x kRegsLaunch, the __launch_bounds__ allocation), so the budgets must sum to
-// at most 4 * kRegsLaunch.
-constexpr uint32_t kRegsLaunch = 128, kRegsCtl = 96, kRegsEpi = 96, kRegsSoftmax = 160;
-static_assert(kRegsCtl + kRegsEpi + kSoftmaxWGs * kRegsSoftmax <= 4 * kRegsLaunch,
-              "setmaxnreg.inc would wait forever for registers that were never allocated");
+// Register budget: 640 threads x 96 (the __launch_bounds__ allocation); the control and
+// softmax warpgroups both fit in it, so no setmaxnreg split is needed.
+constexpr uint32_t kRegsLaunch = 96;
 
 // TMEM column of the bf16 A-operand chunk kk (16 q columns = 8 TMEM columns) of P^T / dS^T:
-// warpgroup w keeps its 64 columns in the first 32 TMEM columns of its own S / dP slice.
+// warpgroup w keeps its 32 columns in the first 16 TMEM columns of its own S / dP slice.
 FCPB_DEV constexpr uint32_t a_col(uint32_t base, int kk) {
-  return base + static_cast<uint32_t>((kk >> 2) * kCols + (kk & 3) * 8);
+  return base + static_cast<uint32_t>((kk >> 1) * kCols + (kk & 1) * 8);
 }
 
 struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
@@ -231,8 +229,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     mbar_init(&sm.p_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.ds_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.acc_full, 1);
-    mbar_init(&sm.acc_free, 128);
-    sched_init(sm.sched, 1 + 4 * kSoftmaxWGs + 4);
+    mbar_init(&sm.acc_free, 128 * kSoftmaxWGs);
+    sched_init(sm.sched, 1 + 4 * kSoftmaxWGs);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem_base);
@@ -242,7 +240,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   const uint32_t tmem = sm.tmem_base;
 
   if (warp < 4) {
-    reg_dealloc<kRegsCtl>();
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer (all lanes:
       // lane 0 issues the TMA tiles, every lane copies 4 lse2 + 4 delta values with cp.async)
@@ -407,19 +404,19 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         __syncwarp();
       }
     }
-  } else if (warp < 4 + 4 * kSoftmaxWGs) {
+  } else {
     // ------------------------------------------------------------ softmax (thread == kv row)
-    reg_alloc<kRegsSoftmax>();
-    const int wg = (warp - 4) >> 2;                       // q columns [64 wg, 64 wg + 64)
+    const int wg = (warp - 4) >> 2;                       // q columns [32 wg, 32 wg + 32)
     const int tid = ((warp & 3) << 5) + lane_id();        // kv row == TMEM lane
     const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const uint32_t t_s = tmem + lane_bits + kColS + wg * kCols;
     const uint32_t t_dp = tmem + lane_bits + kColDP + wg * kCols;
     const float sl2 = p.scale_log2;
-    uint32_t s_phase = 0, dp_phase = 0, slot = 0, slot_phase = 0, tile = 0;
+    uint32_t s_phase = 0, dp_phase = 0, slot = 0, slot_phase = 0, acc_phase = 0, tile = 0;
     SchedCursor sc;
     for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
+      const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
       const int kv_row = it.nblock * kBK + tid;
       const bool kv_live = kv_row < ks.kv_len;
@@ -441,24 +438,18 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             tc_fence_after();
             const uint32_t l2 = smem_u32(&sm.lse2[slot][wg * kCols]);
             const uint32_t dl = smem_u32(&sm.delta[slot][wg * kCols]);
-            // phase 1: P (chunk c's bf16 lands over S columns already read)
-            // chunk 1's TMEM load is in flight while chunk 0 computes
+            // phase 1: P (bf16 lands over the first 16 of this warpgroup's S columns)
             {
-              uint32_t s0[32], s1[32];
-              tmem_ld32(t_s, s0);
+              uint32_t sv[32];
+              tmem_ld32(t_s, sv);
               tmem_wait_ld();
-              tmem_ld32(t_s + 32, s1);
+              FCPB_TR(kTrSLd, (int)tile);
               if (plain)
-                p_chunk<false>(s0, l2, sl2, pr, t_s, true, 0, 0, 0);
+                p_chunk<false>(sv, l2, sl2, pr, t_s, true, 0, 0, 0);
               else
-                p_chunk<true>(s0, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift);
-              tmem_wait_ld();
-              if (plain)
-                p_chunk<false>(s1, l2 + 128, sl2, pr + 32, t_s + 16, true, 0, 0, 0);
-              else
-                p_chunk<true>(s1, l2 + 128, sl2, pr + 32, t_s + 16, kv_live, wg * kCols + 32,
-                              q_valid, shift);
+                p_chunk<true>(sv, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift);
             }
+            FCPB_TR(kTrPSt, (int)tile);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&sm.p_full);
@@ -469,13 +460,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             FCPB_TR(kTrDpGot, (int)tile);
             tc_fence_after();
             {
-              uint32_t d0[32], d1[32];
-              tmem_ld32(t_dp, d0);
+              uint32_t dv[32];
+              tmem_ld32(t_dp, dv);
               tmem_wait_ld();
-              tmem_ld32(t_dp + 32, d1);
-              ds_chunk(d0, dl, pr, t_dp);
-              tmem_wait_ld();
-              ds_chunk(d1, dl + 128, pr + 32, t_dp + 16);
+              ds_chunk(dv, dl, pr, t_dp);
             }
             tmem_wait_st();
             tc_fence_before();
@@ -485,36 +473,22 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           }
         }
       }
-    }
-  } else {
-    // ------------------------------------------------------------ dK/dV epilogue
-    reg_dealloc<kRegsEpi>();          // below the launch allocation: .dec
-    const int tid = ((warp & 3) << 5) + lane_id();        // kv row
-    const uint32_t lane_bits = static_cast<uint32_t>((warp & 3) * 32) << 16;
-    uint32_t acc_phase = 0;
-    SchedCursor sc;
-    for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
-      const Item it = p.items[item_of(g, p)];
-      const int kvh = head_of(g, p);
-      const KvSeg ks = p.kvsegs[it.kvseg];
+      // ---- dK/dV epilogue: this warpgroup's 32 d columns of its kv row
       mbar_wait(&sm.acc_full, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
-      const int kv_row = it.nblock * kBK + tid;
-      const bool kv_live = kv_row < ks.kv_len;
-      const bool recv = ks.flags & FCPB_KV_RECV;
-      float* dkb = recv ? p.dk_recv : p.dk;
-      float* dvb = recv ? p.dv_recv : p.dv;
-      const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD;
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
+      {
+        const bool recv = ks.flags & FCPB_KV_RECV;
+        float* dkb = recv ? p.dk_recv : p.dk;
+        float* dvb = recv ? p.dv_recv : p.dv;
+        const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD + wg * 32;
         uint32_t a[32], bb[32];
-        tmem_ld32(tmem + lane_bits + kColDK + c * 32, a);
-        tmem_ld32(tmem + lane_bits + kColDV + c * 32, bb);
+        tmem_ld32(tmem + lane_bits + kColDK + wg * 32, a);
+        tmem_ld32(tmem + lane_bits + kColDV + wg * 32, bb);
         tmem_wait_ld();
         if (kv_live) {
-          float4* k4 = reinterpret_cast<float4*>(dkb + row + c * 32);
-          float4* v4 = reinterpret_cast<float4*>(dvb + row + c * 32);
+          float4* k4 = reinterpret_cast<float4*>(dkb + row);
+          float4* v4 = reinterpret_cast<float4*>(dvb + row);
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             k4[i / 4] = make_float4(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale,

@@ -14,7 +14,7 @@ for _ in range(3):
     ex.step(q, k, v, do)
 torch.cuda.synchronize()
 lib = native.load()
-EV = ["QIssue", "QGot", "SIssue", "PGot", "DvIssue", "DsGot", "DkIssue", "SGot", "PArrive", "DpGot", "DsArrive"]
+EV = ["QIssue", "QGot", "SIssue", "PGot", "DvIssue", "DsGot", "DkIssue", "SGot", "PArrive", "DpGot", "DsArrive", "SLd", "PSt"]
 T = 256
 buf = (ctypes.c_ulonglong * (len(EV) * T))()
 lib.fcpb_debug_bwd_trace(buf, len(EV) * T)
@@ -26,7 +26,7 @@ for j in range(0, int(os.environ.get("NPRINT", "120"))):
     print(f"{j:4d} " + " ".join(f"{a[e, j]:9d}" for e in range(len(EV))))
 d = np.diff(a[EV.index("DkIssue"), 20:120])
 print("median DkIssue period (cycles):", np.median(d))
-for x, y in [("SGot", "PArrive"), ("DpGot", "DsArrive"), ("SIssue", "SGot")]:
+for x, y in [("SGot", "PArrive"), ("DpGot", "DsArrive"), ("SIssue", "SGot"), ("SGot", "SLd"), ("SLd", "PSt"), ("PSt", "PArrive")]:
     print(f"median {x}->{y}:", np.median(a[EV.index(y), 20:120] - a[EV.index(x), 20:120]))
 import time
 s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
