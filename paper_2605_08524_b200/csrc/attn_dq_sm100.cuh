@@ -28,6 +28,10 @@
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
 
+#ifndef FCPB_DQ_SPIN
+#define FCPB_DQ_SPIN 1    // 1: MMA warp spins on ds_full; 2: also the softmax's dP wait
+#endif
+
 namespace fcpb {
 namespace dq {
 
@@ -294,7 +298,8 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
             issue_score(kColQ, smem_u32(sm.k[ks]), kColS, &sm.s_full, nullptr);
             FCPB_DQTR(kDqSIssue, (int)tile + 1);
           }
-          mbar_wait(&sm.ds_full, ds_phase);
+          if (FCPB_DQ_SPIN >= 1) mbar_wait_spin(&sm.ds_full, ds_phase);
+          else mbar_wait(&sm.ds_full, ds_phase);
           ds_phase ^= 1;
           FCPB_DQTR(kDqDsGot, (int)tile);
           if (j == 0) {                                   // epilogue drained the previous dQ
@@ -389,7 +394,8 @@ attn_dq_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__
             else
               p_cols<true>(sv, p.scale_log2, nlse, pr, part * kCols, valid, diag_row);
           }
-          mbar_wait(&sm.dp_full, dp_phase);
+          if (FCPB_DQ_SPIN >= 2) mbar_wait_spin(&sm.dp_full, dp_phase);
+          else mbar_wait(&sm.dp_full, dp_phase);
           dp_phase ^= 1;
           FCPB_DQTR(kDqDpGot, (int)tile);
           tc_fence_after();

@@ -53,6 +53,17 @@ FCPB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+FCPB_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 FCPB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -72,6 +83,20 @@ FCPB_DEV uint64_t global_timer_ns() {
 #ifndef FCPB_WATCHDOG_NS
 #define FCPB_WATCHDOG_NS 8000000000ull  // a pipeline stall this long is a bug: trap, don't hang
 #endif
+// Spinning wait (no suspend): for a warp on the critical path (the MMA issuer), where the
+// suspend/wake latency of try_wait would sit on the tile chain.
+FCPB_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  if (mbar_test_wait(bar, parity)) return;
+  const uint64_t t0 = global_timer_ns();
+  uint32_t spins = 0;
+  while (!mbar_test_wait(bar, parity)) {
+    if ((++spins & 4095u) == 0 && global_timer_ns() - t0 > FCPB_WATCHDOG_NS) {
+      printf("fcpb watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
+             blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+}
 FCPB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = global_timer_ns();

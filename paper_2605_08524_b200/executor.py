@@ -228,6 +228,90 @@ class FcpExecutor:
         out["peak_GBps_per_direction"] = 900.0
         return out
 
+    def measured_report(self, q, k, v, do, reps: int = 3):
+        """A measured counterpart of the reference's analytic ``simulate()`` report
+        (``simulator.py:60-70`` / ``simmodel.SimReport``) for one fwd+bwd step:
+
+        * ``total_time``: device step time in seconds (max over ranks);
+        * ``per_worker[r]``: compute_time = summed durations of rank r's attention launches
+          (CUDA events around each), send/recv_time = its exchange bytes over the isolated
+          copy-engine pull time, idle_time = total - compute, eta = total / compute;
+        * ``stages``: one record per coalesced stage, the isolated pull time of this rank;
+        * ``total_flops``: the reference accounting, 3.5 * 4*Hq*D * visible pairs of the batch;
+        * ``total_bytes``: the plan's edge bytes (``planner.py:81-102``).
+        Collective over the process group when world > 1."""
+        import torch.distributed as dist
+        from .distributor import worker_loads
+        from .simmodel import SimReport, StageRecord, WorkerStats
+        op = self.op
+        cur = torch.cuda.current_stream(self.device)
+        spans = []
+        names = ("forward_wave", "merge", "backward_prepare", "backward_launch", "backward_dq",
+                 "reduce_dkv", "to_bf16")
+        orig = {n: getattr(op, n) for n in names}
+
+        def wrap(fn):
+            def w(*a, **kw):
+                s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(cur)
+                out = fn(*a, **kw)
+                e0.record(cur)
+                spans.append((s0, e0))
+                return out
+            return w
+
+        self.step(q, k, v, do)                          # warm
+        torch.cuda.synchronize(self.device)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(cur)
+        for _ in range(reps):
+            self.step(q, k, v, do)
+        t1.record(cur)
+        torch.cuda.synchronize(self.device)
+        total = t0.elapsed_time(t1) / reps / 1e3
+        for n in names:
+            setattr(op, n, wrap(orig[n]))
+        try:
+            for _ in range(reps):
+                self.step(q, k, v, do)
+            torch.cuda.synchronize(self.device)
+        finally:
+            for n in names:
+                setattr(op, n, orig[n])
+        compute = sum(a.elapsed_time(b) for a, b in spans) / reps / 1e3
+        xb = self.exchange_benchmark(reps) if self.world > 1 else None
+        b = self.exchange_bytes()
+        send = recv = 0.0
+        if xb:
+            rate = xb["fwd_kv_pull"]["bytes"] / max(xb["fwd_kv_pull"]["ms"] * 1e-3, 1e-12)
+            send, recv = b["fwd_send"] / rate, b["fwd_recv"] / rate
+        stages = []
+        if self.xchg is not None and self.stages:
+            for s_idx in range(len(self.stages)):
+                torch.cuda.synchronize(self.device)
+                s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(self.comm):
+                    self.xchg.barrier("kv", 0)
+                    s0.record(self.comm)
+                    self.xchg.pull_stage(s_idx, self.k_recv, self.v_recv)
+                    e0.record(self.comm)
+                    self.xchg.barrier("kv", 1)
+                torch.cuda.synchronize(self.device)
+                stages.append(StageRecord(s0.elapsed_time(e0) / 1e3, "comm"))
+        mine = (total, compute, send, recv)
+        if self.world > 1 and dist.is_initialized():
+            allv = [None] * self.world
+            dist.all_gather_object(allv, mine, group=self.group)
+        else:
+            allv = [mine]
+        t_max = max(x[0] for x in allv)
+        per = [WorkerStats(compute_time=c, send_time=sd, recv_time=rv, idle_time=t_max - c,
+                           eta=t_max / c if c > 0 else 1.0) for _, c, sd, rv in allv]
+        loads = worker_loads(self.result.assignment, self.result.units, self.result.deps, self.cfg)
+        flops = 3.5 * float(sum(loads.compute_flops))      # distributor.py:151-155 accounting
+        nbytes = int(sum(e.nbytes for st in self.result.plan.stages for e in st))
+        return SimReport(t_max, per, stages, flops, nbytes)
+
     def step(self, q, k, v, do):
         """One attention layer fwd+bwd; returns (o, lse, dq, dk, dv)."""
         o, lse = self.forward(q, k, v)

@@ -49,8 +49,14 @@ def main():
     for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))
     ok = all((e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2) for n, e in rep.items())
+    # measured SimReport-shaped record (collective): one WorkerStats per rank, one record per stage
+    mr = ex.measured_report(*loc, reps=2)
+    ok = ok and len(mr.per_worker) == world and len(mr.stages) == len(ex.stages) \
+        and mr.total_time > 0 and all(w.compute_time > 0 for w in mr.per_worker) and mr.total_flops > 0
     print(json.dumps({"rank": rank, "world": world, "recv_tokens": lay.recv_tokens,
-                      "stages": len(ex.stages), "ok": ok, "errors": rep}), flush=True)
+                      "stages": len(ex.stages), "ok": ok, "errors": rep,
+                      "measured_total_ms": mr.total_time * 1e3,
+                      "measured_eta": [round(w.eta, 3) for w in mr.per_worker]}), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()

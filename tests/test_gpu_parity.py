@@ -84,3 +84,22 @@ def test_c2_llama8b_n1_sampled():
     rep = _full_check(lengths, 1, 2048, LLAMA, seq_ids=pick)
     _report("C2 N=1 sampled", rep)
     assert_within_tolerance(rep)
+
+
+def test_measured_report_single_rank():
+    """The executor's measured SimReport-shaped record (the counterpart of the reference's
+    analytic simulate()) at N=1: one worker, no stages, FLOPs from the reference accounting."""
+    from paper_2605_08524_b200.costmodel import batch_token_pairs
+    from paper_2605_08524_b200.executor import FcpExecutor
+    lengths = [1500, 700, 300]
+    r = schedule(lengths, 1, 512, GQA_SMALL)
+    from oracle.simworkers import global_offsets, gather_rank
+    goff, T = global_offsets(r)
+    ex = FcpExecutor(r, 0, GQA_SMALL, torch.device("cuda", 0))
+    loc = [gather_rank(x, ex.layout, goff, r.deps).cuda() for x in make_inputs(T, GQA_SMALL)]
+    rep = ex.measured_report(*loc, reps=2)
+    _report("measured report N=1", {"total_ms": rep.total_time * 1e3,
+                                    "compute_ms": rep.per_worker[0].compute_time * 1e3})
+    assert len(rep.per_worker) == 1 and rep.stages == []
+    assert 0 < rep.per_worker[0].compute_time <= rep.total_time * 1.05
+    assert rep.total_flops == 3.5 * GQA_SMALL.flops_per_token_pair * batch_token_pairs(lengths, "causal")
