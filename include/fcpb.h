@@ -89,7 +89,7 @@ typedef struct {
 
 FCPB_API int fcpb_lse_merge(const FcpbMergeArgs* args, void* stream);
 
-/* K2 preprocess: -delta = -rowsum(dO * O) and -lse * log2(e), both written negated and
+/* K2 preprocess (num_q_heads <= 64): -delta = -rowsum(dO * O) and -lse * log2(e), both written negated and
  * head-major [Hq, t_pad] fp32 (t_pad = tokens rounded up to 4, TMA row pitch), and
  * zero the fp32 dQ accumulator [tokens, Hq, D]. */
 FCPB_API int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse,

@@ -50,36 +50,64 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
 
 // delta = <dO[row,:], O[row,:]>, lse2 = lse*log2(e) (both head-major [H, t_pad]) and
 // dq_accum[row,:] = 0; one warp per (token, head) row.
+// Backward preprocess: -delta = -rowsum(dO * O) and -lse * log2(e), written head-major
+// [H, t_pad].  A block owns 32 consecutive tokens x all heads: warps stream the (token, head)
+// rows (256 B of O and of dO each, one uint2 per lane), park the 32 x H results in shared
+// memory, and write every head's 32 tokens as one coalesced 128 B row (a warp-per-row
+// layout wrote one scattered 4 B word per row and ran at half the HBM rate).
+constexpr int kPrepTokens = 32;
+constexpr int kPrepMaxHeads = 64;
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                               const __nv_bfloat16* __restrict__ dout,
                                                               const float* __restrict__ lse,
                                                               float* __restrict__ lse2_t,
                                                               float* __restrict__ delta_t,
                                                               int64_t t_pad, float* __restrict__ dq,
-                                                              int64_t rows, int heads) {
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= rows) return;
-  const uint2 ov = reinterpret_cast<const uint2*>(o + w * 128)[lane];
-  const uint2 dv = reinterpret_cast<const uint2*>(dout + w * 128)[lane];
-  const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
-  const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
-  float s = 0.f;
+                                                              int64_t tokens, int heads) {
+  __shared__ float sd[kPrepMaxHeads][kPrepTokens + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kPrepTokens;
+  const int nt = static_cast<int>(tokens - t0 < kPrepTokens ? tokens - t0 : kPrepTokens);
+  const int nrows = nt * heads;
+  constexpr int kU = 4;                     // rows in flight per warp (memory-level parallelism)
+  for (int r0 = warp * kU; r0 < nrows; r0 += nwarps * kU) {
+    uint2 ov[kU], dv[kU];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const float2 a = __bfloat1622float2(o2[i]);
-    const float2 b = __bfloat1622float2(d2[i]);
-    s = fmaf(a.x, b.x, s);
-    s = fmaf(a.y, b.y, s);
-  }
+    for (int u = 0; u < kU; ++u) {
+      const int r = r0 + u;
+      const int64_t row = (t0 + r / heads) * heads + r % heads;   // token-major (t, h) row
+      ov[u] = r < nrows ? reinterpret_cast<const uint2*>(o + row * 128)[lane] : make_uint2(0, 0);
+      dv[u] = r < nrows ? reinterpret_cast<const uint2*>(dout + row * 128)[lane] : make_uint2(0, 0);
+    }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) {
-    const int64_t t = w / heads, h = w % heads;
-    delta_t[h * t_pad + t] = -s;                                  // negated: dP + ndelta
-    lse2_t[h * t_pad + t] = -lse[w] * 1.4426950408889634f;        // negated: S*c + nlse2
+    for (int u = 0; u < kU; ++u) {
+      const int r = r0 + u;
+      const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov[u]);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[u]);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float2 a = __bfloat1622float2(o2[i]);
+        const float2 b = __bfloat1622float2(d2[i]);
+        s = fmaf(a.x, b.x, s);
+        s = fmaf(a.y, b.y, s);
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (r < nrows) {
+        if (lane == 0) sd[r % heads][r / heads] = -s;                   // negated: dP + ndelta
+        const int64_t row = (t0 + r / heads) * heads + r % heads;
+        if (dq) reinterpret_cast<float4*>(dq + row * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
   }
-  if (dq) reinterpret_cast<float4*>(dq + w * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  for (int h = warp; h < heads; h += nwarps) {
+    if (lane < nt) {
+      delta_t[h * t_pad + t0 + lane] = sd[h][lane];
+      lse2_t[h * t_pad + t0 + lane] = -lse[(t0 + lane) * heads + h] * 1.4426950408889634f;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(256) f32_to_bf16_kernel(const float4* __restrict__ src,

@@ -283,14 +283,15 @@ int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse, float
                         int32_t num_q_heads, int32_t head_dim, void* stream) {
   if (head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", head_dim);
   if (t_pad < tokens || t_pad % 4) return fail(FCPB_ERR_INVALID, "bad t_pad %lld", (long long)t_pad);
-  const int64_t rows = tokens * num_q_heads;
-  if (rows == 0) return FCPB_OK;
+  if (num_q_heads <= 0 || num_q_heads > fcpb::aux::kPrepMaxHeads)
+    return fail(FCPB_ERR_UNSUPPORTED, "num_q_heads %d (max %d)", num_q_heads, fcpb::aux::kPrepMaxHeads);
+  if (tokens == 0) return FCPB_OK;
   const int block = 256;
-  const int64_t grid = (rows * 32 + block - 1) / block;
+  const int64_t grid = (tokens + fcpb::aux::kPrepTokens - 1) / fcpb::aux::kPrepTokens;
   fcpb::aux::bwd_preprocess_kernel<<<static_cast<unsigned>(grid), block, 0,
                                      static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, lse2_t,
-      delta_t, t_pad, dq_accum, rows, num_q_heads);
+      delta_t, t_pad, dq_accum, tokens, num_q_heads);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
