@@ -46,6 +46,9 @@ class FcpExecutor:
         if check_plan and self.world > 1:
             exchange.sync_plan_digest(plan_digest(result, cfg), group)
         self.work = build_rank_work(result, rank)
+        self.fuse_remote = self._fuse_remote_waves(result, rank, cfg)
+        if self.fuse_remote:
+            self.work = build_rank_work(result, rank, fuse_remote=True)
         self.layout = self.work.layout
         self.op = BlockAttention(self.work, cfg, self.device, softmax_scale, num_ctas)
         # The exchange runs on copy engines (p2p.SymmetricExchange), so the persistent
@@ -70,6 +73,24 @@ class FcpExecutor:
         self.v_recv = torch.empty((R, Hk, D), dtype=torch.bfloat16, device=self.device) if R else None
         self.kv_bytes_per_token = 2 * Hk * D * 2
         self._marks = None          # optional per-phase CUDA-event timeline (see timeline())
+
+    def _fuse_remote_waves(self, result, rank, cfg) -> bool:
+        """One remote forward wave instead of one per stage when this rank's pulls are
+        expected to finish while its local wave still runs: copy-engine pulls at ~200 GB/s
+        (measured 260-480 GB/s) against the local wave at ~600 TFLOP/s.  Then waiting for
+        the last stage costs nothing and one launch saves the other waves' tails.
+        FCPB_FUSE_REMOTE=0/1 overrides (experiments)."""
+        import os
+        env = os.environ.get("FCPB_FUSE_REMOTE")
+        if env is not None:
+            return env == "1"
+        waves = self.work.fwd.waves
+        if self.world == 1 or sum(1 for w in waves if w.stage != LOCAL_WAVE) < 2:
+            return False
+        recv_s = self.work.layout.recv_tokens * 2 * cfg.kv_heads * cfg.head_dim * 2 / 200e9
+        local = sum(w.pairs for w in waves if w.stage == LOCAL_WAVE)
+        local_s = local * cfg.flops_per_token_pair / 600e12
+        return recv_s <= local_s
 
     # ------------------------------------------------------------------ timeline
     def timeline(self, enabled: bool = True):

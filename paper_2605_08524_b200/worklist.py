@@ -161,15 +161,21 @@ def _lpt_order(items):
     return sorted(items, key=lambda t: (-t[0], t[1], t[2]))
 
 
-def build_forward(result: ScheduleResult, lay: RankLayout) -> FwdPlan:
+def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = False) -> FwdPlan:
+    """Forward waves.  fuse_remote: every received KV chunk goes into one wave released by
+    this rank's last arrival stage (one launch, one tail, and at most a local and a remote
+    partial per Q chunk) instead of one wave per coalesced stage."""
     deps = result.deps
     causal = deps.mask == CAUSAL
+    last_stage = max(lay.recv_stage.values(), default=LOCAL_WAVE)
     # per Q chunk: wave -> ordered kv list
     per_q: dict[ChunkKey, dict[int, list[tuple[int, int, int, int]]]] = {}
     for q in lay.chunks:
         waves: dict[int, list] = {}
         for kv in deps.q_to_kv[q]:
             wave, off, flags = _kv_location(lay, kv)
+            if fuse_remote and wave != LOCAL_WAVE:
+                wave = last_stage
             if causal and kv == q:
                 flags |= KV_DIAG
             waves.setdefault(wave, []).append((off, deps.chunk_tokens[kv], flags, 0))
@@ -295,8 +301,8 @@ def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
                   pairs)
 
 
-def build_rank_work(result: ScheduleResult, rank: int) -> RankWork:
+def build_rank_work(result: ScheduleResult, rank: int, fuse_remote: bool = False) -> RankWork:
     lay = rank_layout(result, rank)
-    fwd = build_forward(result, lay)
+    fwd = build_forward(result, lay, fuse_remote)
     bwd = build_backward(result, lay)
     return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves), build_dq(result, lay))

@@ -25,10 +25,11 @@ from paper_2605_08524_b200.worklist import build_rank_work
 MODEL = ModelConfig(q_heads=4, kv_heads=2, head_dim=32, dtype_bytes=2)
 
 
-def _schedule(lengths, n, block, mask="causal"):
+def _schedule(lengths, n, block, mask="causal", coalesce=16):
     tpw = -(-sum(lengths) // n)
     batch = Batch(tuple(Sequence(i, l) for i, l in enumerate(lengths)), n, tpw)
-    return fcp_schedule(batch, n, ShardingConfig(block, mask), MODEL, DEFAULT_EFFICIENCY)
+    return fcp_schedule(batch, n, ShardingConfig(block, mask), MODEL, DEFAULT_EFFICIENCY,
+                        coalesce_degree=coalesce)
 
 
 def _inputs(T, seed=0):
@@ -90,15 +91,20 @@ def test_tiled_equals_dense(mask):
     assert torch.allclose(l1, l2, atol=1e-10)
 
 
-@pytest.mark.parametrize("n,lengths,block", [
-    (1, [700, 260, 130, 100, 50, 9], 256),
-    (2, [700, 260, 130, 100, 50, 9], 256),
-    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256),
+@pytest.mark.parametrize("fuse", [False, True])
+@pytest.mark.parametrize("n,lengths,block,coalesce", [
+    (1, [700, 260, 130, 100, 50, 9], 256, 16),
+    (2, [700, 260, 130, 100, 50, 9], 256, 16),
+    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 16),
+    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 1),     # many stages: fusion matters
 ])
-def test_worklist_emulation_matches_dense(n, lengths, block):
-    """Simulated workers: per-rank work lists + in-process exchange == dense attention."""
-    r = _schedule(lengths, n, block)
-    works = [build_rank_work(r, w) for w in range(n)]
+def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, fuse):
+    """Simulated workers: per-rank work lists + in-process exchange == dense attention,
+    with one forward wave per arrival stage or all remote KV fused into one wave."""
+    r = _schedule(lengths, n, block, coalesce=coalesce)
+    works = [build_rank_work(r, w, fuse_remote=fuse) for w in range(n)]
+    if fuse:
+        assert all(sum(1 for wv in wk.fwd.waves if wv.stage >= 0) <= 1 for wk in works)
     goff, T = global_offsets(r)
     q, k, v, do = _inputs(T, 3)
     scale = 1 / math.sqrt(MODEL.head_dim)
