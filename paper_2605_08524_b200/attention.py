@@ -42,6 +42,9 @@ def _check(t, name, shape, dtype=torch.bfloat16):
         raise ParameterError(f"{name} must be contiguous")
 
 
+# per-rank tokens from which the head-major work order pays (see BlockAttention.__init__)
+HEAD_MAJOR_MIN_TOKENS = 40960
+
 class BlockAttention:
     def __init__(self, work: RankWork, cfg: ModelConfig, device=None,
                  softmax_scale: float | None = None, num_ctas: int = 0):
@@ -69,13 +72,17 @@ class BlockAttention:
         self._dq = (d, _dev_i32(d.segments, dev), _dev_i32(d.kvrefs, dev), _dev_i32(d.items, dev))
         self.launches = 0   # kernel launches issued by this object (bench accounting)
         import os
-        # Work order of the dynamic scheduler: head-major (all items of one head, LPT order,
-        # before the next head) keeps one head's Q/dO (or K/V) stream resident in L2.  On
-        # C2 it cut DRAM reads 17.8 -> 2.6 GB (dK/dV), 5.0 -> 1.4 GB (dQ), 3.5 -> 0.9 GB (fwd)
-        # per launch, which under the B200's 1 kW power cap is time (profiles/r01_notes.md).
-        # FCPB_SCHED="f,b,q" overrides it for experiments.
+        # Work order of the dynamic scheduler.  Head-major (all items of one head, LPT order,
+        # before the next head) keeps one head's Q/dO (or K/V) stream resident in L2: on C2
+        # at N=1 it cut DRAM reads 17.8 -> 2.6 GB (dK/dV), 5.0 -> 1.4 GB (dQ), 3.5 -> 0.9 GB
+        # (fwd) per launch, which under the 1 kW power cap is time.  But it starts the
+        # largest items of the last heads late, a tail that grows as the per-rank work
+        # shrinks.  Measured step time (profiles/r01_notes.md): head-major wins for C2 at N=1
+        # (63K tokens/rank) and C3 at N=1/4 (>= 419K), head-interleaved wins for C2 at N=2/4
+        # (31K / 16K tokens/rank) by 2.7% / 3.4%.  FCPB_SCHED="f,b,q" overrides.
         sched = os.environ.get("FCPB_SCHED", "")
-        flags = [int(x) for x in sched.split(",")] if sched else [1, 1, 1]
+        hm = 1 if self.tokens >= HEAD_MAJOR_MIN_TOKENS else 0
+        flags = [int(x) for x in sched.split(",")] if sched else [hm, hm, hm]
         self.head_major = {"fwd": flags[0], "bwd": flags[1], "dq": flags[2]}
         # one dynamic-scheduler counter per kernel kind (zeroed by the C ABI before each launch)
         self._sched = torch.zeros(4, dtype=torch.int32, device=self.device)
