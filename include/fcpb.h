@@ -65,6 +65,7 @@ typedef struct {
   const FcpbItem* items;       int32_t num_items;     /* LPT-ordered                  */
   int32_t num_ctas;            /* 0 = one per SM                                      */
   int32_t head_major;          /* grid order: 0 = heads of an item adjacent, 1 = items of a head */
+  int32_t hm_lead;             /* head_major: the first hm_lead (largest) items still run heads-adjacent */
   int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbFwdArgs;
 
@@ -115,6 +116,7 @@ typedef struct {
   const FcpbItem* items;       int32_t num_items;
   int32_t num_ctas;
   int32_t head_major;
+  int32_t hm_lead;
   int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbDqArgs;
 
@@ -158,6 +160,7 @@ typedef struct {
   const FcpbBwdItem* items; int32_t num_items;
   int32_t num_ctas;
   int32_t head_major;
+  int32_t hm_lead;
   int32_t* sched_counter;      /* device int scratch for the dynamic tile scheduler (zeroed here) */
 } FcpbBwdArgs;
 

@@ -94,6 +94,7 @@ struct Params {
   int32_t num_items;
   int32_t num_q_heads, num_kv_heads;
   int32_t head_major;
+  int32_t hm_lead;         // head_major: items run heads-adjacent before the head-major rest
   float scale;            // softmax scale
   float scale_log2;       // scale * log2(e)
   const float* lse2_t;    // [Hq, t_pad] -lse * log2(e)
@@ -108,8 +109,16 @@ struct Params {
 
 // Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
 // one head (they stream the same Q/dO tiles); else the heads of one item.
-FCPB_DEV int item_of(int g, const Params& p) { return p.head_major ? g % p.num_items : g / p.num_kv_heads; }
-FCPB_DEV int head_of(int g, const Params& p) { return p.head_major ? g / p.num_items : g % p.num_kv_heads; }
+FCPB_DEV int item_of(int g, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, p.num_kv_heads, p.head_major, p.hm_lead, it, h);
+  return it;
+}
+FCPB_DEV int head_of(int g, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, p.num_kv_heads, p.head_major, p.hm_lead, it, h);
+  return h;
+}
 
 // Q blocks (128 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= nb.
 FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? nb : 0; }

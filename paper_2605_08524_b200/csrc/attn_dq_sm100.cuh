@@ -90,6 +90,7 @@ struct Params {
   int32_t num_items;
   int32_t num_q_heads, num_kv_heads;
   int32_t head_major;      // grid index -> (item, head) mapping, see item_of()
+  int32_t hm_lead;         // head_major: items run heads-adjacent before the head-major rest
   float scale, scale_log2;
   const __nv_bfloat16* q;  // [Tq, Hq, D]
   const __nv_bfloat16* dout;
@@ -99,8 +100,16 @@ struct Params {
   __nv_bfloat16* dq;       // [Tq, Hq, D] bf16 output
 };
 
-FCPB_DEV int item_of(int g, const Params& p) { return p.head_major ? g % p.num_items : g / p.num_q_heads; }
-FCPB_DEV int head_of(int g, const Params& p) { return p.head_major ? g / p.num_items : g % p.num_q_heads; }
+FCPB_DEV int item_of(int g, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, p.num_q_heads, p.head_major, p.hm_lead, it, h);
+  return it;
+}
+FCPB_DEV int head_of(int g, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, p.num_q_heads, p.head_major, p.hm_lead, it, h);
+  return h;
+}
 
 FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
   int n = (ref.len + kBN - 1) / kBN;

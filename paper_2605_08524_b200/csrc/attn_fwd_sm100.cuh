@@ -63,6 +63,7 @@ struct Params {
   int32_t num_q_heads;
   int32_t num_kv_heads;
   int32_t head_major;    // grid index -> (item, head pair) mapping
+  int32_t hm_lead;         // head_major: items run heads-adjacent before the head-major rest
   float scale_log2;      // softmax_scale * log2(e)
   float scale;           // softmax_scale
   __nv_bfloat16* o;      // [Tq, Hq, D]
@@ -71,8 +72,16 @@ struct Params {
   float* lse_part;       // [P, Hq]
 };
 
-FCPB_DEV int item_of(int g, int hp, const Params& p) { return p.head_major ? g % p.num_items : g / hp; }
-FCPB_DEV int pair_of(int g, int hp, const Params& p) { return p.head_major ? g / p.num_items : g % hp; }
+FCPB_DEV int item_of(int g, int hp, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, hp, p.head_major, p.hm_lead, it, h);
+  return it;
+}
+FCPB_DEV int pair_of(int g, int hp, const Params& p) {
+  int it, h;
+  grid_map(g, p.num_items, hp, p.head_major, p.hm_lead, it, h);
+  return h;
+}
 
 // Number of 128-row KV tiles a Q tile at m-block `mb` visits in `ref`.
 FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {

@@ -135,6 +135,7 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   p.o_part = a->o_partial;
   p.lse_part = a->lse_partial;
   p.head_major = a->head_major;
+  p.hm_lead = a->hm_lead;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
@@ -189,6 +190,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.t_pad = a->t_pad;
   p.q_tokens = static_cast<int32_t>(a->q_tokens);
   p.head_major = a->head_major;
+  p.hm_lead = a->hm_lead;
   p.dk = a->dk_accum;
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
@@ -247,6 +249,7 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   p.q = static_cast<const __nv_bfloat16*>(a->q);
   p.dout = static_cast<const __nv_bfloat16*>(a->dout);
   p.head_major = a->head_major;
+  p.hm_lead = a->hm_lead;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));

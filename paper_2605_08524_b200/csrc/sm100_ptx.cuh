@@ -298,6 +298,24 @@ FCPB_DEV int sched_consume(SchedRing& r, SchedCursor& c) {
   return g;
 }
 
+// ----------------------------------------------------------------------------- work order
+// Grid index g -> (item, head) for `items` LPT-ordered items x `heads` heads.
+// head_major == 0: the heads of an item are adjacent.  Otherwise the first `lead` items run
+// heads-adjacent (every head's largest items start first, no late tail) and the remaining
+// items run head-major (one head's operand stream at a time stays in L2).
+FCPB_DEV void grid_map(int g, int items, int heads, int head_major, int lead, int& item, int& head) {
+  const int k = head_major ? (lead < items ? lead : items) : items;
+  if (g < k * heads) {
+    item = g / heads;
+    head = g % heads;
+    return;
+  }
+  g -= k * heads;
+  const int rest = items - k;
+  item = k + g % rest;
+  head = g / rest;
+}
+
 // ----------------------------------------------------------------------------- math
 FCPB_DEV float ex2(float x) {
   float y;

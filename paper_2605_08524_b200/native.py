@@ -29,7 +29,7 @@ class FwdArgs(ctypes.Structure):
                 ("segments", c_vp), ("num_segments", c_i32),
                 ("kv_refs", c_vp), ("num_kv_refs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
-                ("num_ctas", c_i32), ("head_major", c_i32), ("sched_counter", c_vp)]
+                ("num_ctas", c_i32), ("head_major", c_i32), ("hm_lead", c_i32), ("sched_counter", c_vp)]
 
 
 class MergeArgs(ctypes.Structure):
@@ -52,7 +52,7 @@ class BwdArgs(ctypes.Structure):
                 ("kvsegs", c_vp), ("num_kvsegs", c_i32),
                 ("qrefs", c_vp), ("num_qrefs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
-                ("num_ctas", c_i32), ("head_major", c_i32), ("sched_counter", c_vp)]
+                ("num_ctas", c_i32), ("head_major", c_i32), ("hm_lead", c_i32), ("sched_counter", c_vp)]
 
 
 class DqArgs(ctypes.Structure):
@@ -66,7 +66,7 @@ class DqArgs(ctypes.Structure):
                 ("segments", c_vp), ("num_segments", c_i32),
                 ("kv_refs", c_vp), ("num_kv_refs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
-                ("num_ctas", c_i32), ("head_major", c_i32), ("sched_counter", c_vp)]
+                ("num_ctas", c_i32), ("head_major", c_i32), ("hm_lead", c_i32), ("sched_counter", c_vp)]
 
 
 EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_lse_merge", "fcpb_bwd_preprocess",
