@@ -155,6 +155,9 @@ typedef struct {
   float* dq_accum;              /* unused (dQ comes from fcpb_attn_bwd_dq); may be NULL */
   float* dk_accum; float* dv_accum;             /* local  [Tkv, Hkv, D] fp32         */
   float* dk_recv_accum; float* dv_recv_accum;   /* recv   [Trecv, Hkv, D] fp32       */
+  void* dk_out; void* dv_out;   /* optional bf16 [Tkv, Hkv, D]: local segments write the final
+                                   (scaled) dK/dV here instead of dk/dv_accum -- only when no
+                                   partials of this rank's chunks come back from peers      */
   const FcpbBwdKvSeg* kvsegs; int32_t num_kvsegs;
   const FcpbBwdQRef* qrefs; int32_t num_qrefs;
   const FcpbBwdItem* items; int32_t num_items;

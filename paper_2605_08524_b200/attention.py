@@ -228,7 +228,10 @@ class BlockAttention:
                 torch.empty(shape, dtype=torch.float32, device=self.device))
 
     def backward_launch(self, recv: bool, q, k, v, k_recv, v_recv, prep, do,
-                        dk, dv, dk_r, dv_r, stream=None):
+                        dk, dv, dk_r, dv_r, stream=None, dk_out=None, dv_out=None):
+        """K2 over the received (recv=True) or local chunks.  dk_out/dv_out (bf16): local
+        chunks write their final dK/dV there directly -- only when no partials of this
+        rank's chunks come back from peers."""
         for b, kvsegs, qrefs, items in self._bwd:
             if b.recv != recv:
                 continue
@@ -243,6 +246,7 @@ class BlockAttention:
             a.k_recv, a.v_recv, a.kv_recv_tokens = native.ptr(k_recv), native.ptr(v_recv), self.recv_tokens
             a.dq_accum, a.dk_accum, a.dv_accum = None, native.ptr(dk), native.ptr(dv)
             a.dk_recv_accum, a.dv_recv_accum = native.ptr(dk_r), native.ptr(dv_r)
+            a.dk_out, a.dv_out = native.ptr(dk_out), native.ptr(dv_out)
             a.kvsegs, a.num_kvsegs = native.ptr(kvsegs), len(b.kvsegs)
             a.qrefs, a.num_qrefs = native.ptr(qrefs), len(b.qrefs)
             a.items, a.num_items = native.ptr(items), len(b.items)

@@ -105,6 +105,8 @@ struct Params {
   float* dv;
   float* dk_recv;         // recv   [Tr, Hkv, D] fp32
   float* dv_recv;
+  __nv_bfloat16* dk_out;  // optional final bf16 [Tkv, Hkv, D] for local segments
+  __nv_bfloat16* dv_out;
 };
 
 // Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
@@ -488,14 +490,31 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       tc_fence_after();
       {
         const bool recv = ks.flags & FCPB_KV_RECV;
-        float* dkb = recv ? p.dk_recv : p.dk;
-        float* dvb = recv ? p.dv_recv : p.dv;
         const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD + wg * 32;
         uint32_t a[32], bb[32];
         tmem_ld32(tmem + lane_bits + kColDK + wg * 32, a);
         tmem_ld32(tmem + lane_bits + kColDV + wg * 32, bb);
         tmem_wait_ld();
-        if (kv_live) {
+        if (kv_live && !recv && p.dk_out) {      // final bf16 (no partials come back)
+          uint4* k4 = reinterpret_cast<uint4*>(p.dk_out + row);
+          uint4* v4 = reinterpret_cast<uint4*>(p.dv_out + row);
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            uint4 wk, wv;
+            wk.x = pack_bf16(__uint_as_float(a[i]) * p.scale, __uint_as_float(a[i + 1]) * p.scale);
+            wk.y = pack_bf16(__uint_as_float(a[i + 2]) * p.scale, __uint_as_float(a[i + 3]) * p.scale);
+            wk.z = pack_bf16(__uint_as_float(a[i + 4]) * p.scale, __uint_as_float(a[i + 5]) * p.scale);
+            wk.w = pack_bf16(__uint_as_float(a[i + 6]) * p.scale, __uint_as_float(a[i + 7]) * p.scale);
+            wv.x = pack_bf16(__uint_as_float(bb[i]), __uint_as_float(bb[i + 1]));
+            wv.y = pack_bf16(__uint_as_float(bb[i + 2]), __uint_as_float(bb[i + 3]));
+            wv.z = pack_bf16(__uint_as_float(bb[i + 4]), __uint_as_float(bb[i + 5]));
+            wv.w = pack_bf16(__uint_as_float(bb[i + 6]), __uint_as_float(bb[i + 7]));
+            k4[i / 8] = wk;
+            v4[i / 8] = wv;
+          }
+        } else if (kv_live) {
+          float* dkb = recv ? p.dk_recv : p.dk;
+          float* dvb = recv ? p.dv_recv : p.dv;
           float4* k4 = reinterpret_cast<float4*>(dkb + row);
           float4* v4 = reinterpret_cast<float4*>(dvb + row);
 #pragma unroll

@@ -195,6 +195,8 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.dv = a->dv_accum;
   p.dk_recv = a->dk_recv_accum;
   p.dv_recv = a->dv_recv_accum;
+  p.dk_out = static_cast<__nv_bfloat16*>(a->dk_out);
+  p.dv_out = static_cast<__nv_bfloat16*>(a->dv_out);
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));

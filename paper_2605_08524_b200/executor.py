@@ -177,7 +177,8 @@ class FcpExecutor:
         cur = torch.cuda.current_stream(self.device)
         prep = op.backward_prepare(o, lse, do, cur)
         self._mark("bwd_prep", cur)
-        dk, dv = op.alloc_dkv(False)
+        final = self.ret_tokens == 0     # see below: dK/dV written straight to bf16
+        dk, dv = (None, None) if final else op.alloc_dkv(False)
         x = self.xchg
         staged = None
         if x is not None and self.stages:
@@ -198,7 +199,14 @@ class FcpExecutor:
         else:
             dk_r, dv_r = op.alloc_dkv(True)
             args = (q, k, v, self.k_recv, self.v_recv, prep, do, dk, dv, dk_r, dv_r, cur)
-        op.backward_launch(False, *args)
+        # No partial of this rank's chunks comes back (always at N=1): the dK/dV kernel
+        # writes the final bf16 gradients itself (no fp32 round trip, no convert launches).
+        if final:
+            dk_b = torch.empty(k.shape, dtype=torch.bfloat16, device=self.device)
+            dv_b = torch.empty(v.shape, dtype=torch.bfloat16, device=self.device)
+            op.backward_launch(False, *args, dk_out=dk_b, dv_out=dv_b)
+        else:
+            op.backward_launch(False, *args)
         self._mark("bwd_dkv_local", cur)
         dq = op.backward_dq(q, k, v, self.k_recv, self.v_recv, prep, do, cur)
         self._mark("bwd_dq", cur)
@@ -208,7 +216,7 @@ class FcpExecutor:
             for src, dst in self.ret_rounds:        # K4, one race-free round per receiver rank
                 op.reduce_dkv(dk, staged[0].index_select(0, src), dst, cur)
                 op.reduce_dkv(dv, staged[1].index_select(0, src), dst, cur)
-        out = dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur)
+        out = (dq, dk_b, dv_b) if final else (dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur))
         self._mark("bwd_reduce_convert", cur)
         return out
 

@@ -48,7 +48,7 @@ class BwdArgs(ctypes.Structure):
                 ("k", c_vp), ("v", c_vp), ("kv_tokens", c_i64),
                 ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
                 ("dq_accum", c_vp), ("dk_accum", c_vp), ("dv_accum", c_vp),
-                ("dk_recv_accum", c_vp), ("dv_recv_accum", c_vp),
+                ("dk_recv_accum", c_vp), ("dv_recv_accum", c_vp), ("dk_out", c_vp), ("dv_out", c_vp),
                 ("kvsegs", c_vp), ("num_kvsegs", c_i32),
                 ("qrefs", c_vp), ("num_qrefs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),

@@ -103,3 +103,32 @@ def test_measured_report_single_rank():
     assert len(rep.per_worker) == 1 and rep.stages == []
     assert 0 < rep.per_worker[0].compute_time <= rep.total_time * 1.05
     assert rep.total_flops == 3.5 * GQA_SMALL.flops_per_token_pair * batch_token_pairs(lengths, "causal")
+
+
+def test_executor_single_rank_parity():
+    """FcpExecutor at N=1 (the bench path): no partials come back, so the dK/dV kernel
+    writes the final bf16 gradients directly; checked against the fp64 oracle."""
+    import math
+    from oracle.attention_ref import mono_bwd, mono_fwd
+    from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows
+    from paper_2605_08524_b200.executor import FcpExecutor
+    from tests.gpu_harness import err, REL_L2, LSE_ABS
+    model = GQA_SMALL
+    r = schedule([1500, 700, 300, 129, 40], 1, 512, model)
+    goff, T = global_offsets(r)
+    q, k, v, do = make_inputs(T, model)
+    ex = FcpExecutor(r, 0, model, torch.device("cuda", 0))
+    assert ex.ret_tokens == 0
+    loc = [gather_rank(x, ex.layout, goff, r.deps).cuda() for x in (q, k, v, do)]
+    o, lse, dq, dk, dv = ex.step(*loc)
+    assert dk.dtype == torch.bfloat16 and dv.dtype == torch.bfloat16
+    rows = global_sequence_rows(r)
+    scale = 1 / math.sqrt(model.head_dim)
+    qf, kf, vf, dof = (x.double() for x in (q, k, v, do))
+    ro, rl = mono_fwd(qf, kf, vf, rows, scale)
+    rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
+    rep = {n: err(g.cpu(), gather_rank(ref, ex.layout, goff, r.deps))
+           for n, g, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv))}
+    _report("executor N=1", rep)
+    for n, e in rep.items():
+        assert (e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2), (n, e)
