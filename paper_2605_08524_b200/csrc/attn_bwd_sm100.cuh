@@ -28,6 +28,10 @@
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
 
+#ifndef FCPB_BWD_POLY
+#define FCPB_BWD_POLY 1
+#endif
+
 namespace fcpb {
 namespace bwd {
 
@@ -162,7 +166,11 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p,
       // Phase 1 is MUFU-bound (2 warps x 64 ex2 per SMSP per tile): every other pair goes
       // to the FMA pipe (FA4-style), which measured-balances MUFU time against issue slots.
       float p0, p1;
-      if (u & 1) {
+      // poly pairs per 4: FCPB_BWD_POLY (0..3); cycles on C2 with four softmax warpgroups:
+      // 0: 13.50M, 1: 13.06M, 2: 13.37M, 3: 14.24M
+      const bool use_poly = FCPB_BWD_POLY == 0 ? false : FCPB_BWD_POLY == 1 ? (u & 3) == 3
+                            : FCPB_BWD_POLY == 2 ? (u & 1) != 0 : (u & 3) != 0;
+      if (use_poly) {
         const float2 e = ex2_poly2(x);
         p0 = e.x;
         p1 = e.y;
