@@ -28,6 +28,9 @@
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
 
+#ifndef FCPB_DQ_POLY
+#define FCPB_DQ_POLY 1    // polynomial exp2 pairs per 4 (0..3)
+#endif
 #ifndef FCPB_DQ_SPIN
 #define FCPB_DQ_SPIN 1    // 1: MMA warp spins on ds_full; 2: also the softmax's dP wait
 #endif
@@ -129,7 +132,9 @@ FCPB_DEV void p_cols(const uint32_t (&s)[kCols], float c, float nlse, float (&pr
     const int i = 2 * u;
     const float2 x = __ffma2_rn(make_float2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), c2, nl);
     float p0, p1;
-    if ((u & 3) == 3) {
+    const bool use_poly = FCPB_DQ_POLY == 0 ? false : FCPB_DQ_POLY == 1 ? (u & 3) == 3
+                          : FCPB_DQ_POLY == 2 ? (u & 1) != 0 : (u & 3) != 0;
+    if (use_poly) {
       const float2 e = ex2_poly2(x);
       p0 = e.x;
       p1 = e.y;
