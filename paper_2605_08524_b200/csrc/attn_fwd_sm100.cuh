@@ -268,9 +268,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
         mbar_wait(&sm.q_full, q_phase);
         q_phase ^= 1;
-        // S(0) only needs the S columns (the previous item's last P was read by its last PV,
-        // earlier in the in-order pipe), so it runs while the epilogue still drains O; the
-        // O accumulators are waited for right before each head's first PV below.
+        // O accumulators of the previous item must have been drained by the epilogue.
+        mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
+        mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
+        oe_phase ^= 1;
         tc_fence_after();
         // K(0)
         const uint32_t ks = take_full();
@@ -283,7 +284,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           const uint32_t vs = take_full();
           mbar_wait(&sm.p_full[0], p_phase);
           FCPB_FWTR(kFwP0Got, trt);
-          if (j == 0) mbar_wait(&sm.o_empty[0], oe_phase ^ 1);   // previous item's O0 drained
           tc_fence_after();
           issue_pv(0, vs, j > 0);
           FCPB_FWTR(kFwPv0Issue, trt);
@@ -298,10 +298,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           }
           mbar_wait(&sm.p_full[1], p_phase);
           FCPB_FWTR(kFwP1Got, trt);
-          if (j == 0) {
-            mbar_wait(&sm.o_empty[1], oe_phase ^ 1);               // previous item's O1 drained
-            oe_phase ^= 1;
-          }
           tc_fence_after();
           issue_pv(1, vs, j > 0);
           FCPB_FWTR(kFwPv1Issue, trt);
