@@ -50,14 +50,14 @@ def err(a, b):
             "ref_max": b.abs().max().item()}
 
 
-def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True):
+def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True, fuse_remote=False):
     """Execute every rank's work list with the CUDA kernels; the exchange is an
     on-device gather of the owners' K/V, the dKV return uses the K4 kernel."""
     n = result.assignment.n_workers
     deps = result.deps
     goff, T = global_offsets(result)
     owner = chunk_placement(result.assignment, result.units)
-    works = [build_rank_work(result, w) for w in range(n)]
+    works = [build_rank_work(result, w, fuse_remote=fuse_remote) for w in range(n)]
     ops = [BlockAttention(w, model, device) for w in works]
     o = torch.zeros((T, model.q_heads, model.head_dim), dtype=torch.bfloat16)
     lse = torch.zeros((T, model.q_heads), dtype=torch.float32)

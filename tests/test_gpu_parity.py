@@ -24,12 +24,13 @@ def _report(name, rep):
     print(f"\n[parity] {name}: " + json.dumps(rep))
 
 
-def _full_check(lengths, n, block, model, mask="causal", seq_ids=None, backward=True):
+def _full_check(lengths, n, block, model, mask="causal", seq_ids=None, backward=True,
+                fuse_remote=False):
     r = schedule(lengths, n, block, model, mask)
     from oracle.simworkers import global_offsets
     _, T = global_offsets(r)
     q, k, v, do = make_inputs(T, model)
-    gpu = run_plan_on_gpu(r, model, q, k, v, do, backward=backward)
+    gpu = run_plan_on_gpu(r, model, q, k, v, do, backward=backward, fuse_remote=fuse_remote)
     ref, idx = oracle(r, model, q, k, v, do, seq_ids)
     keys = ("o", "lse", "dq", "dk", "dv") if backward else ("o", "lse")
     rep = compare(gpu, ref, idx, keys)
@@ -132,3 +133,18 @@ def test_executor_single_rank_parity():
     _report("executor N=1", rep)
     for n, e in rep.items():
         assert (e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2), (n, e)
+
+
+def test_fwd_bwd_eight_simulated_ranks():
+    """N=8 plan structures on one GPU (simulated workers): many stages, chunks with several
+    receivers (race-free K4 rounds), merges of multi-stage partials."""
+    rep = _full_check([4000, 3100, 2100, 1500, 1000, 700, 520, 300, 129, 128, 64, 5], 8, 512, GQA_SMALL)
+    _report("ragged N=8", rep)
+    assert_within_tolerance(rep)
+
+
+def test_fwd_bwd_four_simulated_ranks_fused_remote_wave():
+    """All received KV of a rank in one forward wave (the executor's fused-remote policy)."""
+    rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 512, GQA_SMALL, fuse_remote=True)
+    _report("ragged N=4 fused remote wave", rep)
+    assert_within_tolerance(rep)
