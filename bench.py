@@ -438,6 +438,39 @@ def main():
             dist.all_reduce(g, op=dist.ReduceOp.MIN)
             xbw[key]["GBps_min_over_ranks"] = g.item()
 
+    # transparent reshuffler (§8f, N > 1): user layout -> FCP layout for Q/K/V/dO and back
+    # for O/LSE/dQ/dK/dV, measured on the comm path, beside the reference's analytic cost
+    reshuffle = None
+    if world > 1:
+        from paper_2605_08524_b200.costmodel import B200_HARDWARE, DEFAULT_EFFICIENCY as _EFF
+        from paper_2605_08524_b200.reshuffle import Reshuffler
+        from paper_2605_08524_b200.simmodel import default_contiguous_layout, reshuffle_cost
+        rs = Reshuffler(result, rank, cfg, device)
+        tu = rs.plan.user_tokens
+        usr = [torch.randn((tu,) + tuple(x.shape[1:]), device=device).to(x.dtype) for x in (q, k, v, do)]
+        fin = ex.step(q, k, v, do)
+        tms = []
+        for _ in range(4):
+            barrier()
+            torch.cuda.synchronize()
+            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record(stream)
+            rs.to_fcp(*usr)
+            b.record(stream)
+            rs.from_fcp(*fin)
+            c.record(stream)
+            torch.cuda.synchronize()
+            tms.append((a.elapsed_time(b), b.elapsed_time(c)))
+        to_ms, from_ms = sorted(tms)[len(tms) // 2]
+        t = torch.tensor([to_ms, from_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rc = reshuffle_cost(default_contiguous_layout(result.units, n), result.assignment, result.units,
+                            result.deps, B200_HARDWARE, cfg, _EFF)
+        reshuffle = {"to_fcp_ms_max_over_ranks": t[0].item(), "from_fcp_ms_max_over_ranks": t[1].item(),
+                     "reference_model": {"to_fcp_ms_at_900GBps": rc.time * 1e3,
+                                         "hidden_fraction": rc.hidden_fraction,
+                                         "total_bytes": rc.total_bytes}}
+
     t = torch.tensor([ms], device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -485,6 +518,7 @@ def main():
             "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
             "exchange_bytes_rank0": exb,
             "exchange_bw_rank0": xbw,
+            "reshuffle": reshuffle,
             "phases_ms_rank0": {kk: round(vv, 3) for kk, vv in phases.items()},
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,

@@ -1,0 +1,198 @@
+"""the transparent reshuffler -- user layout <-> FCP layout over NVLink.
+
+A model keeps its activations in a *user layout*: each rank holds a contiguous share of
+the batch's chunks.  This is the reference's ``default_contiguous_layout``
+(``simulator.py:279-291``): chunks fill ranks in unit order; any other chunk -> rank map
+can be passed instead.  FCP computes in the plan's layout (``worklist.rank_layout``).  The
+reshuffler moves every row of Q/K/V/dO into the FCP layout before the attention step and
+every row of O/LSE/dQ/dK/dV back afterwards, so the op drops into a model without
+touching its data loader.
+
+* Plan (host, every rank, deterministic): for each chunk a rank owns in the destination
+  layout, pull it from the rank that holds it in the source layout.  Contiguous runs on
+  the same peer are merged.  A chunk whose two owners coincide is a local copy.  The
+  bytes moved are exactly the reference's ``reshuffle_cost`` accounting
+  (``simulator.py:294-342``); ``tests/test_reshuffle.py`` checks that.
+* Transport (GPU): one symmetric-memory byte buffer (``torch.distributed._symmetric_memory``)
+  with one contiguous region per tensor of a call, so each call is:
+  1. one contiguous publish per tensor;
+  2. one device barrier;
+  3. copy-engine pulls of whole contiguous row runs from the peers' regions, straight into
+     the output tensors;
+  4. one barrier.
+  This is the same transport as the KV exchange (``p2p.py``).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from .costmodel import ModelConfig
+from .distributor import chunk_placement
+from .errors import ConsistencyError, ParameterError
+from .pipeline import ScheduleResult
+from .simmodel import default_contiguous_layout
+from .worklist import rank_layout
+
+
+@dataclass
+class UserLayout:
+    """One rank's share of the user layout: its chunks in user order and their rows."""
+    rank: int
+    chunks: list
+    offset: dict
+    tokens: int
+
+
+def user_layouts(result: ScheduleResult, initial_layout=None) -> list[UserLayout]:
+    """Per-rank user layouts.  ``initial_layout``: ChunkKey -> rank (default: the
+    reference's contiguous layout); rows follow unit order, then member order."""
+    n = result.assignment.n_workers
+    init = initial_layout if initial_layout is not None else default_contiguous_layout(result.units, n)
+    keys = {c.key for u in result.units for c in u.members}
+    if set(init) != keys:
+        raise ConsistencyError("initial layout covers a different chunk set")
+    out = [UserLayout(r, [], {}, 0) for r in range(n)]
+    for u in result.units:
+        for c in u.members:
+            r = init[c.key]
+            if not 0 <= r < n:
+                raise ParameterError(f"initial layout puts {c.key} on rank {r} (N={n})")
+            lay = out[r]
+            lay.offset[c.key] = lay.tokens
+            lay.chunks.append(c.key)
+            lay.tokens += c.token_count
+    return out
+
+
+def _append(pulls, pull):
+    """Append (peer, src_row, dst_row, n), merging with a contiguous predecessor."""
+    if pulls:
+        pp, ps, pd, pn = pulls[-1]
+        peer, src, dst, n = pull
+        if pp == peer and ps + pn == src and pd + pn == dst:
+            pulls[-1] = (pp, ps, pd, pn + n)
+            return
+    pulls.append(pull)
+
+
+@dataclass
+class ReshufflePlan:
+    """Row moves of one rank, both directions: (peer, src_row, dst_row, rows)."""
+    rank: int
+    to_fcp: list
+    from_fcp: list
+    user_tokens: int
+    fcp_tokens: int
+
+
+def reshuffle_plans(result: ScheduleResult, initial_layout=None) -> list[ReshufflePlan]:
+    n = result.assignment.n_workers
+    users = user_layouts(result, initial_layout)
+    fcps = [rank_layout(result, r) for r in range(n)]
+    user_of = {c: u.rank for u in users for c in u.chunks}
+    owner = chunk_placement(result.assignment, result.units)
+    tokens = result.deps.chunk_tokens
+    plans = []
+    for r in range(n):
+        to_f: list = []
+        for c in fcps[r].chunks:              # rows this rank needs in the FCP layout
+            src = user_of[c]
+            _append(to_f, (src, users[src].offset[c], fcps[r].offset[c], tokens[c]))
+        back: list = []
+        for c in users[r].chunks:             # rows this rank needs back in its user layout
+            src = owner[c]
+            _append(back, (src, fcps[src].offset[c], users[r].offset[c], tokens[c]))
+        plans.append(ReshufflePlan(r, to_f, back, users[r].tokens, fcps[r].tokens))
+    return plans
+
+
+def moved_bytes(plans: list[ReshufflePlan], bytes_per_token: int) -> tuple[list[int], list[int]]:
+    """(out_bytes, in_bytes) per rank of the to-FCP direction, excluding local copies --
+    the quantity ``simulator.reshuffle_cost`` reports."""
+    n = len(plans)
+    out, inn = [0] * n, [0] * n
+    for p in plans:
+        for peer, _, _, rows in p.to_fcp:
+            if peer != p.rank:
+                inn[p.rank] += rows * bytes_per_token
+                out[peer] += rows * bytes_per_token
+    return out, inn
+
+
+def apply_pulls(pulls, sources, dst):
+    """Reference semantics of one direction (CPU tests): dst[d:d+n] = sources[peer][s:s+n]."""
+    for peer, s, d, n in pulls:
+        dst[d:d + n] = sources[peer][s:s + n]
+    return dst
+
+
+class Reshuffler:
+    """Collective user <-> FCP layout moves for one rank (call on every rank, same order).
+
+    ``max_row_bytes`` bounds the per-token bytes of one call.  The default covers Q, K, V,
+    dO in and O, LSE, dQ, dK, dV out for ``cfg``.
+    """
+
+    def __init__(self, result: ScheduleResult, rank: int, cfg: ModelConfig, device,
+                 initial_layout=None, group=None, max_row_bytes: int | None = None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.rank = rank
+        self.world = result.assignment.n_workers
+        self.device = torch.device(device)
+        self.plans = reshuffle_plans(result, initial_layout)
+        self.plan = self.plans[rank]
+        H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
+        self.row_cap = max_row_bytes or ((2 * H + 2 * Hk) * D * 2 + 4 * H)
+        self.t_max = max(max(max(p.user_tokens, p.fcp_tokens) for p in self.plans), 1)
+        self.buf = symm.empty(self.t_max * self.row_cap, dtype=torch.uint8, device=self.device)
+        self.h = symm.rendezvous(self.buf, group or dist.group.WORLD)
+        self.peer = [self.h.get_buffer(p, (self.t_max * self.row_cap,), torch.uint8)
+                     for p in range(self.world)]
+        self.bytes_moved = 0
+
+    def _move(self, tensors, pulls, rows_in: int, rows_out: int):
+        widths, elems = [], []
+        for t in tensors:
+            if t.shape[0] != rows_in:
+                raise ParameterError(f"tensor has {t.shape[0]} rows, layout has {rows_in}")
+            row = 1
+            for x in t.shape[1:]:
+                row *= x
+            elems.append(row)
+            widths.append(row * t.element_size())
+        if sum(widths) > self.row_cap:
+            raise ParameterError(f"{sum(widths)} bytes per row exceed the reshuffler's {self.row_cap}")
+        # one contiguous region per tensor (capacity t_max rows each): publish and pulls are
+        # plain contiguous copies and the pulls land directly in the outputs (no unpack)
+        region, acc = [], 0
+        for w in widths:
+            region.append(acc)
+            acc += self.t_max * w
+        for t, w, e, off in zip(tensors, widths, elems, region):           # publish
+            self.buf[off:off + rows_in * w].view(rows_in, w).copy_(
+                t.contiguous().reshape(rows_in, e).view(torch.uint8), non_blocking=True)
+        self.h.barrier(channel=0)
+        outs = []
+        for t, w, e, off in zip(tensors, widths, elems, region):
+            o = torch.empty((rows_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device)
+            ob = o.view(rows_out, e).view(torch.uint8)
+            for peer, s0, d, n in pulls:
+                src = self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w)
+                ob[d:d + n].copy_(src, non_blocking=True)
+                if peer != self.rank:
+                    self.bytes_moved += n * w
+            outs.append(o)
+        self.h.barrier(channel=1)              # every pull done: buffers reusable
+        return outs
+
+    def to_fcp(self, *tensors):
+        """User-layout [T_user, ...] tensors -> FCP-layout [T_fcp, ...] tensors."""
+        return self._move(tensors, self.plan.to_fcp, self.plan.user_tokens, self.plan.fcp_tokens)
+
+    def from_fcp(self, *tensors):
+        """FCP-layout [T_fcp, ...] tensors -> user-layout [T_user, ...] tensors."""
+        return self._move(tensors, self.plan.from_fcp, self.plan.fcp_tokens, self.plan.user_tokens)

@@ -49,6 +49,22 @@ def main():
     for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))
     ok = all((e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2) for n, e in rep.items())
+    # transparent reshuffler (§8f): user layout -> FCP layout equals the executor's inputs
+    # exactly, and the round trip is the identity (symmetric-memory copy-engine pulls)
+    from paper_2605_08524_b200.reshuffle import Reshuffler, user_layouts
+    ul = user_layouts(r)[rank]
+    usr = [torch.cat([x[goff[c]:goff[c] + r.deps.chunk_tokens[c]] for c in ul.chunks]).to(dev)
+           if ul.chunks else x.new_zeros((0,) + tuple(x.shape[1:])).to(dev) for x in (q, k, v, do)]
+    rs = Reshuffler(r, rank, model, dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    fcp_in = rs.to_fcp(*usr)
+    t1.record()
+    back = rs.from_fcp(*fcp_in)
+    torch.cuda.synchronize()
+    reshuffle_ok = all(torch.equal(a, b) for a, b in zip(fcp_in, loc)) and \
+        all(torch.equal(a, b) for a, b in zip(back, usr))
+    ok = ok and reshuffle_ok
     # measured SimReport-shaped record (collective): one WorkerStats per rank, one record per stage
     mr = ex.measured_report(*loc, reps=2)
     ok = ok and len(mr.per_worker) == world and len(mr.stages) == len(ex.stages) \
@@ -56,6 +72,7 @@ def main():
     print(json.dumps({"rank": rank, "world": world, "recv_tokens": lay.recv_tokens,
                       "stages": len(ex.stages), "ok": ok, "errors": rep,
                       "measured_total_ms": mr.total_time * 1e3,
+                      "reshuffle_ok": reshuffle_ok, "reshuffle_to_fcp_ms": t0.elapsed_time(t1),
                       "measured_eta": [round(w.eta, 3) for w in mr.per_worker]}), flush=True)
     flag = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
