@@ -19,9 +19,10 @@ from dataclasses import dataclass, replace
 from .costmodel import EfficiencyCurve, ModelConfig, unit_costs
 from .distributor import AssignParams, Assignment, assign, effective_unit_loads
 from .errors import InfeasibleError
-from .planner import (CoalescedPlan, CommPlan, build_comm_graph, coalesce,
+from .errors import ConsistencyError, ParameterError
+from .planner import (CoalescedPlan, CommPlan, Edge, build_comm_graph, coalesce,
                       decompose_matchings, stage_ordering)
-from .sharding import DependencyMap, ScheduleUnit, ShardingConfig, kv_dependencies, shard_batch
+from .sharding import Chunk, DependencyMap, ScheduleUnit, ShardingConfig, kv_dependencies, shard_batch
 from .workload import Batch
 
 DEFAULT_COALESCE_DEGREE = 16
@@ -98,3 +99,43 @@ def plan_digest(result: ScheduleResult, cfg: ModelConfig) -> str:
                        plan_payload(result.sub_stage_plan, result.plan.degree)],
                       sort_keys=True)
     return hashlib.sha256(blob.encode()).hexdigest()[:16]
+
+
+def result_from_payloads(schedule: dict, plan: dict) -> ScheduleResult:
+    """Inverse of the wire formats (reference ``cli.py:226-258``,
+    ``load_schedule``/``load_plan``): rebuild a ScheduleResult the executor runs directly
+    from a precomputed schedule and plan, e.g. the reference CLI's ``schedule.json`` and
+    ``plan.json``.  Dependencies are rederived from the units and mask
+    (``kv_dependencies``); the coalesced stages from the stored degree."""
+    if schedule.get("format") != SCHEDULE_FORMAT:
+        raise ParameterError("not a blocksched.schedule/1 payload")
+    if plan.get("format") != PLAN_FORMAT:
+        raise ParameterError("not a blocksched.plan/1 payload")
+    n = schedule["n_workers"]
+    if plan["n_workers"] != n:
+        raise ConsistencyError(f"schedule has {n} workers, plan {plan['n_workers']}")
+    units = [ScheduleUnit(u["unit_id"], u["kind"], tuple(Chunk(*m) for m in u["members"]))
+             for u in schedule["units"]]
+    deps = kv_dependencies(units, schedule["mask"])
+    mapping: dict[int, int] = {}
+    memory, compute = [0.0] * n, [0.0] * n
+    for unit_id, worker, mem, comp in schedule["assignment"]:
+        mapping[unit_id] = worker
+        memory[worker] += mem
+        compute[worker] += comp
+    if set(mapping) != {u.unit_id for u in units}:
+        raise ConsistencyError("assignment does not cover exactly the schedule's units")
+    rounds = CommPlan(n, [[Edge(src, dst, tuple(tuple(c) for c in chunks), nbytes)
+                           for src, dst, nbytes, chunks in rnd] for rnd in plan["sub_stages"]])
+    return ScheduleResult(schedule.get("scheduler", "fcp"), units, deps,
+                          Assignment(n, mapping, memory, compute), rounds,
+                          coalesce(rounds, plan["coalesce_degree"]), None)
+
+
+def load_schedule_result(schedule_path, plan_path) -> ScheduleResult:
+    """``result_from_payloads`` on the reference CLI's artifact files."""
+    with open(schedule_path, "r", encoding="utf-8") as fh:
+        sched = json.load(fh)
+    with open(plan_path, "r", encoding="utf-8") as fh:
+        pl = json.load(fh)
+    return result_from_payloads(sched, pl)
