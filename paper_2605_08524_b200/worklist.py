@@ -66,6 +66,7 @@ class FwdWave:
     kvrefs: np.ndarray           # int32 [R, 4]: off len flags pad
     items: np.ndarray            # int32 [I, 2]: seg mblock
     pairs: int                   # visible token pairs (reference tile_token_pairs)
+    costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
 
 
 @dataclass
@@ -84,6 +85,7 @@ class BwdLaunch:
     qrefs: np.ndarray            # int32 [Q, 4]: q_off q_len diag pad
     items: np.ndarray            # int32 [I, 2]: kvseg nblock
     pairs: int
+    costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
 
 
 @dataclass
@@ -94,6 +96,7 @@ class DqPlan:
     kvrefs: np.ndarray           # int32 [R, 4]
     items: np.ndarray            # int32 [I, 2]: seg mblock (LPT order)
     pairs: int
+    costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
 
 
 @dataclass
@@ -145,13 +148,9 @@ def _kv_location(lay: RankLayout, kv: ChunkKey) -> tuple[int, int, int]:
 
 
 def _lpt_order(items):
-    """Longest-first (cost, a, b, seq) items over the persistent grid.
-
-    The kernels map grid index g -> (item g // heads, head g % heads): the heads of
-    one item run on neighbouring CTAs at the same time.  (A head-major, sequence-
-    grouped order was measured slower on B200: more dQ reduce contention, worse
-    tail balance.)
-    """
+    """Longest-first (cost, a, b, seq) items over the persistent grid.  The kernels
+    combine this item order with the heads (``grid_map``: heads-adjacent, head-major, or
+    head-major after a heads-adjacent lead; see ``BlockAttention``)."""
     import os
     if os.environ.get("FCPB_ORDER", "lpt") == "seq":     # experiment knob
         seq_cost: dict[int, int] = {}
@@ -217,7 +216,8 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
         out.append(FwdWave(
             w, np.asarray(segs, dtype=np.int32).reshape(-1, 6),
             np.asarray(refs, dtype=np.int32).reshape(-1, 4),
-            np.asarray([(s, m) for _, s, m, _ in items], dtype=np.int32).reshape(-1, 2), pairs))
+            np.asarray([(s, m) for _, s, m, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
+            np.asarray([c for c, _, _, _ in items], dtype=np.int64)))
     groups, rows, tok = [], [], 0
     for q in lay.chunks:
         if q in partial_of:
@@ -269,7 +269,8 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
         launches.append(BwdLaunch(
             recv, np.asarray(kvsegs, dtype=np.int32).reshape(-1, 6),
             np.asarray(qrefs, dtype=np.int32).reshape(-1, 4),
-            np.asarray([(k, b) for _, k, b, _ in items], dtype=np.int32).reshape(-1, 2), pairs))
+            np.asarray([(k, b) for _, k, b, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
+            np.asarray([c for c, _, _, _ in items], dtype=np.int64)))
     return launches
 
 
@@ -298,7 +299,7 @@ def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
     return DqPlan(np.asarray(segs, dtype=np.int32).reshape(-1, 6),
                   np.asarray(refs, dtype=np.int32).reshape(-1, 4),
                   np.asarray([(s_, m) for _, s_, m, _ in items], dtype=np.int32).reshape(-1, 2),
-                  pairs)
+                  pairs, np.asarray([c for c, _, _, _ in items], dtype=np.int64))
 
 
 def build_rank_work(result: ScheduleResult, rank: int, fuse_remote: bool = False) -> RankWork:
