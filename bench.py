@@ -150,8 +150,16 @@ def measured_traffic(kernel: str):
         return None
 
 
-def build_workload(name: str, n: int, block: int | None):
+def build_workload(name: str, n: int, block: int | None, scheduler: str = "fcp"):
+    """The workload and its plan: FCP (default), or the reference's competitor plans
+    (ring / ByteScale) executed by the same B200 executor."""
     w = configs.by_name(name, n, block)
+    if scheduler == "ring":
+        from paper_2605_08524_b200.baselines import ring_schedule
+        return w, ring_schedule(w.batch(), n, w.model)
+    if scheduler == "bytescale":
+        from paper_2605_08524_b200.baselines import bytescale_schedule
+        return w, bytescale_schedule(w.batch(), n, w.tokens_per_worker, w.model)
     result = fcp_schedule(w.batch(), n, ShardingConfig(block_size=w.block_size), w.model,
                           DEFAULT_EFFICIENCY)
     return w, result
@@ -286,7 +294,7 @@ def run_reference(args):
     if rank != 0:
         return
     n = args.gpus
-    w, result = build_workload(args.config, n, args.block)
+    w, result = build_workload(args.config, n, args.block, args.scheduler)
     vals = []
     info = None
     for i in range(args.warmup + args.steps):
@@ -316,6 +324,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--block", type=int, default=None)
+    ap.add_argument("--scheduler", default="fcp", choices=["fcp", "ring", "bytescale"],
+                    help="plan to execute (ring / bytescale: the reference's competitors)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -340,7 +350,7 @@ def main():
 
     peak, peak_sus, hbm, peak_kind = load_peaks()
     t_plan = time.perf_counter()
-    w, result = build_workload(args.config, n, args.block)
+    w, result = build_workload(args.config, n, args.block, args.scheduler)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
     cfg = w.model
     ex = FcpExecutor(result, rank, cfg, device)
@@ -504,7 +514,7 @@ def main():
             "config": {"workload": w.name, "global_batch_tokens": w.total_tokens,
                        "sequences": len(w.lengths), "block": w.block_size,
                        "q_heads": cfg.q_heads, "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim,
-                       "parallelism": f"fcp{n}", "l2": "inputs larger than L2 (no flush needed)",
+                       "parallelism": f"{args.scheduler}{n}", "l2": "inputs larger than L2 (no flush needed)",
                        "plan_ms_host": round(plan_ms, 2)},
             "mfu": mfu, "flop_total": flop_total,
             "roofline": {"bound": "tensor", "kernel": names[top],

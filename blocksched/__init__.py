@@ -14,6 +14,7 @@ _SUBMODULES = {
     "errors": "errors", "workload": "workload", "sharding": "sharding",
     "costmodel": "costmodel", "distributor": "distributor", "planner": "planner",
     "pipeline": "pipeline", "simulator": "simmodel", "metrics": "metrics",
+    "baselines": "baselines",
 }
 for _name, _target in _SUBMODULES.items():
     _mod = importlib.import_module(f"{_IMPL}.{_target}")

@@ -70,6 +70,8 @@ def return_partials(dkv_recv_by_rank, dkv_local_by_rank, layouts, deps, owner):
         if part is None:
             continue
         for c in lay.recv_chunks:
+            if c not in lay.consumed:       # relayed only: no partial exists
+                continue
             o = owner[c]
             a = lay.recv_offset[c]
             n = deps.chunk_tokens[c]

@@ -35,6 +35,7 @@ class Transfer:
     row: int          # first token row (local buffer for sends, receive arena for recvs)
     tokens: int
     chunk: tuple[int, int]
+    from_recv: bool = False   # a relay send (ring / ByteScale): the rows sit in the receive arena
 
 
 @dataclass
@@ -58,7 +59,10 @@ def build_stage_ops(result: ScheduleResult, lay: RankLayout, all_layouts=None) -
             for c in e.chunks:
                 n = lay.chunk_tokens[c]
                 if e.src == rank:
-                    ops.sends.append(Transfer(e.dst, lay.offset[c], n, c))
+                    if c in lay.offset:
+                        ops.sends.append(Transfer(e.dst, lay.offset[c], n, c))
+                    else:                   # relay: forwarded from the receive arena
+                        ops.sends.append(Transfer(e.dst, lay.recv_offset[c], n, c, True))
                 if e.dst == rank and lay.recv_stage.get(c) == s:
                     ops.recvs.append(Transfer(e.src, lay.recv_offset[c], n, c))
         out.append(ops)
@@ -76,45 +80,62 @@ def run_stage(stage: StageOps, send_bufs, recv_bufs, group=None):
     lists of [tokens, ...] tensors moved together (e.g. (K, V)); returns works."""
     ops = []
     for t in stage.sends:
-        for buf in send_bufs:
-            ops.append(dist.P2POp(dist.isend, buf[t.row:t.row + t.tokens], t.peer, group))
+        for buf, rbuf in zip(send_bufs, recv_bufs):
+            src = rbuf if t.from_recv else buf
+            ops.append(dist.P2POp(dist.isend, src[t.row:t.row + t.tokens], t.peer, group))
     for t in stage.recvs:
         for buf in recv_bufs:
             ops.append(dist.P2POp(dist.irecv, buf[t.row:t.row + t.tokens], t.peer, group))
     return _p2p(ops, group)
 
 
-def run_return(stages: list[StageOps], partial_bufs, staging_bufs, staging_rows, group=None):
-    """Reverse every edge of every stage in one group: receivers send their fp32
-    dK/dV partials back; owners receive them into ``staging_bufs`` at
-    ``staging_rows[(chunk, peer)]``."""
+def owner_returns(layouts, owner, rank: int) -> list[Transfer]:
+    """K6, owner side: one transfer per (my chunk, rank that consumed it), in consumer rank
+    order then that rank's receive order.  ``row`` is the chunk's row in my local buffer,
+    ``peer`` the consumer.  Owner-centric, so relay plans (where the edge sender is not
+    the owner) return every partial to the right rank."""
+    out = []
+    for q, lay in enumerate(layouts):
+        if q == rank:
+            continue
+        for c in lay.recv_chunks:
+            if c in lay.consumed and owner[c] == rank:
+                out.append(Transfer(q, layouts[rank].offset[c], lay.chunk_tokens[c], c))
+    return out
+
+
+def run_return(lay, layouts, owner, partial_bufs, staging_bufs, staging_rows, group=None):
+    """Reverse traffic of K6 over torch.distributed P2P: every rank sends the partials of
+    the chunks it consumed but does not own to their owners; owners receive them into
+    ``staging_bufs`` at ``staging_rows[(chunk, consumer)]``."""
+    rank = lay.rank
     ops = []
-    for st in stages:
-        for t in st.recvs:          # I received chunk t.chunk from t.peer: send partial back
+    for c in lay.recv_chunks:               # my partials of foreign chunks
+        if c in lay.consumed and owner[c] != rank:
+            a, n = lay.recv_offset[c], lay.chunk_tokens[c]
             for buf in partial_bufs:
-                ops.append(dist.P2POp(dist.isend, buf[t.row:t.row + t.tokens], t.peer, group))
-        for t in st.sends:          # I sent chunk to t.peer: receive its partial
-            r = staging_rows[(t.chunk, t.peer)]
-            for buf in staging_bufs:
-                ops.append(dist.P2POp(dist.irecv, buf[r:r + t.tokens], t.peer, group))
+                ops.append(dist.P2POp(dist.isend, buf[a:a + n], owner[c], group))
+    for t in owner_returns(layouts, owner, rank):
+        r = staging_rows[(t.chunk, t.peer)]
+        for buf in staging_bufs:
+            ops.append(dist.P2POp(dist.irecv, buf[r:r + t.tokens], t.peer, group))
     return _p2p(ops, group)
 
 
-def return_staging_layout(stages: list[StageOps]):
-    """Owner-side staging for returned dK/dV partials.
+def return_staging_layout(returns: list[Transfer]):
+    """Owner-side staging for returned dK/dV partials (``returns`` from ``owner_returns``).
 
     Returns (rows, rounds, total): ``rows[(chunk, peer)]`` is the first staging row of
     that peer's partial; ``rounds`` is a list of (src_rows, dst_rows) pairs where round
-    k holds the k-th receiver of every chunk, so within a round every destination row
+    k holds the k-th consumer of every chunk, so within a round every destination row
     appears once (K4 launches per round are race-free and sum in a fixed order).
     """
     rows, pos = {}, 0
     per_chunk: dict = {}
-    for st in stages:
-        for t in st.sends:
-            rows[(t.chunk, t.peer)] = pos
-            per_chunk.setdefault(t.chunk, []).append((t.row, pos, t.tokens))
-            pos += t.tokens
+    for t in returns:
+        rows[(t.chunk, t.peer)] = pos
+        per_chunk.setdefault(t.chunk, []).append((t.row, pos, t.tokens))
+        pos += t.tokens
     rounds: list[tuple[list[int], list[int]]] = []
     for parts in per_chunk.values():
         for k, (dst0, src0, n) in enumerate(parts):

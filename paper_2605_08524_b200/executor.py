@@ -56,7 +56,13 @@ class FcpExecutor:
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         self.overlap_ctas = max(1, sms - comm_sms) if (self.world > 1 and comm_sms) else 0
         self.stages = exchange.build_stage_ops(result, self.layout)
-        self.ret_rows, rounds, self.ret_tokens = exchange.return_staging_layout(self.stages)
+        from .distributor import chunk_placement
+        from .worklist import rank_layout
+        layouts = [self.layout if r == rank else rank_layout(result, r) for r in range(self.world)]
+        # K6: partials of my chunks come back from every rank that consumed them
+        self.returns = exchange.owner_returns(layouts, chunk_placement(result.assignment, result.units),
+                                              rank)
+        self.ret_rows, rounds, self.ret_tokens = exchange.return_staging_layout(self.returns)
         self.ret_rounds = [(torch.tensor(src, dtype=torch.int64, device=self.device),
                             torch.tensor(dst, dtype=torch.int32, device=self.device))
                            for src, dst in rounds]
@@ -192,7 +198,7 @@ class FcpExecutor:
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 x.barrier("part", 0)                    # every rank's partials written
-                x.pull_returns(self.stages, sk, sv, self.ret_rows)
+                x.pull_returns(self.returns, sk, sv, self.ret_rows)
                 x.barrier("part", 1)                    # pulled: partial buffers reusable
                 self._mark("comm_return_done", self.comm)
             staged = (sk, sv)
@@ -247,7 +253,7 @@ class FcpExecutor:
                         for s_idx in range(len(self.stages)):
                             x.pull_stage(s_idx, self.k_recv, self.v_recv)
                     else:
-                        x.pull_returns(self.stages, sk, sv, self.ret_rows)
+                        x.pull_returns(self.returns, sk, sv, self.ret_rows)
                     e0.record(self.comm)
                     x.barrier(which, 1)
                 torch.cuda.synchronize(self.device)

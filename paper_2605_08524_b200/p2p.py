@@ -28,6 +28,7 @@ import torch
 import torch.distributed as dist
 import torch.distributed._symmetric_memory as symm
 
+from .distributor import chunk_placement
 from .worklist import rank_layout
 
 
@@ -71,6 +72,9 @@ class SymmetricExchange:
         self.t_local = me.tokens
         self.r_local = me.recv_tokens
         # forward pulls, per coalesced stage: (peer, src_row in peer's K/V, dst_row in my arena, n)
+        # Every chunk is pulled from its owner's buffer: over NVSwitch any peer is one hop
+        # away, so a relay edge (ring / ByteScale plans) only fixes *when* it arrives.
+        owner = chunk_placement(result.assignment, result.units)
         self.stage_pulls: list[list[tuple[int, int, int, int]]] = []
         for s, stage in enumerate(result.plan.stages):
             pulls: list[tuple[int, int, int, int]] = []
@@ -79,7 +83,8 @@ class SymmetricExchange:
                     continue
                 for c in e.chunks:
                     if me.recv_stage.get(c) == s:
-                        _append_merged(pulls, (e.src, layouts[e.src].offset[c],
+                        o = owner[c]
+                        _append_merged(pulls, (o, layouts[o].offset[c],
                                                me.recv_offset[c], me.chunk_tokens[c]))
             self.stage_pulls.append(pulls)
 
@@ -135,16 +140,16 @@ class SymmetricExchange:
             return None, None
         return self.part[0, :self.r_local], self.part[1, :self.r_local]
 
-    def pull_returns(self, stages, staging_k, staging_v, staging_rows):
-        """Owner side: pull every receiver's partial of my chunks into staging rows."""
+    def pull_returns(self, returns, staging_k, staging_v, staging_rows):
+        """Owner side: pull every consumer's partial of my chunks (``exchange.owner_returns``)
+        into staging rows."""
         def pull(peer, src, r, n):
             pp = self.peer_part[peer]
             staging_k[r:r + n].copy_(pp[0, src:src + n], non_blocking=True)
             staging_v[r:r + n].copy_(pp[1, src:src + n], non_blocking=True)
         copies = []
-        for st in stages:
-            for t in st.sends:          # I sent chunk t.chunk to t.peer
-                a = (t.peer, self.layouts[t.peer].recv_offset[t.chunk],
-                     staging_rows[(t.chunk, t.peer)], t.tokens)
-                copies.append((t.peer, (lambda a=a: pull(*a))))
-        self._fanout(copies, sum(t.tokens for st in stages for t in st.sends) * 2 * self.part_row_bytes)
+        for t in returns:               # chunk t.chunk of mine, consumed by t.peer
+            a = (t.peer, self.layouts[t.peer].recv_offset[t.chunk], staging_rows[(t.chunk, t.peer)],
+                 t.tokens)
+            copies.append((t.peer, (lambda a=a: pull(*a))))
+        self._fanout(copies, sum(t.tokens for t in returns) * 2 * self.part_row_bytes)

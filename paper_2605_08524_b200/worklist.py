@@ -57,6 +57,10 @@ class RankLayout:
     recv_tokens: int
     recv_stage: dict[ChunkKey, int]
     chunk_tokens: dict[ChunkKey, int]
+    # received KV chunks some local Q chunk attends to.  FCP plans deliver only these;
+    # relay plans (ring / ByteScale) also deliver chunks a rank merely forwards, whose
+    # dK/dV partials do not exist and must not be returned.
+    consumed: frozenset = frozenset()
 
 
 @dataclass
@@ -135,7 +139,9 @@ def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
         roff[c] = rpos
         rpos += sizes[c]
     rstage = {c: arrival[(c, rank)] for c in recv}
-    return RankLayout(rank, chunks, offset, pos, recv, roff, rpos, rstage, sizes)
+    needed = {kv for q in chunks for kv in result.deps.q_to_kv[q]}
+    return RankLayout(rank, chunks, offset, pos, recv, roff, rpos, rstage, sizes,
+                      frozenset(c for c in recv if c in needed))
 
 
 def _kv_location(lay: RankLayout, kv: ChunkKey) -> tuple[int, int, int]:
@@ -244,9 +250,9 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
         for kv in kv_list:
             qs = consumers.get(kv, [])
             if not qs:
-                if not recv:
-                    continue
-                raise ConsistencyError(f"received chunk {kv} has no consumer on rank {lay.rank}")
+                # a local chunk no local Q attends to, or a chunk this rank only relays
+                # (ring / ByteScale plans): no dK/dV work here
+                continue
             kn = deps.chunk_tokens[kv]
             off = lay.recv_offset[kv] if recv else lay.offset[kv]
             begin = len(qrefs)

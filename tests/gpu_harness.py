@@ -96,11 +96,13 @@ def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True, fu
                            dka, dva, dkr, dvr)
         dqa = op.backward_dq(t["q"], t["k"], t["v"], t["kr"], t["vr"], prep, t["do"])
         acc.append((dqa, dka, dva, dkr, dvr))
-    # dKV return along reversed edges + K4 reduce at the owner
+    # dKV return to the owner from every consuming rank + K4 reduce at the owner
     for w, work in enumerate(works):
         lay = work.layout
         dkr, dvr = acc[w][3], acc[w][4]
         for c in lay.recv_chunks:
+            if c not in lay.consumed:       # relayed only (ring / ByteScale plans)
+                continue
             o_rank = owner[c]
             m = deps.chunk_tokens[c]
             a = lay.recv_offset[c]

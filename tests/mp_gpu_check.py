@@ -31,7 +31,14 @@ def main():
     lengths = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3523,2702,2219,1292,1438,413,544,319").split(",")]
     block = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     model = ModelConfig(q_heads=8, kv_heads=2, head_dim=128)
-    r = schedule(lengths, world, block, model)
+    sched = os.environ.get("FCPB_CHECK_SCHED", "fcp")
+    if sched == "fcp":
+        r = schedule(lengths, world, block, model)
+    else:                            # the reference's ring plan (relays) on the same executor
+        from paper_2605_08524_b200.baselines import ring_schedule
+        from paper_2605_08524_b200.workload import Batch, Sequence
+        r = ring_schedule(Batch(tuple(Sequence(i, l) for i, l in enumerate(lengths)), world,
+                                -(-sum(lengths) // world)), world, model)
     goff, T = global_offsets(r)
     q, k, v, do = make_inputs(T, model)
     ex = FcpExecutor(r, rank, model, dev)

@@ -21,15 +21,19 @@ from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, ModelConfig
 from paper_2605_08524_b200.pipeline import fcp_schedule, plan_digest
 from paper_2605_08524_b200.sharding import ShardingConfig
 from paper_2605_08524_b200.workload import Batch, Sequence
+from paper_2605_08524_b200.distributor import chunk_placement
 from paper_2605_08524_b200.worklist import rank_layout
 
 MODEL = ModelConfig(q_heads=4, kv_heads=2, head_dim=8)
 LENGTHS = [3000, 1700, 900, 400, 130, 77, 5]
 
 
-def _schedule(n):
+def _schedule(n, sched="fcp"):
     tpw = -(-sum(LENGTHS) // n)
     batch = Batch(tuple(Sequence(i, l) for i, l in enumerate(LENGTHS)), n, tpw)
+    if sched == "ring":
+        from paper_2605_08524_b200.baselines import ring_schedule
+        return ring_schedule(batch, n, MODEL)
     return fcp_schedule(batch, n, ShardingConfig(256), MODEL, DEFAULT_EFFICIENCY, coalesce_degree=4)
 
 
@@ -39,11 +43,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, errq):
+def _worker(rank, world, port, errq, sched="fcp"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        r = _schedule(world)
+        r = _schedule(world, sched)
         exchange.sync_plan_digest(plan_digest(r, MODEL))
         lay = rank_layout(r, rank)
         goff, T = global_offsets(r)
@@ -59,16 +63,18 @@ def _worker(rank, world, port, errq):
             exchange.wait_all(exchange.run_stage(st, (k, v), (kr, vr)))
         assert torch.equal(kr, gather_rank(kg, lay, goff, r.deps, recv=True))
         assert torch.equal(vr, gather_rank(vg, lay, goff, r.deps, recv=True))
-        # reverse: each receiver returns (its rank + chunk data) as the "partial"
+        # reverse: each consumer returns (its rank + chunk data) as the "partial", to the owner
         part = kr + 1000.0 * (rank + 1)
-        rows, rounds, n_stage = exchange.return_staging_layout(stages)
+        layouts = [rank_layout(r, q) for q in range(world)]
+        owner = chunk_placement(r.assignment, r.units)
+        returns = exchange.owner_returns(layouts, owner, rank)
+        rows, rounds, n_stage = exchange.return_staging_layout(returns)
         staged = torch.zeros((n_stage, MODEL.kv_heads, MODEL.head_dim))
-        exchange.wait_all(exchange.run_return(stages, (part,), (staged,), rows))
-        for st in stages:
-            for t in st.sends:
-                got = staged[rows[(t.chunk, t.peer)]:rows[(t.chunk, t.peer)] + t.tokens]
-                want = k[t.row:t.row + t.tokens] + 1000.0 * (t.peer + 1)
-                assert torch.equal(got, want), (rank, t)
+        exchange.wait_all(exchange.run_return(lay, layouts, owner, (part,), (staged,), rows))
+        for t in returns:
+            got = staged[rows[(t.chunk, t.peer)]:rows[(t.chunk, t.peer)] + t.tokens]
+            want = k[t.row:t.row + t.tokens] + 1000.0 * (t.peer + 1)
+            assert torch.equal(got, want), (rank, t)
         # rounds: every staged row used once; destinations unique within a round
         srcs = sorted(x for src, _ in rounds for x in src)
         assert srcs == list(range(n_stage))
@@ -82,14 +88,14 @@ def _worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_plan_exchange_over_gloo(world):
-    r = _schedule(world)
+@pytest.mark.parametrize("world,sched", [(2, "fcp"), (3, "fcp"), (3, "ring")])
+def test_plan_exchange_over_gloo(world, sched):
+    r = _schedule(world, sched)
     assert sum(len(s) for s in r.plan.stages) > 0
     ctx = mp.get_context("spawn")
     errq = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(i, world, port, errq)) for i in range(world)]
+    procs = [ctx.Process(target=_worker, args=(i, world, port, errq, sched)) for i in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -25,9 +25,15 @@ from paper_2605_08524_b200.worklist import build_rank_work
 MODEL = ModelConfig(q_heads=4, kv_heads=2, head_dim=32, dtype_bytes=2)
 
 
-def _schedule(lengths, n, block, mask="causal", coalesce=16):
+def _schedule(lengths, n, block, mask="causal", coalesce=16, scheduler="fcp"):
     tpw = -(-sum(lengths) // n)
     batch = Batch(tuple(Sequence(i, l) for i, l in enumerate(lengths)), n, tpw)
+    if scheduler == "ring":
+        from paper_2605_08524_b200.baselines import ring_schedule
+        return ring_schedule(batch, n, MODEL, mask)
+    if scheduler == "bytescale":
+        from paper_2605_08524_b200.baselines import bytescale_schedule
+        return bytescale_schedule(batch, n, tpw, MODEL, mask)
     return fcp_schedule(batch, n, ShardingConfig(block, mask), MODEL, DEFAULT_EFFICIENCY,
                         coalesce_degree=coalesce)
 
@@ -92,16 +98,19 @@ def test_tiled_equals_dense(mask):
 
 
 @pytest.mark.parametrize("fuse", [False, True])
-@pytest.mark.parametrize("n,lengths,block,coalesce", [
-    (1, [700, 260, 130, 100, 50, 9], 256, 16),
-    (2, [700, 260, 130, 100, 50, 9], 256, 16),
-    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 16),
-    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 1),     # many stages: fusion matters
+@pytest.mark.parametrize("n,lengths,block,coalesce,sched", [
+    (1, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
+    (2, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
+    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 16, "fcp"),
+    (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 1, "fcp"),     # many stages: fusion matters
+    (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "ring"),     # relays, unconsumed chunks
+    (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "bytescale"),
 ])
-def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, fuse):
+def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fuse):
     """Simulated workers: per-rank work lists + in-process exchange == dense attention,
-    with one forward wave per arrival stage or all remote KV fused into one wave."""
-    r = _schedule(lengths, n, block, coalesce=coalesce)
+    with one forward wave per arrival stage or all remote KV fused into one wave, for FCP
+    plans and for the ring / ByteScale plans (relay edges) of baselines.py."""
+    r = _schedule(lengths, n, block, coalesce=coalesce, scheduler=sched)
     works = [build_rank_work(r, w, fuse_remote=fuse) for w in range(n)]
     if fuse:
         assert all(sum(1 for wv in wk.fwd.waves if wv.stage >= 0) <= 1 for wk in works)

@@ -1,6 +1,6 @@
 """Run the reference's own hot-path tests, unchanged, against the drop-in.
 
-``pkg/tests/test_{sharding,costmodel,distributor,planner,pipeline,simulator}.py``
+``pkg/tests/test_{sharding,costmodel,distributor,planner,pipeline,simulator,baselines}.py``
 import ``blocksched``; with the repo root first on ``PYTHONPATH`` that name is
 the alias package ``blocksched/`` over ``paper_2605_08524_b200``.  Skipped
 where the reference checkout is absent (the GPU box).
@@ -16,7 +16,8 @@ import pytest
 REF_TESTS = "/root/reference/pkg/tests"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HOT_PATH = ["test_sharding.py", "test_costmodel.py", "test_distributor.py",
-            "test_planner.py", "test_pipeline.py", "test_simulator.py"]
+            "test_planner.py", "test_pipeline.py", "test_simulator.py",
+            "test_baselines.py"]                        # §8f-2: competitor plans
 
 
 @pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference checkout absent")
