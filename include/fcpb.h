@@ -158,6 +158,9 @@ typedef struct {
   void* dk_out; void* dv_out;   /* optional bf16 [Tkv, Hkv, D]: local segments write the final
                                    (scaled) dK/dV here instead of dk/dv_accum -- only when no
                                    partials of this rank's chunks come back from peers      */
+  void* ds_out;                 /* optional bf16 dS^T tiles [pairs * Hq][128 q / 8][128 kv][8 q] for
+                                   fcpb_attn_bwd_dq_ds (materialised-dS backward)         */
+  const int32_t* pair_base;     /* with ds_out: per item, its first (kv block, q block) pair */
   const FcpbBwdKvSeg* kvsegs; int32_t num_kvsegs;
   const FcpbBwdQRef* qrefs; int32_t num_qrefs;
   const FcpbBwdItem* items; int32_t num_items;
@@ -168,6 +171,28 @@ typedef struct {
 } FcpbBwdArgs;
 
 FCPB_API int fcpb_attn_bwd(const FcpbBwdArgs* args, void* stream);
+
+/* K2c: dQ from materialised dS tiles (written by fcpb_attn_bwd with ds_out): a grouped
+ * GEMM dQ = scale * sum dS K over each item's KV tiles.  Tables as FcpbDqArgs, plus the
+ * dS pair id of every (item, KV tile) (worklist.build_ds_tiles). */
+typedef struct {
+  int32_t num_q_heads, num_kv_heads, head_dim;
+  float softmax_scale;
+  const void* ds; int64_t ds_tiles;              /* bf16 [ds_tiles][16][128][8] (see ds_out) */
+  const void* k; int64_t kv_tokens;
+  const void* k_recv; int64_t kv_recv_tokens;
+  void* dq;                                      /* bf16 [Tq, Hq, D] output                */
+  const FcpbSegment* segments; int32_t num_segments;
+  const FcpbKvRef* kv_refs;    int32_t num_kv_refs;
+  const FcpbItem* items;       int32_t num_items;
+  const int32_t* pair_ids; const int32_t* pair_off;
+  int32_t num_ctas;
+  int32_t head_major;
+  int32_t hm_lead;
+  int32_t* sched_counter;
+} FcpbDqDsArgs;
+
+FCPB_API int fcpb_attn_bwd_dq_ds(const FcpbDqDsArgs* args, void* stream);
 
 /* fp32 -> bf16 conversion of an accumulator (dQ, dK, dV). */
 FCPB_API int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream);

@@ -71,7 +71,21 @@ class BlockAttention:
         d = work.dq
         self._dq = (d, _dev_i32(d.segments, dev), _dev_i32(d.kvrefs, dev), _dev_i32(d.items, dev))
         self.launches = 0   # kernel launches issued by this object (bench accounting)
-        self.sm_count = num_ctas or torch.cuda.get_device_properties(self.device).multi_processor_count
+        props = torch.cuda.get_device_properties(self.device)
+        self.sm_count = num_ctas or props.multi_processor_count
+        # Materialised-dS backward: the dK/dV kernel writes every bf16 dS^T tile and dQ is a
+        # grouped GEMM over them (attn_dqg_sm100.cuh) instead of recomputing S, dP and the
+        # softmax.  Used when the tiles fit the budget (FCPB_DS=0/1 forces, FCPB_DS_BUDGET_GB).
+        import os as _os
+        ds_bytes = work.ds_pairs * cfg.q_heads * 128 * 128 * 2
+        budget = float(_os.environ.get("FCPB_DS_BUDGET_GB", min(40.0, props.total_memory / 4 / 1e9))) * 1e9
+        force = _os.environ.get("FCPB_DS")
+        self.ds_mode = (force == "1") if force is not None else (0 < ds_bytes <= budget)
+        self._ds = None
+        if self.ds_mode:
+            self._ds_pairs_base = [_dev_i32(b.pair_base, dev) for b in work.bwd]
+            self._dq_pairs = (_dev_i32(work.dq.pair_ids, dev), _dev_i32(work.dq.pair_off, dev))
+            self._ds_tiles = work.ds_pairs * cfg.q_heads
         import os
         # Work order of the dynamic scheduler.  Head-major (all items of one head, LPT order,
         # before the next head) keeps one head's Q/dO (or K/V) stream resident in L2: on C2
@@ -199,10 +213,35 @@ class BlockAttention:
         self.launches += 1
         return lse2_t, delta_t, t_pad
 
+    def _ds_buffer(self):
+        if self._ds is None:            # persistent across steps (one step's dS tiles)
+            self._ds = torch.empty((self._ds_tiles, 128, 128), dtype=torch.bfloat16, device=self.device)
+        return self._ds
+
     def backward_dq(self, q, k, v, k_recv, v_recv, prep, do, stream=None):
-        """K2b: query-stationary dQ over every KV chunk of each local Q chunk -> bf16."""
+        """dQ of every local Q chunk -> bf16: a grouped GEMM over the dS tiles the dK/dV
+        launches wrote (K2c, ds_mode), else the query-stationary recompute kernel (K2b)."""
         d, segs, refs, items = self._dq
         dq = torch.empty(self.q_shape(), dtype=torch.bfloat16, device=self.device)
+        if self.ds_mode:
+            a = native.DqDsArgs()
+            a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
+            a.softmax_scale = self.scale
+            a.ds, a.ds_tiles = native.ptr(self._ds_buffer()), self._ds_tiles
+            a.k, a.kv_tokens = native.ptr(k), self.tokens
+            a.k_recv, a.kv_recv_tokens = native.ptr(k_recv), self.recv_tokens
+            a.dq = native.ptr(dq)
+            a.segments, a.num_segments = native.ptr(segs), len(d.segments)
+            a.kv_refs, a.num_kv_refs = native.ptr(refs), len(d.kvrefs)
+            a.items, a.num_items = native.ptr(items), len(d.items)
+            a.pair_ids, a.pair_off = native.ptr(self._dq_pairs[0]), native.ptr(self._dq_pairs[1])
+            a.num_ctas = self.num_ctas
+            a.head_major = self.head_major["dq"]
+            a.hm_lead = self._hm_lead(d.costs)
+            a.sched_counter = self._sched.data_ptr() + 8
+            native.check(self.lib.fcpb_attn_bwd_dq_ds(ctypes_ref(a), self._stream(stream)))
+            self.launches += 1
+            return dq
         a = native.DqArgs()
         a.num_q_heads, a.num_kv_heads, a.head_dim = self.cfg.q_heads, self.cfg.kv_heads, self.cfg.head_dim
         a.softmax_scale = self.scale
@@ -236,7 +275,7 @@ class BlockAttention:
         """K2 over the received (recv=True) or local chunks.  dk_out/dv_out (bf16): local
         chunks write their final dK/dV there directly -- only when no partials of this
         rank's chunks come back from peers."""
-        for b, kvsegs, qrefs, items in self._bwd:
+        for bi, (b, kvsegs, qrefs, items) in enumerate(self._bwd):
             if b.recv != recv:
                 continue
             a = native.BwdArgs()
@@ -251,6 +290,9 @@ class BlockAttention:
             a.dq_accum, a.dk_accum, a.dv_accum = None, native.ptr(dk), native.ptr(dv)
             a.dk_recv_accum, a.dv_recv_accum = native.ptr(dk_r), native.ptr(dv_r)
             a.dk_out, a.dv_out = native.ptr(dk_out), native.ptr(dv_out)
+            if self.ds_mode:
+                a.ds_out = native.ptr(self._ds_buffer())
+                a.pair_base = native.ptr(self._ds_pairs_base[bi])
             a.kvsegs, a.num_kvsegs = native.ptr(kvsegs), len(b.kvsegs)
             a.qrefs, a.num_qrefs = native.ptr(qrefs), len(b.qrefs)
             a.items, a.num_items = native.ptr(items), len(b.items)

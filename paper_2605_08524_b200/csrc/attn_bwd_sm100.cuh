@@ -111,6 +111,8 @@ struct Params {
   float* dv_recv;
   __nv_bfloat16* dk_out;  // optional final bf16 [Tkv, Hkv, D] for local segments
   __nv_bfloat16* dv_out;
+  __nv_bfloat16* ds_out;  // optional dS^T tiles [pairs * Hq][128 q / 8][128 kv][8 q] for the dQ GEMM
+  const int32_t* pair_base;  // per item: first (kv block, q block) pair id (worklist.build_ds_tiles)
 };
 
 // Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
@@ -191,8 +193,10 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p,
   tmem_st16(t_p, pk);
 }
 
-// Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds.
-FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, uint32_t t_ds) {
+// Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds, and (when gdst is
+// set) the same 64 bytes into the materialised dS^T tile for the dQ GEMM.
+FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, uint32_t t_ds,
+                       uint4* gdst) {
   uint32_t dk[16];
 #pragma unroll
   for (int c8 = 0; c8 < 4; ++c8) {
@@ -209,6 +213,11 @@ FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, ui
     }
   }
   tmem_st16(t_ds, dk);
+  if (gdst) {     // tile layout [q/8][kv][8 q]: chunk i of this thread at gdst[i * 128]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      gdst[i * kBK] = make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -440,9 +449,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       const int kv_row = it.nblock * kBK + tid;
       const bool kv_live = kv_row < ks.kv_len;
       const bool kv_full_tile = it.nblock * kBK + kBK <= ks.kv_len;
+      int pair = p.ds_out ? p.pair_base[item_of(g, p)] : 0;   // dS tiles: pair * Hq + q head
       for (int r = ks.q_begin; r < ks.q_end; ++r) {
         const QRef qr = p.qrefs[r];
-        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
+        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb, ++pair) {
           const int q_valid = qr.q_len - mb * kBQ;
           // diagonal: column c (q = 128 mb + c) sees kv row 128 nb + tid iff c >= shift
           const int shift0 = it.nblock * kBK - mb * kBQ;
@@ -450,6 +460,13 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           const int shift = qr.diag ? shift0 + tid : -(1 << 30);
           for (int gq = 0; gq < group; ++gq, ++tile) {
             float pr[kCols];
+            uint4* gdst = nullptr;
+            if (p.ds_out) {
+              const size_t tid_tile = static_cast<size_t>(pair) * p.num_q_heads + kvh * group + gq;
+              // [q/8][kv][8 q]: a warp's 32 kv rows store 512 contiguous bytes per chunk,
+              // and the tile is the no-swizzle MN-major canonical layout of the dQ GEMM's A
+              gdst = reinterpret_cast<uint4*>(p.ds_out + tid_tile * (kBK * kBQ)) + (wg * 4) * kBK + tid;
+            }
             mbar_wait(&sm.s_full, s_phase);
             s_phase ^= 1;
             FCPB_TR(kTrSGot, (int)tile);
@@ -482,7 +499,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               uint32_t dv[32];
               tmem_ld32(t_dp, dv);
               tmem_wait_ld();
-              ds_chunk(dv, dl, pr, t_dp);
+              ds_chunk(dv, dl, pr, t_dp, gdst);
             }
             tmem_wait_st();
             tc_fence_before();

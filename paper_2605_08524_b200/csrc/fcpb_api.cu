@@ -9,6 +9,7 @@
 #include "../../include/fcpb.h"
 #include "attn_bwd_sm100.cuh"
 #include "attn_dq_sm100.cuh"
+#include "attn_dqg_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
 #include "aux_kernels.cuh"
 
@@ -82,6 +83,8 @@ int sm_count() {
 constexpr size_t kFwdSmem = sizeof(fcpb::fwd::Smem) + 1024;
 constexpr size_t kBwdSmem = sizeof(fcpb::bwd::Smem) + 1024;
 constexpr size_t kDqSmem = sizeof(fcpb::dq::Smem) + 1024;
+constexpr size_t kDqgSmem = sizeof(fcpb::dqg::Smem) + 1024;
+static_assert(kDqgSmem <= 232448, "dqg smem budget");
 static_assert(kDqSmem <= 232448, "dq smem budget");
 static_assert(kFwdSmem <= 232448, "fwd smem budget");
 static_assert(kBwdSmem <= 232448, "bwd smem budget");
@@ -197,6 +200,9 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.dv_recv = a->dv_recv_accum;
   p.dk_out = static_cast<__nv_bfloat16*>(a->dk_out);
   p.dv_out = static_cast<__nv_bfloat16*>(a->dv_out);
+  p.ds_out = static_cast<__nv_bfloat16*>(a->ds_out);
+  p.pair_base = a->pair_base;
+  if (p.ds_out && !p.pair_base) return fail(FCPB_ERR_INVALID, "ds_out needs pair_base");
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
@@ -266,6 +272,54 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   if (grid > total) grid = total;
   fcpb::dq::attn_dq_kernel<<<grid, fcpb::dq::kThreads, kDqSmem, static_cast<cudaStream_t>(stream)>>>(
       tk, tv, tkr, tvr, p);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int fcpb_attn_bwd_dq_ds(const FcpbDqDsArgs* a, void* stream) {
+  if (!a) return fail(FCPB_ERR_INVALID, "null args");
+  if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d (need 128)", a->head_dim);
+  if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
+    return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
+  if (a->num_items <= 0) return FCPB_OK;
+  if (!a->ds || a->ds_tiles <= 0 || !a->pair_ids || !a->pair_off)
+    return fail(FCPB_ERR_INVALID, "dS tiles / pair tables missing");
+  const int H = a->num_q_heads, Hk = a->num_kv_heads;
+  CUtensorMap tk, tkr;
+  int rc;
+  if ((rc = make_map(&tk, a->k, a->kv_tokens, Hk, 128, fcpb::dqg::kBN))) return rc;
+  const bool has_recv = a->k_recv && a->kv_recv_tokens > 0;
+  if ((rc = make_map(&tkr, has_recv ? a->k_recv : a->k, has_recv ? a->kv_recv_tokens : a->kv_tokens,
+                     Hk, 128, fcpb::dqg::kBN)))
+    return rc;
+  fcpb::dqg::Params p;
+  p.segs = a->segments;
+  p.kvrefs = a->kv_refs;
+  p.items = a->items;
+  p.ds = static_cast<const __nv_bfloat16*>(a->ds);
+  p.pair_ids = a->pair_ids;
+  p.pair_off = a->pair_off;
+  p.num_items = a->num_items;
+  p.num_q_heads = H;
+  p.num_kv_heads = Hk;
+  p.head_major = a->head_major;
+  p.hm_lead = a->hm_lead;
+  p.scale = a->softmax_scale;
+  p.dq = static_cast<__nv_bfloat16*>(a->dq);
+  if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
+  p.sched_counter = a->sched_counter;
+  FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
+  static bool attr = false;
+  if (!attr) {
+    FCPB_CUDA(cudaFuncSetAttribute(fcpb::dqg::attn_dqg_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqgSmem));
+    attr = true;
+  }
+  const int total = a->num_items * H;
+  int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
+  if (grid > total) grid = total;
+  fcpb::dqg::attn_dqg_kernel<<<grid, fcpb::dqg::kThreads, kDqgSmem, static_cast<cudaStream_t>(stream)>>>(
+      tk, tkr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }

@@ -221,6 +221,26 @@ FCPB_DEV uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t s
   return d;
 }
 
+// Same descriptor for the no-swizzle ("interleave") canonical layout: 8x16-byte core
+// matrices.  For an MN-major operand stored [MN/8][K][8] (16-byte rows of 8 MN elements,
+// consecutive K rows 16 B apart): LBO = stride between K groups of 8 rows, SBO = stride
+// between MN groups of 8 elements.
+FCPB_DEV uint64_t smem_desc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;                                        // layout type 0: no swizzle
+}
+
+// 1-D bulk copy global -> shared, completion on an mbarrier (transaction bytes).
+FCPB_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> f32.
 //   bits 4-5 c fmt (1=f32), 7-9 a fmt (1=bf16), 10-12 b fmt (1=bf16),
 //   bit 15 a major (0=K,1=MN), bit 16 b major, bits 17-22 N>>3, bits 24-28 M>>4

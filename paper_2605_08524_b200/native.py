@@ -49,6 +49,7 @@ class BwdArgs(ctypes.Structure):
                 ("k_recv", c_vp), ("v_recv", c_vp), ("kv_recv_tokens", c_i64),
                 ("dq_accum", c_vp), ("dk_accum", c_vp), ("dv_accum", c_vp),
                 ("dk_recv_accum", c_vp), ("dv_recv_accum", c_vp), ("dk_out", c_vp), ("dv_out", c_vp),
+                ("ds_out", c_vp), ("pair_base", c_vp),
                 ("kvsegs", c_vp), ("num_kvsegs", c_i32),
                 ("qrefs", c_vp), ("num_qrefs", c_i32),
                 ("items", c_vp), ("num_items", c_i32),
@@ -69,7 +70,22 @@ class DqArgs(ctypes.Structure):
                 ("num_ctas", c_i32), ("head_major", c_i32), ("hm_lead", c_i32), ("sched_counter", c_vp)]
 
 
-EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_lse_merge", "fcpb_bwd_preprocess",
+class DqDsArgs(ctypes.Structure):
+    _fields_ = [("num_q_heads", c_i32), ("num_kv_heads", c_i32), ("head_dim", c_i32),
+                ("softmax_scale", c_f32),
+                ("ds", c_vp), ("ds_tiles", c_i64),
+                ("k", c_vp), ("kv_tokens", c_i64),
+                ("k_recv", c_vp), ("kv_recv_tokens", c_i64),
+                ("dq", c_vp),
+                ("segments", c_vp), ("num_segments", c_i32),
+                ("kv_refs", c_vp), ("num_kv_refs", c_i32),
+                ("items", c_vp), ("num_items", c_i32),
+                ("pair_ids", c_vp), ("pair_off", c_vp),
+                ("num_ctas", c_i32), ("head_major", c_i32), ("hm_lead", c_i32), ("sched_counter", c_vp)]
+
+
+EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_dq_ds",
+           "fcpb_lse_merge", "fcpb_bwd_preprocess",
            "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_last_error", "fcpb_version",
            "fcpb_device_supported")
 
@@ -88,6 +104,7 @@ def load(path: str | None = None):
     lib.fcpb_attn_fwd.argtypes = [ctypes.POINTER(FwdArgs), c_vp]
     lib.fcpb_attn_bwd.argtypes = [ctypes.POINTER(BwdArgs), c_vp]
     lib.fcpb_attn_bwd_dq.argtypes = [ctypes.POINTER(DqArgs), c_vp]
+    lib.fcpb_attn_bwd_dq_ds.argtypes = [ctypes.POINTER(DqDsArgs), c_vp]
     lib.fcpb_lse_merge.argtypes = [ctypes.POINTER(MergeArgs), c_vp]
     lib.fcpb_bwd_preprocess.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32,
                                          c_i32, c_vp]

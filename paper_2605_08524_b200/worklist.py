@@ -90,6 +90,9 @@ class BwdLaunch:
     items: np.ndarray            # int32 [I, 2]: kvseg nblock
     pairs: int
     costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
+    kv_keys: list | None = None       # chunk key of every kvseg
+    q_keys: list | None = None        # chunk key of every qref
+    pair_base: np.ndarray | None = None   # int32 [I]: first dS pair id of the item (build_ds_tiles)
 
 
 @dataclass
@@ -101,6 +104,10 @@ class DqPlan:
     items: np.ndarray            # int32 [I, 2]: seg mblock (LPT order)
     pairs: int
     costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
+    q_keys: list | None = None        # chunk key of every segment
+    kv_keys: list | None = None       # chunk key of every kvref
+    pair_ids: np.ndarray | None = None    # int32: dS pair id of every (item, kv tile), item-major
+    pair_off: np.ndarray | None = None    # int32 [I]: first entry of each item in pair_ids
 
 
 @dataclass
@@ -110,6 +117,7 @@ class RankWork:
     bwd: list[BwdLaunch] = field(default_factory=list)
     pairs: int = 0
     dq: DqPlan | None = None
+    ds_pairs: int = 0                 # (kv block, q block) pairs with a materialised dS tile
 
 
 def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
@@ -247,6 +255,7 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
     for recv in (True, False):
         kv_list = lay.recv_chunks if recv else lay.chunks
         kvsegs, qrefs, items, pairs = [], [], [], 0
+        kv_keys, q_keys = [], []
         for kv in kv_list:
             qs = consumers.get(kv, [])
             if not qs:
@@ -260,9 +269,11 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
                 assert q in local
                 diag = int(causal and q == kv)
                 qrefs.append((lay.offset[q], deps.chunk_tokens[q], diag, 0))
+                q_keys.append(q)
                 pairs += tile_token_pairs(deps.chunk_tokens[q], kn, bool(diag))
             kidx = len(kvsegs)
             kvsegs.append((off, kn, KV_RECV if recv else 0, begin, len(qrefs), 0))
+            kv_keys.append(kv)
             for nb in range(_cdiv(kn, TILE)):
                 cost = 0
                 for q in qs:
@@ -276,7 +287,7 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
             recv, np.asarray(kvsegs, dtype=np.int32).reshape(-1, 6),
             np.asarray(qrefs, dtype=np.int32).reshape(-1, 4),
             np.asarray([(k, b) for _, k, b, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
-            np.asarray([c for c, _, _, _ in items], dtype=np.int64)))
+            np.asarray([c for c, _, _, _ in items], dtype=np.int64), kv_keys, q_keys))
     return launches
 
 
@@ -284,10 +295,13 @@ def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
     deps = result.deps
     causal = deps.mask == CAUSAL
     segs, refs, items, pairs = [], [], [], 0
+    q_keys, kv_keys = [], []
     for q in lay.chunks:
         qn = deps.chunk_tokens[q]
         begin = len(refs)
+        q_keys.append(q)
         for kv in deps.q_to_kv[q]:
+            kv_keys.append(kv)
             _, off, flags = _kv_location(lay, kv)
             if causal and kv == q:
                 flags |= KV_DIAG
@@ -305,11 +319,52 @@ def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
     return DqPlan(np.asarray(segs, dtype=np.int32).reshape(-1, 6),
                   np.asarray(refs, dtype=np.int32).reshape(-1, 4),
                   np.asarray([(s_, m) for _, s_, m, _ in items], dtype=np.int32).reshape(-1, 2),
-                  pairs, np.asarray([c for c, _, _, _ in items], dtype=np.int64))
+                  pairs, np.asarray([c for c, _, _, _ in items], dtype=np.int64), q_keys, kv_keys)
+
+
+def build_ds_tiles(bwd: list[BwdLaunch], dq: DqPlan, causal: bool) -> int:
+    """Materialised-dS backward: number the (KV block, Q block) pairs in the order the
+    dK/dV kernel visits them (launch, item in LPT order, qref, q block) -> pair ids.
+    Every dK/dV item gets the first id of its pairs (``pair_base``); every dQ item the id
+    of each KV tile it visits (``pair_ids``/``pair_off``), so the dQ kernel reads exactly
+    the dS tiles the dK/dV kernel wrote: tile = pair * Hq + q head.  Returns the pair
+    count."""
+    ids: dict = {}
+    nxt = 0
+    for b in bwd:
+        base = []
+        for k, nb in b.items.tolist():
+            base.append(nxt)
+            kv = b.kv_keys[k]
+            seg = b.kvsegs[k]
+            for r in range(seg[3], seg[4]):
+                q_off, q_len, diag, _ = b.qrefs[r].tolist()
+                first = nb if diag else 0
+                for mb in range(first, _cdiv(q_len, TILE)):
+                    ids[(kv, nb, b.q_keys[r], mb)] = nxt
+                    nxt += 1
+        b.pair_base = np.asarray(base, dtype=np.int32)
+    flat, off = [], []
+    for s_idx, mb in dq.items.tolist():
+        off.append(len(flat))
+        seg = dq.segments[s_idx]
+        q = dq.q_keys[s_idx]
+        for r in range(seg[2], seg[3]):
+            kv_off, kv_len, flags, _ = dq.kvrefs[r].tolist()
+            nt = _cdiv(kv_len, TILE)
+            if flags & KV_DIAG:
+                nt = min(nt, mb + 1)
+            for t in range(nt):
+                flat.append(ids[(dq.kv_keys[r], t, q, mb)])
+    dq.pair_ids = np.asarray(flat, dtype=np.int32)
+    dq.pair_off = np.asarray(off, dtype=np.int32)
+    return nxt
 
 
 def build_rank_work(result: ScheduleResult, rank: int, fuse_remote: bool = False) -> RankWork:
     lay = rank_layout(result, rank)
     fwd = build_forward(result, lay, fuse_remote)
     bwd = build_backward(result, lay)
-    return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves), build_dq(result, lay))
+    dq = build_dq(result, lay)
+    n_pairs = build_ds_tiles(bwd, dq, result.deps.mask == CAUSAL)
+    return RankWork(lay, fwd, bwd, sum(w.pairs for w in fwd.waves), dq, n_pairs)

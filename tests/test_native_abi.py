@@ -45,7 +45,8 @@ def test_struct_layouts_match_header(tmp_path):
     if cc is None:
         pytest.skip("no C compiler")
     fields = {"FcpbFwdArgs": native.FwdArgs, "FcpbMergeArgs": native.MergeArgs,
-              "FcpbBwdArgs": native.BwdArgs}
+              "FcpbBwdArgs": native.BwdArgs, "FcpbDqArgs": native.DqArgs,
+              "FcpbDqDsArgs": native.DqDsArgs}
     lines = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
     for cname, py in fields.items():
         lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
