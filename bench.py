@@ -500,12 +500,17 @@ def main():
         # algorithmic FLOPs per kernel (reference costmodel: fwd 4*Hq*D per pair; the
         # backward's 2.5x splits 4 GEMMs dK/dV + 3 GEMMs dQ of the 7 the split executes,
         # so each kernel is credited its share of the 2.5x: dK/dV 2.5*4/7, dQ 2.5*3/7)
-        kfl = {"fwd": fwd_f, "bwd": bwd_f * 4 / 7, "dq": bwd_f * 3 / 7}
+        # recompute dQ executes 4 + 3 GEMM-equivalents for the backward's algorithmic 5;
+        # with materialised dS (K2c) the two kernels execute exactly 4 + 1
+        ds_mode = ex.op.ds_mode
+        kfl = ({"fwd": fwd_f, "bwd": bwd_f * 4 / 5, "dq": bwd_f * 1 / 5} if ds_mode else
+               {"fwd": fwd_f, "bwd": bwd_f * 4 / 7, "dq": bwd_f * 3 / 7})
         ktf = {key: (kfl[key] / (kms[key] / 1e3) / 1e12 if kms[key] > 0 else 0.0) for key in kms}
         bwd_ms = kms["bwd"] + kms["dq"]
         bwd_tflops = bwd_f / (bwd_ms / 1e3) / 1e12 if bwd_ms > 0 else 0.0
         top = max(kms, key=lambda kk: kms[kk])
-        names = {"fwd": "attn_fwd_kernel", "bwd": "attn_bwd_kernel", "dq": "attn_dq_kernel"}
+        names = {"fwd": "attn_fwd_kernel", "bwd": "attn_bwd_kernel",
+                 "dq": "attn_dqg_kernel" if ds_mode else "attn_dq_kernel"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -522,7 +527,9 @@ def main():
                          "frac": ktf[top] * 1e12 / peak, "peak_kind": peak_kind + " burst",
                          "traffic": measured_traffic(names[top]),
                          "per_unit": "4*Hq*D FLOP per visible (q,kv) pair (fwd); bwd 2.5x split "
-                                     "4/7 dK/dV, 3/7 dQ; units = rank-0 visible pairs"},
+                                     "4/5 dK/dV, 1/5 dQ GEMM (materialised dS) or 4/7, 3/7 "
+                                     "(recompute dQ); units = rank-0 visible pairs"},
+            "ds_mode": ds_mode,
             "kernels": {names[key]: {"ms": kms[key], "tflops": ktf[key], "frac": ktf[key] * 1e12 / peak,
                                      "launches": nl[key]} for key in kms},
             "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
