@@ -215,8 +215,8 @@ FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, ui
   tmem_st16(t_ds, dk);
   if (gdst) {     // tile layout [q/8][kv][8 q]: chunk i of this thread at gdst[i * 128]
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      gdst[i * kBK] = make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]);
+    for (int i = 0; i < 4; ++i)      // streaming: keep L2 for the Q/dO stream
+      st_global_cs(gdst + i * kBK, make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]));
   }
 }
 

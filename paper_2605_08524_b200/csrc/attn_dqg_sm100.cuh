@@ -92,7 +92,8 @@ attn_dqg_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant_
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
-      const uint64_t keep = policy_evict_last();
+      const uint64_t keep = policy_evict_last();     // K tiles: reused by other Q blocks
+      const uint64_t once = policy_evict_first();    // dS tiles: read exactly once
       uint32_t slot = 0, phase = 0;
       SchedCursor sc;
       for (int g; (g = sched_produce(sm.sched, sc, p.sched_counter)) < total;) {
@@ -110,7 +111,7 @@ attn_dqg_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant_
             mbar_wait(&sm.empty[slot], phase ^ 1);
             mbar_arrive_expect_tx(&sm.full[slot], 2 * kTile);
             const size_t tile = static_cast<size_t>(p.pair_ids[j]) * H + h;
-            bulk_load(sm.ds[slot], p.ds + tile * (kBN * kBM), kTile, &sm.full[slot]);
+            bulk_load_hint(sm.ds[slot], p.ds + tile * (kBN * kBM), kTile, &sm.full[slot], once);
             for (int half = 0; half < 2; ++half)
               tma_load_3d_hint(&sm.k[slot][half * kPanel], recv ? &tm_k_recv : &tm_k, &sm.full[slot],
                                half * 64, kvh, ref.off + t * kBN, keep);

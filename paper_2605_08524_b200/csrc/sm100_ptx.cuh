@@ -234,6 +234,20 @@ FCPB_DEV uint64_t smem_desc_noswz(uint32_t saddr, uint32_t lbo_bytes, uint32_t s
   return d;                                        // layout type 0: no swizzle
 }
 
+// 16-byte streaming store (evict-first in L2: written once, read once later).
+FCPB_DEV void st_global_cs(uint4* dst, uint4 v) {
+  asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};"
+               ::"l"(dst), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// 1-D bulk copy global -> shared with an L2 cache-policy hint.
+FCPB_DEV void bulk_load_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion on an mbarrier (transaction bytes).
 FCPB_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
   asm volatile(
