@@ -148,3 +148,20 @@ def test_fwd_bwd_four_simulated_ranks_fused_remote_wave():
     rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 512, GQA_SMALL, fuse_remote=True)
     _report("ragged N=4 fused remote wave", rep)
     assert_within_tolerance(rep)
+
+
+def test_fwd_bwd_recompute_dq(monkeypatch):
+    """The recompute dQ kernel (K2b), used when dS does not fit in HBM (C3, C4): forced
+    here on a case the default would run with materialised dS."""
+    monkeypatch.setenv("FCPB_DS", "0")
+    rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 2, 512, GQA_SMALL)
+    _report("recompute dQ N=2", rep)
+    assert_within_tolerance(rep)
+
+
+def test_materialised_ds_is_default_when_it_fits():
+    from paper_2605_08524_b200.attention import BlockAttention
+    from paper_2605_08524_b200.worklist import build_rank_work
+    r = schedule([1000, 300], 1, 512, GQA_SMALL)
+    op = BlockAttention(build_rank_work(r, 0), GQA_SMALL, torch.device("cuda", 0))
+    assert op.ds_mode
