@@ -21,6 +21,9 @@
 // S(j+1) cannot overwrite P(j) before dV(j) read it, nor dP(j+1) dS(j) before dK(j); and
 // phase 1 of tile j+1 (the exp work) overlaps dK(j)/dP(j+1), phase 2 of tile j overlaps
 // dV(j)/S(j+1).
+// Operand rings: Q is held from S(j) to dK(j), dO from dP(j) to phase 2 of tile j (its slot
+// carries delta), so Q gets three slots and dO two (227 KB of shared memory, exactly); lse2
+// travels with the Q slot.  Phase 1 keeps P as the same bf16 pairs the dV MMA consumes.
 // Warps: w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4-19 four softmax warpgroups, which
 //        also drain dK/dV at the end of each item (four warps per SMSP hide the exp
 //        phase's dependency latency; with two it ran at ~40% issue efficiency).
@@ -55,7 +58,8 @@ constexpr int kKVBytes = kBK * kD * 2;          // 32 KB (two 16 KB SW128 panels
 constexpr int kKVPanel = kKVBytes / 2;
 constexpr int kQBytes = kBQ * kD * 2;           // 32 KB (two 16 KB panels)
 constexpr int kQPanel = kQBytes / 2;
-constexpr int kSlots = 2;                       // Q ring and dO ring depth
+constexpr int kQSlots = 3;                      // Q ring depth (Q(j) is held until dK(j))
+constexpr int kDoSlots = 2;                     // dO ring depth (dO(j) is freed with Q(j))
 constexpr int kSoftmaxWGs = 4;
 constexpr int kCols = kBQ / kSoftmaxWGs;        // q columns per softmax warpgroup
 constexpr int kThreads = 128 * (1 + kSoftmaxWGs);
@@ -70,6 +74,15 @@ FCPB_DEV constexpr uint32_t a_col(uint32_t base, int kk) {
   return base + static_cast<uint32_t>((kk >> 1) * kCols + (kk & 1) * 8);
 }
 
+// Position in a ring of N slots: slot index and the parity of the current lap.
+template <int N>
+struct RingPos {
+  uint32_t slot = 0, phase = 0;
+  FCPB_DEV void next() {
+    if (++slot == N) { slot = 0; phase ^= 1; }
+  }
+};
+
 struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
 struct QRef { int32_t q_off, q_len, diag, pad_; };
 struct Item { int32_t kvseg, nblock; };
@@ -77,13 +90,13 @@ struct Item { int32_t kvseg, nblock; };
 struct Smem {
   uint8_t k[kKVBytes];
   uint8_t v[kKVBytes];
-  uint8_t q[kSlots][kQBytes];
-  uint8_t dout[kSlots][kQBytes];
-  float lse2[kSlots][kBQ];          // -lse * log2(e), per q column (travels with the Q slot)
-  float delta[kSlots][kBQ];         // -delta (read in phase 2, freed with the Q slot)
+  uint8_t q[kQSlots][kQBytes];
+  uint8_t dout[kDoSlots][kQBytes];
+  float lse2[kQSlots][kBQ];         // -lse * log2(e) (phase 1; travels with the Q slot)
+  float delta[kDoSlots][kBQ];       // -delta (phase 2; travels with the dO slot)
   uint64_t kv_full, kv_empty;
-  uint64_t q_full[kSlots], q_empty[kSlots];
-  uint64_t do_full[kSlots], do_empty[kSlots];
+  uint64_t q_full[kQSlots], q_empty[kQSlots];
+  uint64_t do_full[kDoSlots], do_empty[kDoSlots];
   uint64_t s_full, dp_full, p_full, ds_full;
   uint64_t acc_full, acc_free;
   SchedRing sched;
@@ -149,13 +162,13 @@ FCPB_DEV float4 lds128(uint32_t addr) {
   return v;
 }
 
-// Phase 1, 32 q columns of one kv row:  P = exp2(S*c + nlse2[q])  -> p (fp32, kept for
-// phase 2) and bf16 pairs stored at t_p.  kMask: ragged kv row / ragged q / causal diagonal.
+// Phase 1, 32 q columns of one kv row:  P = exp2(S*c + nlse2[q])  -> bf16 pairs in pk (kept
+// for phase 2; the dV MMA consumes the same bf16 P) and stored at t_p.
+// kMask: ragged kv row / ragged q / causal diagonal.
 template <bool kMask>
-FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p, uint32_t t_p,
+FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t (&pk)[16], uint32_t t_p,
                       bool kv_live, int col0, int q_valid, int shift) {
   const float2 c2 = make_float2(sl2, sl2);
-  uint32_t pk[16];
 #pragma unroll
   for (int c8 = 0; c8 < 4; ++c8) {
     const float4 la = lds128(l2 + c8 * 32), lb = lds128(l2 + c8 * 32 + 16);
@@ -185,8 +198,6 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p,
         p0 = (kv_live && col < q_valid && col >= shift) ? p0 : 0.f;
         p1 = (kv_live && col + 1 < q_valid && col + 1 >= shift) ? p1 : 0.f;
       }
-      p[i] = p0;
-      p[i + 1] = p1;
       pk[c8 * 4 + u] = pack_bf16(p0, p1);
     }
   }
@@ -195,7 +206,7 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, float* p,
 
 // Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds, and (when gdst is
 // set) the same 64 bytes into the materialised dS^T tile for the dQ GEMM.
-FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, uint32_t t_ds,
+FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const uint32_t (&pk)[16], uint32_t t_ds,
                        uint4* gdst) {
   uint32_t dk[16];
 #pragma unroll
@@ -206,8 +217,9 @@ FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const float* p, ui
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int i = c8 * 8 + 2 * u;
+      const uint32_t pp = pk[c8 * 4 + u];     // bf16 pair: low half = column i
       const float2 dd = __fmul2_rn(
-          make_float2(p[i], p[i + 1]),
+          make_float2(__uint_as_float(pp << 16), __uint_as_float(pp & 0xffff0000u)),
           __fadd2_rn(make_float2(__uint_as_float(dp[i]), __uint_as_float(dp[i + 1])), nd[u]));
       dk[c8 * 4 + u] = pack_bf16(dd.x, dd.y);
     }
@@ -231,6 +243,11 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  {
+    uint32_t dyn;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (reinterpret_cast<uint8_t*>(&sm) + sizeof(Smem) > smem_raw + dyn) __trap();
+  }
   const uint32_t warp = warp_id();
   const int group = p.num_q_heads / p.num_kv_heads;
   const int total = p.num_items * p.num_kv_heads;
@@ -246,10 +263,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   if (warp == 1 && elect_one()) {
     mbar_init(&sm.kv_full, 1);
     mbar_init(&sm.kv_empty, 1);
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&sm.q_full[s], 1 + 32);   // TMA expect_tx arrive + 32 cp.async arrives
+    for (int s = 0; s < kQSlots; ++s) {
+      mbar_init(&sm.q_full[s], 1 + 32);   // TMA expect_tx arrive + 32 cp.async (lse2) arrives
       mbar_init(&sm.q_empty[s], 1);
-      mbar_init(&sm.do_full[s], 1);
+    }
+    for (int s = 0; s < kDoSlots; ++s) {
+      mbar_init(&sm.do_full[s], 1 + 32);  // TMA expect_tx arrive + 32 cp.async (delta) arrives
       mbar_init(&sm.do_empty[s], 1);
     }
     mbar_init(&sm.s_full, 1);
@@ -273,7 +292,9 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       // lane 0 issues the TMA tiles, every lane copies 4 lse2 + 4 delta values with cp.async)
       const uint32_t lane = lane_id();
       const uint64_t keep = policy_evict_last();
-      uint32_t kv_phase = 0, slot = 0, slot_phase = 0;
+      uint32_t kv_phase = 0;
+      RingPos<kQSlots> qr_;
+      RingPos<kDoSlots> dr_;
       int ptile = 0;
       SchedCursor sc;
       for (int g; (g = __shfl_sync(0xffffffffu, lane == 0 ? sched_produce(sm.sched, sc, p.sched_counter) : 0, 0)) < total;) {
@@ -303,11 +324,12 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             const int qrow = qr.q_off + mb * kBQ;
             for (int gq = 0; gq < group; ++gq) {
               const int h = kvh * group + gq;
-              mbar_wait(&sm.q_empty[slot], slot_phase ^ 1);
+              const uint32_t qs = qr_.slot, ds = dr_.slot;
+              mbar_wait(&sm.q_empty[qs], qr_.phase ^ 1);
               if (lane == 0) {
-                mbar_arrive_expect_tx(&sm.q_full[slot], kQBytes);
+                mbar_arrive_expect_tx(&sm.q_full[qs], kQBytes);
                 for (int half = 0; half < 2; ++half)
-                  tma_load_3d_hint(&sm.q[slot][half * kQPanel], &tm_q, &sm.q_full[slot],
+                  tma_load_3d_hint(&sm.q[qs][half * kQPanel], &tm_q, &sm.q_full[qs],
                                    half * 64, h, qrow, keep);
               }
               const float* lsrc = p.lse2_t + static_cast<int64_t>(h) * p.t_pad + qrow;
@@ -316,21 +338,28 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               for (int u = 0; u < kBQ / 32; ++u) {
                 const int i = lane + 32 * u;
                 const bool ok = qrow + i < p.q_tokens;
-                cp_async_4(&sm.lse2[slot][i], ok ? lsrc + i : p.lse2_t, ok);
-                cp_async_4(&sm.delta[slot][i], ok ? dsrc + i : p.delta_t, ok);
+                cp_async_4(&sm.lse2[qs][i], ok ? lsrc + i : p.lse2_t, ok);
               }
-              cp_async_arrive_noinc(&sm.q_full[slot]);
+              cp_async_arrive_noinc(&sm.q_full[qs]);
               // the first Q tile of an item goes out before K/V (they only wait on the ring)
               if (!kv_issued) issue_kv();
-              mbar_wait(&sm.do_empty[slot], slot_phase ^ 1);
+              mbar_wait(&sm.do_empty[ds], dr_.phase ^ 1);
               if (lane == 0) {
-                mbar_arrive_expect_tx(&sm.do_full[slot], kQBytes);
+                mbar_arrive_expect_tx(&sm.do_full[ds], kQBytes);
                 for (int half = 0; half < 2; ++half)
-                  tma_load_3d_hint(&sm.dout[slot][half * kQPanel], &tm_do, &sm.do_full[slot],
+                  tma_load_3d_hint(&sm.dout[ds][half * kQPanel], &tm_do, &sm.do_full[ds],
                                    half * 64, h, qrow, keep);
               }
+#pragma unroll
+              for (int u = 0; u < kBQ / 32; ++u) {
+                const int i = lane + 32 * u;
+                const bool ok = qrow + i < p.q_tokens;
+                cp_async_4(&sm.delta[ds][i], ok ? dsrc + i : p.delta_t, ok);
+              }
+              cp_async_arrive_noinc(&sm.do_full[ds]);
+              qr_.next();
+              dr_.next();
               FCPB_TR(kTrQIssue, ptile); ++ptile;
-              if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
             }
           }
         }
@@ -342,7 +371,9 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       const uint32_t id_acc = idesc_bf16_f32(kBK, kD, false, true);    // dV, dK (B MN-major)
       const uint32_t a_k = smem_u32(sm.k), a_v = smem_u32(sm.v);
       const bool leader = elect_one();
-      uint32_t kv_phase = 0, slot = 0, slot_phase = 0, acc_phase = 0;
+      uint32_t kv_phase = 0, acc_phase = 0;
+      RingPos<kQSlots> qr_;
+      RingPos<kDoSlots> dr_;
       uint32_t p_phase = 0, ds_phase = 0;
       uint32_t tile = 0;
 
@@ -361,13 +392,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         __syncwarp();
       };
       // dV += P^T dO  /  dK += dS^T Q:  A from TMEM, B = the [q, d] tile (MN-major).
-      auto issue_acc = [&](uint32_t a_base, uint32_t b_base, uint32_t col, bool acc, uint64_t* done) {
+      auto issue_acc = [&](uint32_t a_base, uint32_t b_base, uint32_t col, bool acc, uint64_t* done,
+                           uint64_t* done2 = nullptr) {
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < kBQ / 16; ++kk)
             mma_ts(tmem + col, tmem + a_col(a_base, kk),
                    smem_desc_sw128(b_base + kk * 2048, kQPanel, 1024), id_acc, acc || kk > 0);
-          mma_commit(done);
+          if (done) mma_commit(done);
+          if (done2) mma_commit(done2);
         }
         __syncwarp();
       };
@@ -385,17 +418,18 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         kv_phase ^= 1;
         // prologue: S(0), dP(0).  The S/dP regions are free: the previous item's last
         // dV/dK were issued after its softmax finished with them (in-order pipe).
-        mbar_wait(&sm.q_full[slot], slot_phase);
+        mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
         FCPB_TR(kTrQGot, (int)tile);
         tc_fence_after();
-        issue_kq(a_k, smem_u32(sm.q[slot]), kColS, &sm.s_full);
+        issue_kq(a_k, smem_u32(sm.q[qr_.slot]), kColS, &sm.s_full);
         FCPB_TR(kTrSIssue, (int)tile);
-        mbar_wait(&sm.do_full[slot], slot_phase);
+        mbar_wait(&sm.do_full[dr_.slot], dr_.phase);
         tc_fence_after();
-        issue_kq(a_v, smem_u32(sm.dout[slot]), kColDP, &sm.dp_full);
+        issue_kq(a_v, smem_u32(sm.dout[dr_.slot]), kColDP, &sm.dp_full);
         for (int j = 0; j < n; ++j, ++tile) {
-          const uint32_t cur = slot;
-          if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+          const uint32_t qcur = qr_.slot, dcur = dr_.slot;
+          qr_.next();
+          dr_.next();
           mbar_wait(&sm.p_full, p_phase);
           p_phase ^= 1;
           FCPB_TR(kTrPGot, (int)tile);
@@ -404,25 +438,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             acc_phase ^= 1;
           }
           tc_fence_after();
-          issue_acc(kColS, smem_u32(sm.dout[cur]), kColDV, j > 0, &sm.do_empty[cur]);
+          issue_acc(kColS, smem_u32(sm.dout[dcur]), kColDV, j > 0, nullptr);
           FCPB_TR(kTrDvIssue, (int)tile);
           if (j + 1 < n) {
-            mbar_wait(&sm.q_full[slot], slot_phase);
+            mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
             FCPB_TR(kTrQGot, (int)tile + 1);
             tc_fence_after();
-            issue_kq(a_k, smem_u32(sm.q[slot]), kColS, &sm.s_full);
+            issue_kq(a_k, smem_u32(sm.q[qr_.slot]), kColS, &sm.s_full);
             FCPB_TR(kTrSIssue, (int)tile + 1);
           }
           mbar_wait(&sm.ds_full, ds_phase);
           ds_phase ^= 1;
           FCPB_TR(kTrDsGot, (int)tile);
           tc_fence_after();
-          issue_acc(kColDP, smem_u32(sm.q[cur]), kColDK, j > 0, &sm.q_empty[cur]);
+          // dO(j) is freed with Q(j): phase 2 reads delta from the dO slot until ds_full(j)
+          issue_acc(kColDP, smem_u32(sm.q[qcur]), kColDK, j > 0, &sm.q_empty[qcur], &sm.do_empty[dcur]);
           FCPB_TR(kTrDkIssue, (int)tile);
           if (j + 1 < n) {
-            mbar_wait(&sm.do_full[slot], slot_phase);
+            mbar_wait(&sm.do_full[dr_.slot], dr_.phase);
             tc_fence_after();
-            issue_kq(a_v, smem_u32(sm.dout[slot]), kColDP, &sm.dp_full);
+            issue_kq(a_v, smem_u32(sm.dout[dr_.slot]), kColDP, &sm.dp_full);
           }
         }
         if (leader) {
@@ -440,7 +475,9 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     const uint32_t t_s = tmem + lane_bits + kColS + wg * kCols;
     const uint32_t t_dp = tmem + lane_bits + kColDP + wg * kCols;
     const float sl2 = p.scale_log2;
-    uint32_t s_phase = 0, dp_phase = 0, slot = 0, slot_phase = 0, acc_phase = 0, tile = 0;
+    uint32_t s_phase = 0, dp_phase = 0, acc_phase = 0, tile = 0;
+    RingPos<kQSlots> qr_;
+    RingPos<kDoSlots> dr_;
     SchedCursor sc;
     for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const Item it = p.items[item_of(g, p)];
@@ -459,7 +496,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           const bool plain = kv_full_tile && q_valid >= kBQ && (!qr.diag || shift0 + kBK - 1 <= 0);
           const int shift = qr.diag ? shift0 + tid : -(1 << 30);
           for (int gq = 0; gq < group; ++gq, ++tile) {
-            float pr[kCols];
+            uint32_t pr[kCols / 2];      // bf16 P pairs, phase 1 -> phase 2
             uint4* gdst = nullptr;
             if (p.ds_out) {
               const size_t tid_tile = static_cast<size_t>(pair) * p.num_q_heads + kvh * group + gq;
@@ -470,10 +507,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             mbar_wait(&sm.s_full, s_phase);
             s_phase ^= 1;
             FCPB_TR(kTrSGot, (int)tile);
-            mbar_wait(&sm.q_full[slot], slot_phase);      // lse2 / delta of this tile landed
+            mbar_wait(&sm.q_full[qr_.slot], qr_.phase);   // lse2 of this tile landed
             tc_fence_after();
-            const uint32_t l2 = smem_u32(&sm.lse2[slot][wg * kCols]);
-            const uint32_t dl = smem_u32(&sm.delta[slot][wg * kCols]);
+            const uint32_t l2 = smem_u32(&sm.lse2[qr_.slot][wg * kCols]);
+            const uint32_t dl = smem_u32(&sm.delta[dr_.slot][wg * kCols]);
             // phase 1: P (bf16 lands over the first 16 of this warpgroup's S columns)
             {
               uint32_t sv[32];
@@ -493,6 +530,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             // phase 2: dS
             mbar_wait(&sm.dp_full, dp_phase);
             dp_phase ^= 1;
+            mbar_wait(&sm.do_full[dr_.slot], dr_.phase);  // delta of this tile landed
             FCPB_TR(kTrDpGot, (int)tile);
             tc_fence_after();
             {
@@ -505,7 +543,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             tc_fence_before();
             mbar_arrive(&sm.ds_full);
             FCPB_TR(kTrDsArrive, (int)tile);
-            if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
+            qr_.next();
+            dr_.next();
           }
         }
       }

@@ -40,6 +40,8 @@ EV2 = ["KIssue", "KGot", "SIssue", "DsGot", "DqIssue", "SGot", "Freed", "DpGot",
 buf2 = (ctypes.c_ulonglong * (len(EV2) * T))()
 lib.fcpb_debug_dq_trace(buf2, len(EV2) * T)
 b = np.frombuffer(buf2, dtype=np.uint64).reshape(len(EV2), T).astype(np.int64)
+if not (b > 0).any():
+    b[:] = 1      # materialised-dS mode: the recompute dQ kernel did not run
 t0 = b[b > 0].min()
 b = np.where(b > 0, b - t0, -1)
 print("dq tile " + " ".join(f"{e:>9s}" for e in EV2))
