@@ -156,6 +156,7 @@ class FcpExecutor:
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 x.barrier("kv", 0)                      # everyone's K/V readable
+                self._mark("comm_kv_ready", self.comm)
                 for s_idx in range(len(self.stages)):
                     x.pull_stage(s_idx, self.k_recv, self.v_recv)
                     ev = torch.cuda.Event()
@@ -198,6 +199,7 @@ class FcpExecutor:
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 x.barrier("part", 0)                    # every rank's partials written
+                self._mark("comm_part_ready", self.comm)
                 x.pull_returns(self.returns, sk, sv, self.ret_rows)
                 x.barrier("part", 1)                    # pulled: partial buffers reusable
                 self._mark("comm_return_done", self.comm)
