@@ -202,6 +202,16 @@ FCPB_API int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stre
 FCPB_API int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64_t n_rows,
                     int64_t row_elems, void* stream);
 
+/* Exchange readiness flags without an SM (stream memory operations; replaces a signalling
+ * kernel, which cannot become resident beside the persistent attention kernels).
+ * fcpb_stream_signal: after the stream's prior work, write `value` to the 32-bit `flag`
+ *   (local or peer-mapped symmetric memory), preceded by a stream-scoped system fence.
+ * fcpb_stream_wait: later work on the stream waits until (int32)(*flag - value) >= 0.
+ * Replaces the symmetric-memory barrier kernels the exchange used around each pull set
+ * (the reference models this ordering as stage boundaries, simulator.py:136-151). */
+FCPB_API int fcpb_stream_signal(void* flag, uint32_t value, void* stream);
+FCPB_API int fcpb_stream_wait(const void* flag, uint32_t value, void* stream);
+
 FCPB_API const char* fcpb_last_error(void);
 FCPB_API int fcpb_version(void);
 FCPB_API int fcpb_device_supported(int device);

@@ -358,6 +358,43 @@ int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse, float
   return FCPB_OK;
 }
 
+// Exchange readiness flags, executed by the stream's front end (no SM): the persistent
+// attention kernels fill every SM's shared memory, so a signalling *kernel* queued beside
+// them waits for a whole launch before it can run.
+namespace {
+using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+StreamValueFn stream_value_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    return reinterpret_cast<StreamValueFn>(p);
+  return nullptr;
+}
+}  // namespace
+
+int fcpb_stream_signal(void* flag, uint32_t value, void* stream) {
+  static StreamValueFn fn = stream_value_fn("cuStreamWriteValue32");
+  if (!fn) return fail(FCPB_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  if (!flag || reinterpret_cast<uintptr_t>(flag) % 4) return fail(FCPB_ERR_INVALID, "flag must be 4-byte aligned");
+  // default flags: a stream-scoped system fence orders the stream's prior writes first
+  const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(FCPB_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return FCPB_OK;
+}
+
+int fcpb_stream_wait(const void* flag, uint32_t value, void* stream) {
+  static StreamValueFn fn = stream_value_fn("cuStreamWaitValue32");
+  if (!fn) return fail(FCPB_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  if (!flag || reinterpret_cast<uintptr_t>(flag) % 4) return fail(FCPB_ERR_INVALID, "flag must be 4-byte aligned");
+  // GEQ compares (int32)(*flag - value) >= 0: monotonically increasing epochs wrap safely
+  const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                        CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(FCPB_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  return FCPB_OK;
+}
+
 int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
   if (n <= 0) return FCPB_OK;
   if (n % 4) return fail(FCPB_ERR_INVALID, "n must be a multiple of 4");

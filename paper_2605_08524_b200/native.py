@@ -86,8 +86,8 @@ class DqDsArgs(ctypes.Structure):
 
 EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_dq_ds",
            "fcpb_lse_merge", "fcpb_bwd_preprocess",
-           "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_last_error", "fcpb_version",
-           "fcpb_device_supported")
+           "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_stream_signal", "fcpb_stream_wait",
+           "fcpb_last_error", "fcpb_version", "fcpb_device_supported")
 
 _lib = None
 
@@ -110,6 +110,8 @@ def load(path: str | None = None):
                                          c_i32, c_vp]
     lib.fcpb_f32_to_bf16.argtypes = [c_vp, c_vp, c_i64, c_vp]
     lib.fcpb_dkv_reduce.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]
+    lib.fcpb_stream_signal.argtypes = [c_vp, ctypes.c_uint32, c_vp]
+    lib.fcpb_stream_wait.argtypes = [c_vp, ctypes.c_uint32, c_vp]
     lib.fcpb_last_error.restype = ctypes.c_char_p
     lib.fcpb_device_supported.argtypes = [ctypes.c_int]
     for name in EXPORTS:
@@ -135,3 +137,13 @@ def ptr(t) -> int:
 
 def stream_handle(stream) -> int:
     return stream.cuda_stream if stream is not None else 0
+
+
+def stream_signal(flag_addr: int, value: int, stream) -> None:
+    """Write `value` to a (peer-mapped) 32-bit flag after the stream's prior work."""
+    check(load().fcpb_stream_signal(flag_addr, value & 0xFFFFFFFF, stream_handle(stream)))
+
+
+def stream_wait(flag_addr: int, value: int, stream) -> None:
+    """Later work on `stream` waits until the local 32-bit flag reaches `value`."""
+    check(load().fcpb_stream_wait(flag_addr, value & 0xFFFFFFFF, stream_handle(stream)))

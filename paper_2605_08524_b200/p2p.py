@@ -14,9 +14,12 @@ Buffers (torch symmetric memory, same size on every rank):
 * ``part`` fp32 [2, R_max, Hkv, D] -- dK/dV partials of the chunks a rank *received*
   (written directly by the dK/dV kernel), pulled back by the chunk owners.
 
-Ordering: a symmetric-memory device barrier after the K/V copy (everyone's K/V is
-readable), after the forward pulls (K/V may be overwritten next step), after the
-partials are written, and after the return pulls.  Each plan edge (reference
+* ``flags`` int32 [4, world] -- readiness words written by the peers' streams.
+
+Ordering: an all-rank barrier after the K/V copy (everyone's K/V is readable), after
+the forward pulls (K/V may be overwritten next step), after the partials are written,
+and after the return pulls.  The barrier is stream memory operations on the flag words
+(``fcpb_stream_signal`` / ``fcpb_stream_wait``), executed without an SM.  Each plan edge (reference
 ``planner.py:81-102``) becomes exactly one pull of K and one of V in its coalesced
 stage; the Delta-matching guarantees each GPU reads from at most ``degree`` peers
 and is read by at most ``degree`` peers per stage.
@@ -24,10 +27,13 @@ and is read by at most ``degree`` peers per stage.
 
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 import torch.distributed._symmetric_memory as symm
 
+from . import native
 from .distributor import chunk_placement
 from .worklist import rank_layout
 
@@ -64,6 +70,15 @@ class SymmetricExchange:
                         for p in range(self.world)]
         self.peer_part = [self.h_part.get_buffer(p, (2, r_max, H, D), torch.float32)
                           for p in range(self.world)]
+        # Readiness flags: [channel][src rank] int32 words in symmetric memory, written by
+        # the peers' stream front ends (native.stream_signal) and waited on locally.
+        self.flags = symm.empty(self.N_CHANNELS * self.world, dtype=torch.int32, device=device)
+        self.flags.zero_()
+        self.h_flags = symm.rendezvous(self.flags, self.group)
+        self.flag_base = [int(a) for a in self.h_flags.buffer_ptrs]
+        self.epoch = [0] * self.N_CHANNELS
+        torch.cuda.synchronize(device)
+        dist.barrier(group=self.group)                  # every rank's flags are zero
         # Pulls from different peers go to different streams so several copy engines run
         # at once (one stream serialises every copy on one engine).
         self.copy_streams = [torch.cuda.Stream(device=device) for _ in range(min(4, max(self.world - 1, 1)))]
@@ -94,8 +109,30 @@ class SymmetricExchange:
         self.kv[0, :self.t_local].copy_(k, non_blocking=True)
         self.kv[1, :self.t_local].copy_(v, non_blocking=True)
 
+    N_CHANNELS = 4          # kv ready, kv consumed, partials ready, partials consumed
+    BARRIER = os.environ.get("FCPB_BARRIER", "flags")   # "kernel": torch's barrier (A/B only)
+
     def barrier(self, which: str = "kv", channel: int = 0):
-        (self.h_kv if which == "kv" else self.h_part).barrier(channel=channel)
+        """All-rank barrier on the current stream.  Stream memory operations, not a kernel:
+        every rank writes epoch e into each peer's flag word [channel][me], then waits for
+        its own [channel][p] words to reach e.  A barrier kernel cannot become resident
+        while a persistent attention kernel fills every SM's shared memory (K2 uses all
+        227 KB), so it used to wait for the whole launch (C2 at N=4: the partial returns
+        started 2 ms late)."""
+        if self.BARRIER == "kernel":
+            (self.h_kv if which == "kv" else self.h_part).barrier(channel=channel)
+            return
+        ch = (0 if which == "kv" else 2) + channel
+        self.epoch[ch] += 1
+        e = self.epoch[ch]
+        cur = torch.cuda.current_stream(self.device)
+        w, me = self.world, self.rank
+        for p in range(w):
+            if p != me:
+                native.stream_signal(self.flag_base[p] + 4 * (ch * w + me), e, cur)
+        for p in range(w):
+            if p != me:
+                native.stream_wait(self.flag_base[me] + 4 * (ch * w + p), e, cur)
 
     FANOUT_BYTES = 64 << 20
 
