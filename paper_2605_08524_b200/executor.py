@@ -156,7 +156,6 @@ class FcpExecutor:
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 x.barrier("kv", 0)                      # everyone's K/V readable
-                self._mark("comm_kv_ready", self.comm)
                 for s_idx in range(len(self.stages)):
                     x.pull_stage(s_idx, self.k_recv, self.v_recv)
                     ev = torch.cuda.Event()
@@ -198,9 +197,14 @@ class FcpExecutor:
             sv = torch.empty_like(sk)
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
-                x.barrier("part", 0)                    # every rank's partials written
-                self._mark("comm_part_ready", self.comm)
-                x.pull_returns(self.returns, sk, sv, self.ret_rows)
+                if x.BARRIER == "kernel":
+                    x.barrier("part", 0)                # every rank's partials written
+                    x.pull_returns(self.returns, sk, sv, self.ret_rows)
+                else:
+                    # my partials are written; each owner pulls a consumer's partials as
+                    # soon as that consumer has signalled (no wait for the slowest rank)
+                    x.signal_all("part", 0)
+                    x.pull_returns(self.returns, sk, sv, self.ret_rows, per_peer_ready=True)
                 x.barrier("part", 1)                    # pulled: partial buffers reusable
                 self._mark("comm_return_done", self.comm)
             staged = (sk, sv)

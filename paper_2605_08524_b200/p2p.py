@@ -122,29 +122,47 @@ class SymmetricExchange:
         if self.BARRIER == "kernel":
             (self.h_kv if which == "kv" else self.h_part).barrier(channel=channel)
             return
-        ch = (0 if which == "kv" else 2) + channel
+        self.signal_all(which, channel)
+        cur = torch.cuda.current_stream(self.device)
+        for p in range(self.world):
+            if p != self.rank:
+                self.wait_peer(which, channel, p, cur)
+
+    def _channel(self, which: str, channel: int) -> int:
+        return (0 if which == "kv" else 2) + channel
+
+    def signal_all(self, which: str, channel: int) -> None:
+        """Open a new epoch on the channel and tell every peer (current stream)."""
+        ch = self._channel(which, channel)
         self.epoch[ch] += 1
-        e = self.epoch[ch]
         cur = torch.cuda.current_stream(self.device)
         w, me = self.world, self.rank
         for p in range(w):
             if p != me:
-                native.stream_signal(self.flag_base[p] + 4 * (ch * w + me), e, cur)
-        for p in range(w):
-            if p != me:
-                native.stream_wait(self.flag_base[me] + 4 * (ch * w + p), e, cur)
+                native.stream_signal(self.flag_base[p] + 4 * (ch * w + me), self.epoch[ch], cur)
+
+    def wait_peer(self, which: str, channel: int, peer: int, stream) -> None:
+        """Work queued on `stream` after this waits for peer's signal of the current epoch."""
+        ch = self._channel(which, channel)
+        native.stream_wait(self.flag_base[self.rank] + 4 * (ch * self.world + peer), self.epoch[ch], stream)
 
     FANOUT_BYTES = 64 << 20
 
-    def _fanout(self, copies, nbytes):
+    def _fanout(self, copies, nbytes, pre=None):
         """Run (peer, fn) copies with one stream per peer (mod the copy-stream count), ordered
         after the current stream's prior work; the current stream then waits for all.
         Measured on C2/C4 at N=4: fan-out lifts large exchanges (C4 returns 411 -> 483 GB/s)
         but the fork/join costs more than it gains below ~64 MB (C2 pulls 260 -> 171 GB/s),
-        so small copy sets stay on the current stream."""
+        so small copy sets stay on the current stream.
+        `pre(peer, stream)`, when given, runs once per peer on the stream that carries its
+        copies, before the first of them (a per-peer readiness wait)."""
         cur = torch.cuda.current_stream(self.device)
+        seen = set()
         if nbytes < self.FANOUT_BYTES or len(self.copy_streams) == 1:
-            for _, fn in copies:
+            for peer, fn in copies:
+                if pre is not None and peer not in seen:
+                    pre(peer, cur)
+                    seen.add(peer)
                 fn()
             return
         used = set()
@@ -154,6 +172,9 @@ class SymmetricExchange:
             if i not in used:
                 cs.wait_stream(cur)
                 used.add(i)
+            if pre is not None and peer not in seen:
+                pre(peer, cs)
+                seen.add(peer)
             with torch.cuda.stream(cs):
                 fn()
         for i in used:
@@ -177,9 +198,10 @@ class SymmetricExchange:
             return None, None
         return self.part[0, :self.r_local], self.part[1, :self.r_local]
 
-    def pull_returns(self, returns, staging_k, staging_v, staging_rows):
+    def pull_returns(self, returns, staging_k, staging_v, staging_rows, per_peer_ready=False):
         """Owner side: pull every consumer's partial of my chunks (``exchange.owner_returns``)
-        into staging rows."""
+        into staging rows.  per_peer_ready: each consumer's pulls wait only for that
+        consumer's "partials ready" signal (``signal_all("part", 0)``), not for all ranks."""
         def pull(peer, src, r, n):
             pp = self.peer_part[peer]
             staging_k[r:r + n].copy_(pp[0, src:src + n], non_blocking=True)
@@ -189,4 +211,5 @@ class SymmetricExchange:
             a = (t.peer, self.layouts[t.peer].recv_offset[t.chunk], staging_rows[(t.chunk, t.peer)],
                  t.tokens)
             copies.append((t.peer, (lambda a=a: pull(*a))))
-        self._fanout(copies, sum(t.tokens for t in returns) * 2 * self.part_row_bytes)
+        pre = (lambda peer, st: self.wait_peer("part", 0, peer, st)) if per_peer_ready else None
+        self._fanout(copies, sum(t.tokens for t in returns) * 2 * self.part_row_bytes, pre)
