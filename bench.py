@@ -349,6 +349,8 @@ def main():
     from paper_2605_08524_b200.executor import FcpExecutor
 
     peak, peak_sus, hbm, peak_kind = load_peaks()
+    peak_run, peak_run_kind = ((peak_sus, peak_kind + " sustained (kernel timed inside the step loop)")
+                               if peak_sus > 0 else (peak, peak_kind + " burst"))
     t_plan = time.perf_counter()
     w, result = build_workload(args.config, n, args.block, args.scheduler)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
@@ -522,9 +524,12 @@ def main():
                        "parallelism": f"{args.scheduler}{n}", "l2": "inputs larger than L2 (no flush needed)",
                        "plan_ms_host": round(plan_ms, 2)},
             "mfu": mfu, "flop_total": flop_total,
+            # The kernels are timed inside the step loop (back-to-back steps under the 1 kW
+            # cap), so the denominator is the sustained bf16 figure; the burst one is beside it.
             "roofline": {"bound": "tensor", "kernel": names[top],
-                         "achieved": ktf[top], "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": ktf[top] * 1e12 / peak, "peak_kind": peak_kind + " burst",
+                         "achieved": ktf[top], "peak": peak_run / 1e12, "unit": "TFLOP/s",
+                         "frac": ktf[top] * 1e12 / peak_run, "peak_kind": peak_run_kind,
+                         "peak_burst": peak / 1e12, "frac_of_burst": ktf[top] * 1e12 / peak,
                          "traffic": measured_traffic(names[top]),
                          "per_unit": "4*Hq*D FLOP per visible (q,kv) pair (fwd); bwd 2.5x split "
                                      "4/5 dK/dV, 1/5 dQ GEMM (materialised dS) or 4/7, 3/7 "
