@@ -150,7 +150,8 @@ def measured_traffic(kernel: str):
         return None
 
 
-def build_workload(name: str, n: int, block: int | None, scheduler: str = "fcp"):
+def build_workload(name: str, n: int, block: int | None, scheduler: str = "fcp",
+                   curve: str = "reference"):
     """The workload and its plan: FCP (default), or the reference's competitor plans
     (ring / ByteScale) executed by the same B200 executor."""
     w = configs.by_name(name, n, block)
@@ -160,8 +161,9 @@ def build_workload(name: str, n: int, block: int | None, scheduler: str = "fcp")
     if scheduler == "bytescale":
         from paper_2605_08524_b200.baselines import bytescale_schedule
         return w, bytescale_schedule(w.batch(), n, w.tokens_per_worker, w.model)
+    from paper_2605_08524_b200.costmodel import B200_EFFICIENCY
     result = fcp_schedule(w.batch(), n, ShardingConfig(block_size=w.block_size), w.model,
-                          DEFAULT_EFFICIENCY)
+                          B200_EFFICIENCY if curve == "b200" else DEFAULT_EFFICIENCY)
     return w, result
 
 
@@ -327,6 +329,8 @@ def main():
     ap.add_argument("--scheduler", default="fcp", choices=["fcp", "ring", "bytescale"],
                     help="plan to execute (ring / bytescale: the reference's competitors)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--curve", default="reference", choices=["reference", "b200"],
+                    help="efficiency curve the LPT placement plans with (costmodel.py)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -352,7 +356,7 @@ def main():
     peak_run, peak_run_kind = ((peak_sus, peak_kind + " sustained (kernel timed inside the step loop)")
                                if peak_sus > 0 else (peak, peak_kind + " burst"))
     t_plan = time.perf_counter()
-    w, result = build_workload(args.config, n, args.block, args.scheduler)
+    w, result = build_workload(args.config, n, args.block, args.scheduler, args.curve)
     plan_ms = (time.perf_counter() - t_plan) * 1e3
     cfg = w.model
     ex = FcpExecutor(result, rank, cfg, device)
@@ -522,7 +526,7 @@ def main():
                        "sequences": len(w.lengths), "block": w.block_size,
                        "q_heads": cfg.q_heads, "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim,
                        "parallelism": f"{args.scheduler}{n}", "l2": "inputs larger than L2 (no flush needed)",
-                       "plan_ms_host": round(plan_ms, 2)},
+                       "plan_ms_host": round(plan_ms, 2), "efficiency_curve": args.curve},
             "mfu": mfu, "flop_total": flop_total,
             # The kernels are timed inside the step loop (back-to-back steps under the 1 kW
             # cap), so the denominator is the sustained bf16 figure; the burst one is beside it.
