@@ -202,6 +202,16 @@ FCPB_API int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stre
 FCPB_API int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64_t n_rows,
                     int64_t row_elems, void* stream);
 
+/* K4 (fused): the owner's final bf16 dK, dV rows: out[r] = bf16(local[r] + sum of
+ * staged[src_rows[j]] for j in [row_ptr[r], row_ptr[r+1])), for `n_rows` rows of `row_elems`
+ * fp32.  The staged rows are the partials consumers returned along reversed plan edges; the
+ * reference never models this step.  Replaces fcpb_dkv_reduce rounds plus
+ * two fcpb_f32_to_bf16 passes. */
+FCPB_API int fcpb_dkv_finalize(const float* local_k, const float* local_v, const float* staged_k,
+                               const float* staged_v, const int32_t* row_ptr,
+                               const int32_t* src_rows, int64_t n_rows, int64_t row_elems,
+                               void* out_k, void* out_v, void* stream);
+
 /* Exchange readiness flags without an SM (stream memory operations; replaces a signalling
  * kernel, which cannot become resident beside the persistent attention kernels).
  * fcpb_stream_signal: after the stream's prior work, write `value` to the 32-bit `flag`

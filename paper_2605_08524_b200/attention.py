@@ -317,6 +317,18 @@ class BlockAttention:
                                               src.shape[0], row, self._stream(stream)))
         self.launches += 1
 
+    def finalize_dkv(self, dk, dv, staged_k, staged_v, row_ptr, src_rows, stream=None):
+        """K4 (fused): bf16(dK/dV local rows + their returned partials), one launch."""
+        out_k = torch.empty(dk.shape, dtype=torch.bfloat16, device=self.device)
+        out_v = torch.empty(dv.shape, dtype=torch.bfloat16, device=self.device)
+        row = self.cfg.kv_heads * self.cfg.head_dim
+        native.check(self.lib.fcpb_dkv_finalize(
+            native.ptr(dk), native.ptr(dv), native.ptr(staged_k), native.ptr(staged_v),
+            native.ptr(row_ptr), native.ptr(src_rows), dk.shape[0], row,
+            native.ptr(out_k), native.ptr(out_v), self._stream(stream)))
+        self.launches += 1
+        return out_k, out_v
+
     def backward(self, q, k, v, o, lse, do, k_recv=None, v_recv=None, stream=None):
         """Single-rank backward.  Returns (dq, dk, dv) bf16 and, if the rank
         received KV, the fp32 (dk_recv, dv_recv) partials owed to their owners."""

@@ -139,5 +139,33 @@ __global__ void __launch_bounds__(256) dkv_reduce_kernel(float4* __restrict__ ds
   }
 }
 
+// K4 (fused): the owner's final dK and dV in one pass.  Row r of `local` plus every returned
+// partial of it (staging rows src_rows[row_ptr[r] .. row_ptr[r+1]), one per consuming rank),
+// rounded once to bf16.  Each output row has one owner thread per float4, so no rounds and
+// no atomics; replaces (gather + K4 add) per receiver round and the two fp32->bf16 passes.
+__global__ void __launch_bounds__(256) dkv_finalize_kernel(
+    const float4* __restrict__ local_k, const float4* __restrict__ local_v,
+    const float4* __restrict__ staged_k, const float4* __restrict__ staged_v,
+    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ src_rows,
+    int64_t n_rows, int64_t row4, uint2* __restrict__ out_k, uint2* __restrict__ out_v) {
+  const int64_t work = n_rows * row4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < work;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / row4, c = i % row4;
+    float4 a = local_k[i], b = local_v[i];
+    const int32_t e = row_ptr[r + 1];
+    for (int32_t j = row_ptr[r]; j < e; ++j) {
+      const int64_t sidx = static_cast<int64_t>(src_rows[j]) * row4 + c;
+      const float4 sk = staged_k[sidx], sv = staged_v[sidx];
+      a.x += sk.x; a.y += sk.y; a.z += sk.z; a.w += sk.w;
+      b.x += sv.x; b.y += sv.y; b.z += sv.z; b.w += sv.w;
+    }
+    __nv_bfloat162 k0 = __floats2bfloat162_rn(a.x, a.y), k1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 v0 = __floats2bfloat162_rn(b.x, b.y), v1 = __floats2bfloat162_rn(b.z, b.w);
+    out_k[i] = make_uint2(*reinterpret_cast<uint32_t*>(&k0), *reinterpret_cast<uint32_t*>(&k1));
+    out_v[i] = make_uint2(*reinterpret_cast<uint32_t*>(&v0), *reinterpret_cast<uint32_t*>(&v1));
+  }
+}
+
 }  // namespace aux
 }  // namespace fcpb

@@ -409,6 +409,26 @@ int fcpb_f32_to_bf16(const float* src, void* dst, int64_t n, void* stream) {
   return FCPB_OK;
 }
 
+int fcpb_dkv_finalize(const float* local_k, const float* local_v, const float* staged_k,
+                      const float* staged_v, const int32_t* row_ptr, const int32_t* src_rows,
+                      int64_t n_rows, int64_t row_elems, void* out_k, void* out_v, void* stream) {
+  if (n_rows <= 0) return FCPB_OK;
+  if (row_elems % 4) return fail(FCPB_ERR_INVALID, "row_elems must be a multiple of 4");
+  if (!local_k || !local_v || !row_ptr || !out_k || !out_v)
+    return fail(FCPB_ERR_INVALID, "null local / row_ptr / output pointer");
+  const int block = 256;
+  const int64_t work = n_rows * (row_elems / 4);
+  int64_t grid = (work + block - 1) / block;
+  if (grid > 148 * 16) grid = 148 * 16;
+  fcpb::aux::dkv_finalize_kernel<<<static_cast<unsigned>(grid), block, 0,
+                                   static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const float4*>(local_k), reinterpret_cast<const float4*>(local_v),
+      reinterpret_cast<const float4*>(staged_k), reinterpret_cast<const float4*>(staged_v), row_ptr,
+      src_rows, n_rows, row_elems / 4, reinterpret_cast<uint2*>(out_k), reinterpret_cast<uint2*>(out_v));
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
 int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64_t n_rows,
                     int64_t row_elems, void* stream) {
   if (n_rows <= 0) return FCPB_OK;

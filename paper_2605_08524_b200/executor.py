@@ -63,9 +63,18 @@ class FcpExecutor:
         self.returns = exchange.owner_returns(layouts, chunk_placement(result.assignment, result.units),
                                               rank)
         self.ret_rows, rounds, self.ret_tokens = exchange.return_staging_layout(self.returns)
-        self.ret_rounds = [(torch.tensor(src, dtype=torch.int64, device=self.device),
-                            torch.tensor(dst, dtype=torch.int32, device=self.device))
-                           for src, dst in rounds]
+        # K4 (fused finalize): per local row, the staging rows of its returned partials (CSR)
+        import numpy as np
+        T = self.layout.tokens
+        dst_all = np.array([d for _, dst in rounds for d in dst], dtype=np.int64)
+        src_all = np.array([x for src, _ in rounds for x in src], dtype=np.int64)
+        order = np.argsort(dst_all, kind="stable")
+        row_ptr = np.zeros(T + 1, dtype=np.int32)
+        if len(dst_all):
+            row_ptr[1:] = np.cumsum(np.bincount(dst_all, minlength=T))
+        self.ret_row_ptr = torch.tensor(row_ptr, dtype=torch.int32, device=self.device)
+        self.ret_src_rows = torch.tensor(src_all[order] if len(src_all) else np.zeros(1, np.int64),
+                                         dtype=torch.int32, device=self.device)
         self.comm = torch.cuda.Stream(device=self.device, priority=-1)
         self.xchg = None
         if self.world > 1:
@@ -225,9 +234,10 @@ class FcpExecutor:
         if staged is not None:
             cur.wait_stream(self.comm)
             self._mark("bwd_wait_return", cur)
-            for src, dst in self.ret_rounds:        # K4, one race-free round per receiver rank
-                op.reduce_dkv(dk, staged[0].index_select(0, src), dst, cur)
-                op.reduce_dkv(dv, staged[1].index_select(0, src), dst, cur)
+            # K4: local rows + every returned partial, rounded once to bf16 (one launch)
+            dk_b, dv_b = op.finalize_dkv(dk, dv, staged[0], staged[1], self.ret_row_ptr,
+                                         self.ret_src_rows, cur)
+            final = True
         out = (dq, dk_b, dv_b) if final else (dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur))
         self._mark("bwd_reduce_convert", cur)
         return out
@@ -288,7 +298,7 @@ class FcpExecutor:
         cur = torch.cuda.current_stream(self.device)
         spans = []
         names = ("forward_wave", "merge", "backward_prepare", "backward_launch", "backward_dq",
-                 "reduce_dkv", "to_bf16")
+                 "reduce_dkv", "finalize_dkv", "to_bf16")
         orig = {n: getattr(op, n) for n in names}
 
         def wrap(fn):

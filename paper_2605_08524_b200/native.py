@@ -86,7 +86,7 @@ class DqDsArgs(ctypes.Structure):
 
 EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_dq_ds",
            "fcpb_lse_merge", "fcpb_bwd_preprocess",
-           "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_stream_signal", "fcpb_stream_wait",
+           "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_dkv_finalize", "fcpb_stream_signal", "fcpb_stream_wait",
            "fcpb_last_error", "fcpb_version", "fcpb_device_supported")
 
 _lib = None
@@ -110,6 +110,7 @@ def load(path: str | None = None):
                                          c_i32, c_vp]
     lib.fcpb_f32_to_bf16.argtypes = [c_vp, c_vp, c_i64, c_vp]
     lib.fcpb_dkv_reduce.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp]
+    lib.fcpb_dkv_finalize.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]
     lib.fcpb_stream_signal.argtypes = [c_vp, ctypes.c_uint32, c_vp]
     lib.fcpb_stream_wait.argtypes = [c_vp, ctypes.c_uint32, c_vp]
     lib.fcpb_last_error.restype = ctypes.c_char_p
