@@ -167,3 +167,34 @@ def test_materialised_ds_is_default_when_it_fits():
     r = schedule([1000, 300], 1, 512, GQA_SMALL)
     op = BlockAttention(build_rank_work(r, 0), GQA_SMALL, torch.device("cuda", 0))
     assert op.ds_mode
+
+
+@pytest.mark.gpu
+def test_dkv_finalize_matches_ordered_fp32_sum():
+    """K4 fused finalize through the C ABI: bf16(local + staged partials in CSR order), against
+    the same fp32 sum in the same order on the host side (bit-exact)."""
+    from paper_2605_08524_b200.attention import BlockAttention  # noqa: F401  (loads the lib)
+    from paper_2605_08524_b200 import native
+    lib = native.load()
+    g = torch.Generator().manual_seed(7)
+    T, R, row = 37, 50, 8 * 128
+    local_k, local_v = (torch.randn(T, row, generator=g) for _ in range(2))
+    st_k, st_v = (torch.randn(R, row, generator=g) for _ in range(2))
+    counts = torch.randint(0, 4, (T,), generator=g)
+    row_ptr = torch.zeros(T + 1, dtype=torch.int32)
+    row_ptr[1:] = torch.cumsum(counts, 0).to(torch.int32)
+    src = torch.randint(0, R, (int(row_ptr[-1]),), generator=g, dtype=torch.int32)
+    ref_k, ref_v = local_k.clone(), local_v.clone()
+    for r in range(T):
+        for j in range(int(row_ptr[r]), int(row_ptr[r + 1])):
+            ref_k[r] += st_k[src[j]]
+            ref_v[r] += st_v[src[j]]
+    dev = torch.device("cuda", 0)
+    d = [x.to(dev) for x in (local_k, local_v, st_k, st_v, row_ptr, src)]
+    out_k = torch.empty(T, row, dtype=torch.bfloat16, device=dev)
+    out_v = torch.empty_like(out_k)
+    native.check(lib.fcpb_dkv_finalize(*(x.data_ptr() for x in d), T, row, out_k.data_ptr(),
+                                       out_v.data_ptr(), 0))
+    torch.cuda.synchronize()
+    assert torch.equal(out_k.cpu(), ref_k.to(torch.bfloat16))
+    assert torch.equal(out_v.cpu(), ref_v.to(torch.bfloat16))
