@@ -329,7 +329,11 @@ def main():
     ap.add_argument("--scheduler", default="fcp", choices=["fcp", "ring", "bytescale"],
                     help="plan to execute (ring / bytescale: the reference's competitors)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--curve", default="reference", choices=["reference", "b200"],
+    # The reference's planner takes its efficiency curve as an input (costmodel.py:63-127);
+    # on B200 it plans with the curve measured on B200 (costmodel.B200_EFFICIENCY), and the
+    # plans stay pinned to the unmodified reference run with the same anchors
+    # (tests/test_plan_parity.py::test_plan_bit_identical_with_b200_curve).
+    ap.add_argument("--curve", default="b200", choices=["reference", "b200"],
                     help="efficiency curve the LPT placement plans with (costmodel.py)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu", action="store_true")

@@ -46,14 +46,18 @@ def load():
     return pkg
 
 
-def reference_digest(lengths, n, tpw, block, model_kw, mask="causal", coalesce_degree=16):
-    """sha256[:16] of the reference's canonical schedule+plan JSON."""
+def reference_digest(lengths, n, tpw, block, model_kw, mask="causal", coalesce_degree=16,
+                     curve_anchors=None):
+    """sha256[:16] of the reference's canonical schedule+plan JSON.  curve_anchors: an
+    efficiency curve for the reference's EfficiencyCurve (default: its DEFAULT_EFFICIENCY)."""
     ref = load()
     cli = sys.modules[f"{ALIAS}.cli"]
     model = ref.ModelConfig(**model_kw)
     batch = ref.Batch(tuple(ref.Sequence(i, l) for i, l in enumerate(lengths)), n, tpw)
+    curve = ref.DEFAULT_EFFICIENCY if curve_anchors is None else \
+        sys.modules[f"{ALIAS}.costmodel"].EfficiencyCurve(tuple(tuple(a) for a in curve_anchors))
     r = ref.fcp_schedule(batch, n, ref.ShardingConfig(block_size=block, mask=mask), model,
-                         ref.DEFAULT_EFFICIENCY, coalesce_degree=coalesce_degree)
+                         curve, coalesce_degree=coalesce_degree)
     blob = json.dumps([cli.schedule_payload(r, model),
                        cli.plan_payload(r.sub_stage_plan, r.plan.degree)], sort_keys=True)
     return hashlib.sha256(blob.encode()).hexdigest()[:16], r

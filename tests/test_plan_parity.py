@@ -55,3 +55,28 @@ def test_plan_bit_identical(chunk):
     part = CASES[chunk::8]
     bad = [(c["name"], c["sha"], got) for c in part if (got := _run(c)) != c["sha"]]
     assert not bad, bad[:5]
+
+
+GOLDEN_B200 = os.path.join(os.path.dirname(__file__), "golden", "plan_hashes_b200_curve.json")
+
+
+def test_plan_bit_identical_with_b200_curve():
+    """`bench.py --curve b200` plans: the product planner with costmodel.B200_EFFICIENCY
+    against the unmodified reference run with the same anchors (oracle/gen_plan_golden_b200.py)."""
+    from paper_2605_08524_b200 import configs
+    from paper_2605_08524_b200.costmodel import B200_EFFICIENCY
+    g = json.load(open(GOLDEN_B200))
+    assert [list(a) for a in B200_EFFICIENCY.anchors] == g["curve_anchors"], \
+        "B200_EFFICIENCY changed: rerun oracle/gen_plan_golden_b200.py"
+    by_name = {"C2-llama3-8b-64k": lambda n, b: configs.c2_llama8b_64k(n),
+               "C3-long-tail": lambda n, b: configs.c3_long_tail(n),
+               "C4-uniform-128k": lambda n, b: configs.c4_uniform_128k(n)}
+    bad = []
+    for c in g["cases"]:
+        make = by_name.get(c["name"], lambda n, b: configs.c5_block_sweep(n, b))
+        w = make(c["n"], c["block"])
+        r = fcp_schedule(w.batch(), c["n"], ShardingConfig(block_size=w.block_size), w.model,
+                         B200_EFFICIENCY)
+        if plan_digest(r, w.model) != c["sha"]:
+            bad.append((c["name"], c["n"]))
+    assert not bad, bad
