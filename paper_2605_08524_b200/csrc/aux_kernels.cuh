@@ -55,7 +55,13 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
 // rows (256 B of O and of dO each, one uint2 per lane), park the 32 x H results in shared
 // memory, and write every head's 32 tokens as one coalesced 128 B row (a warp-per-row
 // layout wrote one scattered 4 B word per row and ran at half the HBM rate).
-constexpr int kPrepTokens = 32;
+#ifndef FCPB_PREP_TOKENS
+#define FCPB_PREP_TOKENS 32
+#endif
+#ifndef FCPB_PREP_U
+#define FCPB_PREP_U 4
+#endif
+constexpr int kPrepTokens = FCPB_PREP_TOKENS;
 constexpr int kPrepMaxHeads = 64;
 __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                                               const __nv_bfloat16* __restrict__ dout,
@@ -69,7 +75,7 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kPrepTokens;
   const int nt = static_cast<int>(tokens - t0 < kPrepTokens ? tokens - t0 : kPrepTokens);
   const int nrows = nt * heads;
-  constexpr int kU = 4;                     // rows in flight per warp (memory-level parallelism)
+  constexpr int kU = FCPB_PREP_U;           // rows in flight per warp (memory-level parallelism)
   for (int r0 = warp * kU; r0 < nrows; r0 += nwarps * kU) {
     uint2 ov[kU], dv[kU];
 #pragma unroll
@@ -103,9 +109,9 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   }
   __syncthreads();
   for (int h = warp; h < heads; h += nwarps) {
-    if (lane < nt) {
-      delta_t[h * t_pad + t0 + lane] = sd[h][lane];
-      lse2_t[h * t_pad + t0 + lane] = -lse[(t0 + lane) * heads + h] * 1.4426950408889634f;
+    for (int i = lane; i < nt; i += 32) {
+      delta_t[h * t_pad + t0 + i] = sd[h][i];
+      lse2_t[h * t_pad + t0 + i] = -lse[(t0 + i) * heads + h] * 1.4426950408889634f;
     }
   }
 }
