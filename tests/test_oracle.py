@@ -105,6 +105,7 @@ def test_tiled_equals_dense(mask):
     (3, [1100, 513, 300, 129, 128, 127, 40, 1], 256, 1, "fcp"),     # many stages: fusion matters
     (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "ring"),     # relays, unconsumed chunks
     (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "bytescale"),
+    (8, [1500, 900, 513, 300, 129, 128, 127, 40, 9], 256, 16, "fcp"),  # the driver's N=8 run
 ])
 def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fuse):
     """Simulated workers: per-rank work lists + in-process exchange == dense attention,
@@ -164,3 +165,13 @@ def test_worklist_pairs_match_reference_accounting():
         assert tot == batch_token_pairs(lengths, "causal")
         tot_b = sum(b.pairs for w in range(n) for b in build_rank_work(r, w).bwd)
         assert tot_b == tot
+
+
+@pytest.mark.parametrize("curve", ["reference", "b200"])
+def test_bench_c2_plans_at_eight_ranks(curve):
+    """The driver's scaling run goes to N=8: bench's C2 plan and every rank's work list
+    build, and the ranks' tokens partition the batch."""
+    import bench
+    w, r = bench.build_workload("c2", 8, None, "fcp", curve)
+    works = [build_rank_work(r, k) for k in range(8)]
+    assert sum(wk.layout.tokens for wk in works) == sum(s.length for s in w.batch().sequences)
