@@ -48,18 +48,18 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
   if (lane == 0) a.lse[out] = wsum > 0.f ? mu + __logf(wsum) : -INFINITY;
 }
 
-// delta = <dO[row,:], O[row,:]>, lse2 = lse*log2(e) (both head-major [H, t_pad]) and
-// dq_accum[row,:] = 0; one warp per (token, head) row.
 // Backward preprocess: -delta = -rowsum(dO * O) and -lse * log2(e), written head-major
-// [H, t_pad].  A block owns 32 consecutive tokens x all heads: warps stream the (token, head)
-// rows (256 B of O and of dO each, one uint2 per lane), park the 32 x H results in shared
-// memory, and write every head's 32 tokens as one coalesced 128 B row (a warp-per-row
-// layout wrote one scattered 4 B word per row and ran at half the HBM rate).
+// [H, t_pad], and (recompute-dQ mode) dq_accum[row,:] = 0.  A block owns 32 consecutive
+// tokens x all heads: half-warps stream the (token, head) rows (256 B of O and of dO each,
+// 16 B per lane), park the 32 x H results in shared memory, and write every head's 32 tokens
+// as one coalesced 128 B row (a warp-per-row layout wrote one scattered 4 B word per row and
+// ran at half the HBM rate).  C2 size: 170 us, 94% of measured HBM bandwidth (one uint2 per
+// lane, a warp per row: 225 us; scripts/micro/prep_ab.py).
 #ifndef FCPB_PREP_TOKENS
 #define FCPB_PREP_TOKENS 32
 #endif
 #ifndef FCPB_PREP_U
-#define FCPB_PREP_U 4
+#define FCPB_PREP_U 2
 #endif
 constexpr int kPrepTokens = FCPB_PREP_TOKENS;
 constexpr int kPrepMaxHeads = 64;
@@ -75,35 +75,41 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kPrepTokens;
   const int nt = static_cast<int>(tokens - t0 < kPrepTokens ? tokens - t0 : kPrepTokens);
   const int nrows = nt * heads;
-  constexpr int kU = FCPB_PREP_U;           // rows in flight per warp (memory-level parallelism)
-  for (int r0 = warp * kU; r0 < nrows; r0 += nwarps * kU) {
-    uint2 ov[kU], dv[kU];
+  constexpr int kU = FCPB_PREP_U;           // row pairs in flight per warp
+  // The block's rows are contiguous ((t0 + r / H) * H + r % H == t0 * H + r): a half-warp
+  // reads one 256 B row as 16 B per lane, so one warp load covers two rows.
+  const int half = lane >> 4, hl = lane & 15;
+  const int64_t base = t0 * heads;
+  for (int r0 = warp * 2 * kU; r0 < nrows; r0 += nwarps * 2 * kU) {
+    uint4 ov[kU], dv[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int r = r0 + u;
-      const int64_t row = (t0 + r / heads) * heads + r % heads;   // token-major (t, h) row
-      ov[u] = r < nrows ? reinterpret_cast<const uint2*>(o + row * 128)[lane] : make_uint2(0, 0);
-      dv[u] = r < nrows ? reinterpret_cast<const uint2*>(dout + row * 128)[lane] : make_uint2(0, 0);
+      const int r = r0 + 2 * u + half;
+      ov[u] = r < nrows ? reinterpret_cast<const uint4*>(o + (base + r) * 128)[hl] : make_uint4(0, 0, 0, 0);
+      dv[u] = r < nrows ? reinterpret_cast<const uint4*>(dout + (base + r) * 128)[hl] : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const int r = r0 + u;
+      const int r = r0 + 2 * u + half;
       const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov[u]);
       const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[u]);
       float s = 0.f;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float2 a = __bfloat1622float2(o2[i]);
-        const float2 b = __bfloat1622float2(d2[i]);
-        s = fmaf(a.x, b.x, s);
-        s = fmaf(a.y, b.y, s);
+      for (int i = 0; i < 4; ++i) {
+        const float2 x = __bfloat1622float2(o2[i]);
+        const float2 y = __bfloat1622float2(d2[i]);
+        s = fmaf(x.x, y.x, s);
+        s = fmaf(x.y, y.y, s);
       }
 #pragma unroll
-      for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      for (int off = 8; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (r < nrows) {
-        if (lane == 0) sd[r % heads][r / heads] = -s;                   // negated: dP + ndelta
-        const int64_t row = (t0 + r / heads) * heads + r % heads;
-        if (dq) reinterpret_cast<float4*>(dq + row * 128)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (hl == 0) sd[r % heads][r / heads] = -s;
+        if (dq) {
+          float4* row = reinterpret_cast<float4*>(dq + (base + r) * 128);
+          row[hl] = make_float4(0.f, 0.f, 0.f, 0.f);
+          row[hl + 16] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
     }
   }
