@@ -8,15 +8,22 @@
 namespace fcpb {
 namespace aux {
 
-// K3: one warp per (merged token, q-head); lane owns 4 of the 128 head-dim values.
-// lse = logsumexp_s lse_s ; O = sum_s exp(lse_s - lse) O_s   (partials are normalised).
+// K3: one warp per (merged token, kMergeHeads consecutive q-heads); lane owns 4 of the 128
+// head-dim values.  lse = logsumexp_s lse_s ; O = sum_s exp(lse_s - lse) O_s (partials are
+// normalised).  The heads of one token share the group lookup and the partial row offsets,
+// so the warp pays that dependent chain once and keeps kMergeHeads O rows in flight.
+#ifndef FCPB_MERGE_HEADS
+#define FCPB_MERGE_HEADS 2
+#endif
+constexpr int kMergeHeads = FCPB_MERGE_HEADS;
 __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int H = a.num_q_heads;
-  if (w >= a.merged_tokens * H) return;
-  const int tok = static_cast<int>(w / H);
-  const int h = static_cast<int>(w % H);
+  const int hb = (H + kMergeHeads - 1) / kMergeHeads;
+  if (w >= a.merged_tokens * hb) return;
+  const int tok = static_cast<int>(w / hb);
+  const int h0 = static_cast<int>(w % hb) * kMergeHeads;
   int lo = 0, hi = a.num_groups - 1;  // last group with tok_begin <= tok
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -24,28 +31,50 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
   }
   const FcpbMergeGroup g = a.groups[lo];
   const int t = tok - g.tok_begin;
-  float m = -INFINITY;
-  for (int s = g.part_begin; s < g.part_end; ++s)
-    m = fmaxf(m, a.lse_partial[static_cast<int64_t>(a.part_rows[s] + t) * H + h]);
-  const float mu = (m == -INFINITY) ? 0.f : m;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float wsum = 0.f;
+  float m[kMergeHeads];
+#pragma unroll
+  for (int u = 0; u < kMergeHeads; ++u) m[u] = -INFINITY;
   for (int s = g.part_begin; s < g.part_end; ++s) {
-    const int64_t row = static_cast<int64_t>(a.part_rows[s] + t) * H + h;
-    const float wt = __expf(a.lse_partial[row] - mu);
-    const float4 o = reinterpret_cast<const float4*>(a.o_partial + row * 128)[lane];
-    acc.x += wt * o.x; acc.y += wt * o.y; acc.z += wt * o.z; acc.w += wt * o.w;
-    wsum += wt;
+    const int64_t rb = static_cast<int64_t>(a.part_rows[s] + t) * H + h0;
+#pragma unroll
+    for (int u = 0; u < kMergeHeads; ++u)
+      if (h0 + u < H) m[u] = fmaxf(m[u], a.lse_partial[rb + u]);
   }
-  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
-  const int64_t out = static_cast<int64_t>(g.q_off + t) * H + h;
-  __nv_bfloat162 lo2 = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-  __nv_bfloat162 hi2 = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
-  uint2 packed;
-  packed.x = *reinterpret_cast<uint32_t*>(&lo2);
-  packed.y = *reinterpret_cast<uint32_t*>(&hi2);
-  reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) + out * 128)[lane] = packed;
-  if (lane == 0) a.lse[out] = wsum > 0.f ? mu + __logf(wsum) : -INFINITY;
+  float4 acc[kMergeHeads];
+  float wsum[kMergeHeads];
+#pragma unroll
+  for (int u = 0; u < kMergeHeads; ++u) {
+    m[u] = (m[u] == -INFINITY) ? 0.f : m[u];
+    acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    wsum[u] = 0.f;
+  }
+  for (int s = g.part_begin; s < g.part_end; ++s) {
+    const int64_t rb = static_cast<int64_t>(a.part_rows[s] + t) * H + h0;
+    float4 o[kMergeHeads];
+#pragma unroll
+    for (int u = 0; u < kMergeHeads; ++u)
+      o[u] = h0 + u < H ? reinterpret_cast<const float4*>(a.o_partial + (rb + u) * 128)[lane]
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kMergeHeads; ++u) {
+      const float wt = h0 + u < H ? __expf(a.lse_partial[rb + u] - m[u]) : 0.f;
+      acc[u].x += wt * o[u].x; acc[u].y += wt * o[u].y; acc[u].z += wt * o[u].z; acc[u].w += wt * o[u].w;
+      wsum[u] += wt;
+    }
+  }
+  const int64_t ob = static_cast<int64_t>(g.q_off + t) * H + h0;
+#pragma unroll
+  for (int u = 0; u < kMergeHeads; ++u) {
+    if (h0 + u >= H) break;
+    const float inv = wsum[u] > 0.f ? 1.f / wsum[u] : 0.f;
+    __nv_bfloat162 lo2 = __floats2bfloat162_rn(acc[u].x * inv, acc[u].y * inv);
+    __nv_bfloat162 hi2 = __floats2bfloat162_rn(acc[u].z * inv, acc[u].w * inv);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo2);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi2);
+    reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.o) + (ob + u) * 128)[lane] = packed;
+    if (lane == 0) a.lse[ob + u] = wsum[u] > 0.f ? m[u] + __logf(wsum[u]) : -INFINITY;
+  }
 }
 
 // Backward preprocess: -delta = -rowsum(dO * O) and -lse * log2(e), written head-major

@@ -331,7 +331,8 @@ int fcpb_lse_merge(const FcpbMergeArgs* a, void* stream) {
   if (!a) return fail(FCPB_ERR_INVALID, "null args");
   if (a->head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", a->head_dim);
   if (a->num_groups <= 0) return FCPB_OK;
-  const int64_t rows = a->merged_tokens * a->num_q_heads;  // one warp per (token, head)
+  const int64_t rows = a->merged_tokens *   // one warp per (token, kMergeHeads heads)
+                       ((a->num_q_heads + fcpb::aux::kMergeHeads - 1) / fcpb::aux::kMergeHeads);
   const int block = 256;
   const int64_t grid = (rows * 32 + block - 1) / block;
   fcpb::aux::lse_merge_kernel<<<static_cast<unsigned>(grid), block, 0,
