@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 from paper_2605_08524_b200 import configs  # noqa: E402
 from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, batch_token_pairs  # noqa: E402
 from paper_2605_08524_b200.distributor import worker_loads  # noqa: E402
-from paper_2605_08524_b200.pipeline import fcp_schedule  # noqa: E402
+from paper_2605_08524_b200.pipeline import fcp_schedule, plan_digest  # noqa: E402
 from paper_2605_08524_b200.sharding import ShardingConfig  # noqa: E402
 
 METRIC = "CP attention fwd+bwd tokens/sec and MFU at 1/2/4/8 B200 (max over ranks)"
@@ -256,64 +256,116 @@ def e2e_pipelined(ex, host, device, steps, warmup, barrier):
 
 
 # ---------------------------------------------------------------------------- CPU legs
-def cpu_sample(w, result, budget_s=20.0, threads=None):
-    """Oracle fp32 fwd+bwd (torch CPU, all host threads) on whole sequences of the
-    workload, growing the sample until ~budget; tokens/s extrapolated by the
-    pair fraction.  Returns (tokens_per_s, info)."""
+def cpu_model() -> str:
+    """The host CPU model (lscpu's 'Model name'), recorded next to the CPU numbers."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample_unit(result):
+    """The fixed CPU sample: the schedule unit (zigzag pair) that holds the first and the last
+    chunk of the batch's longest sequence, i.e. its diagonal-only chunk and its chunk with the
+    longest KV list (reference ``sharding.py:84-88,172-201``).  Returns (seq_len, [(q_start,
+    q_len, kv_len, diag_from)], visible pairs)."""
+    from paper_2605_08524_b200.costmodel import tile_token_pairs
+    deps = result.deps
+    seq_len: dict[int, int] = {}
+    for (sid, _), n in deps.chunk_tokens.items():
+        seq_len[sid] = seq_len.get(sid, 0) + n
+    sid = max(seq_len, key=lambda s_: (seq_len[s_], -s_))
+    unit = next(u for u in result.units if any(m.key == (sid, 0) for m in u.members))
+    starts: dict = {}
+    pos = 0
+    for key in sorted((kk for kk in deps.chunk_tokens if kk[0] == sid), key=lambda kk: kk[1]):
+        starts[key] = pos
+        pos += deps.chunk_tokens[key]
+    parts, pairs = [], 0
+    for m in unit.members:
+        kvs = deps.q_to_kv[m.key]
+        q0, qn = starts[m.key], m.token_count
+        kv_len = sum(deps.chunk_tokens[kv] for kv in kvs)
+        parts.append((q0, qn, kv_len, kv_len - qn))
+        pairs += sum(tile_token_pairs(qn, deps.chunk_tokens[kv], kv == m.key) for kv in kvs)
+    return seq_len[sid], parts, pairs
+
+
+def cpu_sample(w, result, reps=1, threads=None):
+    """Oracle fp32 fwd+bwd (torch CPU, all host threads) of the fixed sample of
+    ``cpu_sample_unit``; tokens/s of the whole batch extrapolated by its pair fraction.
+    The same sample in both CPU legs (this arm's ``cpu_baseline`` and ``--impl reference``).
+    Returns ([tokens/s per rep], info)."""
     sys.path.insert(0, ROOT)
-    from oracle.attention_ref import mono_bwd, mono_fwd
+    from oracle.attention_ref import chunk_fwd_bwd
     threads = threads or os.cpu_count()
     torch.set_num_threads(threads)
     cfg = w.model
-    lengths = list(w.lengths)
-    order = sorted(range(len(lengths)), key=lambda i: lengths[i])
+    L, parts, pairs = cpu_sample_unit(result)
     g = torch.Generator().manual_seed(1234)
+    mk = lambda h: torch.randn((L, h, cfg.head_dim), generator=g).to(torch.bfloat16).float()
+    q, k, v, do = mk(cfg.q_heads), mk(cfg.kv_heads), mk(cfg.kv_heads), mk(cfg.q_heads)
     scale = 1.0 / math.sqrt(cfg.head_dim)
-    done_pairs, spent, used = 0, 0.0, []
-    for i in order[len(order) // 2:] + order[:len(order) // 2]:
-        L = lengths[i]
-        if spent > budget_s:
-            break
-        mk = lambda h: torch.randn((L, h, cfg.head_dim), generator=g).to(torch.bfloat16).float()
-        q, k, v, do = mk(cfg.q_heads), mk(cfg.kv_heads), mk(cfg.kv_heads), mk(cfg.q_heads)
-        rows = {0: torch.arange(L)}
+    total_pairs = batch_token_pairs(list(w.lengths), "causal")
+    vals = []
+    for _ in range(reps):
         t0 = time.perf_counter()
-        o, lse = mono_fwd(q, k, v, rows, scale, True, torch.float32)
-        mono_bwd(q, k, v, o, lse, do, rows, scale, True, torch.float32)
-        spent += time.perf_counter() - t0
-        done_pairs += L * (L + 1) // 2
-        used.append(L)
-    total_pairs = batch_token_pairs(lengths, "causal")
-    t_batch = spent * total_pairs / done_pairs
-    return sum(lengths) / t_batch, {"cores": threads, "sample_seqs": used, "sample_s": round(spent, 2),
-                                    "pair_fraction": done_pairs / total_pairs}
+        for q0, qn, kv_len, diag_from in parts:
+            chunk_fwd_bwd(q, k, v, do, torch.arange(q0, q0 + qn), torch.arange(kv_len), diag_from, scale)
+        dt = time.perf_counter() - t0
+        vals.append(w.total_tokens / (dt * total_pairs / pairs))
+    info = {"cores": threads, "cpu_model": cpu_model(), "pair_fraction": pairs / total_pairs,
+            "sample": (f"oracle fp32 fwd+bwd (torch CPU, {threads} threads) of the zigzag unit holding "
+                       f"the first and last chunk of the longest sequence (L={L}: Q chunks "
+                       f"{[(p[1], p[2]) for p in parts]} as (q rows, kv rows)) = {pairs} visible pairs, "
+                       f"{pairs / total_pairs:.4f} of the batch's; tokens/s extrapolated by pair count")}
+    return vals, info
+
+
+def workload_config(w, n, scheduler="fcp"):
+    """The `config` dict both arms print (identical keys and values)."""
+    return {"workload": w.name, "global_batch_tokens": w.total_tokens, "sequences": len(w.lengths),
+            "block": w.block_size, "q_heads": w.model.q_heads, "kv_heads": w.model.kv_heads,
+            "head_dim": w.model.head_dim, "parallelism": f"{scheduler}{n}",
+            "l2": "inputs larger than L2 (no flush needed)"}
+
+
+def reference_control_plane(w, n):
+    """The reference's own fcp_schedule (unmodified, baseline/_ref) on 1 core."""
+    sys.path.insert(0, ROOT)
+    from oracle import ref_control_plane
+    m = w.model
+    return ref_control_plane.run(w.lengths, n, w.tokens_per_worker, w.block_size,
+                                 dict(q_heads=m.q_heads, kv_heads=m.kv_heads, head_dim=m.head_dim,
+                                      dtype_bytes=m.dtype_bytes))
 
 
 def run_reference(args):
-    """--impl reference: the reference path's CPU implementation (the oracle port:
-    the reference has no attention code) on the same workload, all host threads."""
+    """--impl reference: the reference path's CPU implementation on the box's host cores.
+    The reference has no attention code, so the attention math is the oracle port
+    (fp32, all host threads, the fixed sample of ``cpu_sample_unit`` per step); the reference's
+    own control plane (``fcp_schedule`` from baseline/_ref, 1 core) is timed beside it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     n = args.gpus
     w, result = build_workload(args.config, n, args.block, args.scheduler)
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        v, info = cpu_sample(w, result, budget_s=args.cpu_budget / max(1, args.steps))
-        if i >= args.warmup:
-            vals.append(v)
+    vals, info = cpu_sample(w, result, reps=args.warmup + args.steps)
+    vals = vals[args.warmup:]
     value = sorted(vals)[len(vals) // 2]
+    t_step = w.total_tokens / value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": w.name, "global_batch_tokens": w.total_tokens,
-                       "block": w.block_size, "heads": [w.model.q_heads, w.model.kv_heads],
-                       "head_dim": w.model.head_dim},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong" if args.config in ("c2", "c3") else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(w, n, args.scheduler),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "port",
-                             "sample": f"oracle fp32 fwd+bwd of whole sequences {info['sample_seqs']} "
-                                       f"({info['pair_fraction']:.3f} of the batch's pairs), "
-                                       "extrapolated by pair count"},
+                             "cpu_model": info["cpu_model"], "sample": info["sample"],
+                             "spread": [min(vals), max(vals)]},
+            "reference_control_plane": reference_control_plane(w, n),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -329,13 +381,14 @@ def main():
     ap.add_argument("--scheduler", default="fcp", choices=["fcp", "ring", "bytescale"],
                     help="plan to execute (ring / bytescale: the reference's competitors)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    # The reference's planner takes its efficiency curve as an input (costmodel.py:63-127);
-    # on B200 it plans with the curve measured on B200 (costmodel.B200_EFFICIENCY), and the
-    # plans stay pinned to the unmodified reference run with the same anchors
+    # The reference's planner takes its efficiency curve as an input (costmodel.py:63-127).
+    # The headline plans with the reference's stock DEFAULT_EFFICIENCY; the curve
+    # measured on B200 (costmodel.B200_EFFICIENCY) is a labelled variant, its plans pinned to
+    # the unmodified reference run with the same anchors
     # (tests/test_plan_parity.py::test_plan_bit_identical_with_b200_curve).
-    ap.add_argument("--curve", default="b200", choices=["reference", "b200"],
+    ap.add_argument("--curve", default="reference", choices=["reference", "b200"],
                     help="efficiency curve the LPT placement plans with (costmodel.py)")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -357,14 +410,27 @@ def main():
     from paper_2605_08524_b200.executor import FcpExecutor
 
     peak, peak_sus, hbm, peak_kind = load_peaks()
-    peak_run, peak_run_kind = ((peak_sus, peak_kind + " sustained (kernel timed inside the step loop)")
-                               if peak_sus > 0 else (peak, peak_kind + " burst"))
-    t_plan = time.perf_counter()
     w, result = build_workload(args.config, n, args.block, args.scheduler, args.curve)
-    plan_ms = (time.perf_counter() - t_plan) * 1e3
+    # host control plane (fcp_schedule), median of 5 warm calls -- the same statistic as
+    # the reference's own fcp_schedule timed beside it (oracle/ref_control_plane.py)
+    from paper_2605_08524_b200.costmodel import B200_EFFICIENCY
+    plan_ts = []
+    batch = w.batch()
+    for _ in range(5):
+        t_plan = time.perf_counter()
+        fcp_schedule(batch, n, ShardingConfig(block_size=w.block_size), w.model,
+                     B200_EFFICIENCY if args.curve == "b200" else DEFAULT_EFFICIENCY)
+        plan_ts.append((time.perf_counter() - t_plan) * 1e3)
+    plan_ms = sorted(plan_ts)[2]
     cfg = w.model
     ex = FcpExecutor(result, rank, cfg, device)
     host, (q, k, v, do) = rank_inputs(ex, rank, cfg, device, pin=not args.no_e2e)
+    # K/V live in the executor's input buffers (at N > 1 the exchange region's K/V planes,
+    # which the peers read in place: no per-step publish copy)
+    kb, vb = ex.kv_input_buffers()
+    kb.copy_(k)
+    vb.copy_(v)
+    k, v = kb, vb
     stream = torch.cuda.current_stream(device)
 
     # kernel-level events (on the launching stream) for the roofline
@@ -423,6 +489,20 @@ def main():
         barrier()
     launches = ex.op.launches - launches0
     ms = start.elapsed_time(end) / args.steps
+    # Energy per step: the NVML energy counter needs a window of about a second, so it is read
+    # over a separate untimed loop of at least 1.5 s (the timed region may be shorter).
+    energy = None
+    e_steps = max(args.steps, int(math.ceil(1500.0 / max(ms, 1e-3))))
+    with ClockSampler(local) as eclk:
+        torch.cuda.synchronize()
+        for _ in range(e_steps):
+            ex.step(q, k, v, do)
+        torch.cuda.synchronize()
+    if eclk.energy_mj is not None and eclk.energy_mj > 0:
+        energy = {"j_per_step": round(eclk.energy_mj / 1e3 / e_steps, 3),
+                  "power_w_avg": round(eclk.energy_mj / (e_steps * ms), 1), "steps": e_steps,
+                  "window_s": round(e_steps * ms / 1e3, 2),
+                  "how": "NVML total-energy counter over a separate untimed loop of >= 1.5 s"}
     # per-kernel share (separate pass so the kernel events do not perturb the step time)
     timing["on"] = True
     for _ in range(min(3, args.steps)):
@@ -521,30 +601,45 @@ def main():
         top = max(kms, key=lambda kk: kms[kk])
         names = {"fwd": "attn_fwd_kernel", "bwd": "attn_bwd_kernel",
                  "dq": "attn_dqg_kernel" if ds_mode else "attn_dq_kernel"}
+        # Algorithmic bytes of the dominant kernel per launch set (reference accounting,
+        # DESIGN §5): operands read once and results written once, plus the bf16 dS^T tiles
+        # the dK/dV kernel stores (and K2c reads) in materialised-dS mode.
+        T_r, R_r = ex.layout.tokens, ex.layout.recv_tokens
+        H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
+        ds_bytes = (ex.op.ds_bytes if ds_mode else 0)
+        alg_bytes = {"fwd": T_r * H * D * 2 * 2 + (T_r + R_r) * Hk * D * 2 * 2 + T_r * H * 4,
+                     "bwd": T_r * H * D * 2 * 2 + (T_r + R_r) * Hk * D * 2 * 2 * 2 + T_r * H * 8 + ds_bytes,
+                     "dq": T_r * H * D * 2 + (T_r + R_r) * Hk * D * 2 + ds_bytes}
+        traffic = measured_traffic(names[top])
+        per_launch = alg_bytes[top] / max(nl[top], 1)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong" if args.config in ("c2", "c3") else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name, "global_batch_tokens": w.total_tokens,
-                       "sequences": len(w.lengths), "block": w.block_size,
-                       "q_heads": cfg.q_heads, "kv_heads": cfg.kv_heads, "head_dim": cfg.head_dim,
-                       "parallelism": f"{args.scheduler}{n}", "l2": "inputs larger than L2 (no flush needed)",
-                       "plan_ms_host": round(plan_ms, 2), "efficiency_curve": args.curve},
+            "config": workload_config(w, n, args.scheduler),
+            "plan": {"efficiency_curve": args.curve, "plan_ms_host": round(plan_ms, 2),
+                     "digest": plan_digest(result, cfg)},
             "mfu": mfu, "flop_total": flop_total,
-            # The kernels are timed inside the step loop (back-to-back steps under the 1 kW
-            # cap), so the denominator is the sustained bf16 figure; the burst one is beside it.
+            # The kernels are timed on their launching stream inside a 3-step pass; the step is
+            # tens of ms, so the denominator is the measured burst bf16 peak (the sustained
+            # figure applies to seconds-long regions and is shown beside it only).
             "roofline": {"bound": "tensor", "kernel": names[top],
-                         "achieved": ktf[top], "peak": peak_run / 1e12, "unit": "TFLOP/s",
-                         "frac": ktf[top] * 1e12 / peak_run, "peak_kind": peak_run_kind,
-                         "peak_burst": peak / 1e12, "frac_of_burst": ktf[top] * 1e12 / peak,
-                         "traffic": measured_traffic(names[top]),
+                         "achieved": ktf[top], "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": ktf[top] * 1e12 / peak, "peak_kind": peak_kind + " burst (MEASURED_PEAKS.json bf16_tflops)",
+                         "peak_sustained": peak_sus / 1e12 if peak_sus else None,
+                         "traffic": (traffic["bytes_per_launch"] if traffic else None),
+                         "traffic_source": (traffic["source"] if traffic else None),
+                         "algorithmic_bytes": per_launch,
+                         "traffic_over_algorithmic": (traffic["bytes_per_launch"] / per_launch
+                                                      if traffic and per_launch else None),
                          "per_unit": "4*Hq*D FLOP per visible (q,kv) pair (fwd); bwd 2.5x split "
                                      "4/5 dK/dV, 1/5 dQ GEMM (materialised dS) or 4/7, 3/7 "
                                      "(recompute dQ); units = rank-0 visible pairs"},
             "ds_mode": ds_mode,
             "kernels": {names[key]: {"ms": kms[key], "tflops": ktf[key], "frac": ktf[key] * 1e12 / peak,
-                                     "launches": nl[key]} for key in kms},
+                                     "launches": nl[key], "algorithmic_bytes": alg_bytes[key]}
+                        for key in kms},
             "bwd_total": {"ms": bwd_ms, "tflops": bwd_tflops, "frac": bwd_tflops * 1e12 / peak},
             "exchange_bytes_rank0": exb,
             "exchange_bw_rank0": xbw,
@@ -552,18 +647,19 @@ def main():
             "phases_ms_rank0": {kk: round(vv, 3) for kk, vv in phases.items()},
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,
-            "clocks": dict(clocks.summary(), **({} if clocks.energy_mj is None else {
-                "power_w_avg": round(clocks.energy_mj / (args.steps * ms) , 1)})),
-            "energy_j_per_step": (None if clocks.energy_mj is None
-                                  else round(clocks.energy_mj / 1e3 / args.steps, 3)),
+            "clocks": clocks.summary(),
+            "energy": energy,
             "e2e": e2e,
         }
         if not args.no_cpu and n == 1:
-            cv, info = cpu_sample(w, result, budget_s=args.cpu_budget)
+            vals, info = cpu_sample(w, result, reps=args.cpu_reps)
+            cv = sorted(vals)[len(vals) // 2]
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": info["cores"], "kind": "port",
-                                    "sample": f"oracle fp32 fwd+bwd (torch CPU) of whole sequences "
-                                              f"{info['sample_seqs']} = {info['pair_fraction']:.3f} of the "
-                                              f"batch's pairs in {info['sample_s']} s, extrapolated"}
+                                    "cpu_model": info["cpu_model"], "sample": info["sample"],
+                                    "spread": [min(vals), max(vals)]}
+            line["reference_control_plane"] = dict(reference_control_plane(w, n),
+                                                   ours_ms=round(plan_ms, 2),
+                                                   ours_digest=line["plan"]["digest"])
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -17,7 +17,8 @@
  *    bf16 unless noted; LSE is fp32 [T, Hq], natural log; softmax scale given.
  *  - q-head h uses kv-head h / (Hq/Hkv)  (GQA; the reference leaves this open).
  *  - Every pointer is a device pointer owned by the caller; the library
- *    allocates nothing and never synchronises; `stream` is a cudaStream_t.
+ *    allocates nothing (except the fcpb_ipc_* transport regions) and never
+ *    synchronises on the compute path; `stream` is a cudaStream_t.
  *  - Returns 0 (FCPB_OK) or a negative fcpb_status; fcpb_last_error() gives the
  *    message (thread-local).  Python maps these onto ParameterError / NativeError.
  *  - sm_100a only (B200).  D = 128, Hq/Hkv even for the tcgen05 kernels.
@@ -221,6 +222,37 @@ FCPB_API int fcpb_dkv_finalize(const float* local_k, const float* local_v, const
  * (the reference models this ordering as stage boundaries, simulator.py:136-151). */
 FCPB_API int fcpb_stream_signal(void* flag, uint32_t value, void* stream);
 FCPB_API int fcpb_stream_wait(const void* flag, uint32_t value, void* stream);
+
+/* Peer-memory regions for the K5 KV exchange and the K6 dK/dV return (the one place the
+ * library allocates, on behalf of the transport): device memory with a CUDA IPC handle that
+ * the other ranks (processes) open and copy from with copy-engine memcpys.  Works across the
+ * GPUs of one NVSwitch box and between processes that share one GPU.  The reference models
+ * this transport only analytically (simulator.py:136-151). */
+typedef struct { char reserved[64]; } FcpbIpcHandle;
+FCPB_API int fcpb_ipc_alloc(int device, size_t bytes, void** ptr, FcpbIpcHandle* handle);
+FCPB_API int fcpb_ipc_open(int device, const FcpbIpcHandle* handle, void** ptr);
+FCPB_API int fcpb_ipc_close(int device, void* ptr);
+FCPB_API int fcpb_ipc_free(int device, void* ptr);
+/* One copy-engine transfer of `height` rows of `width` bytes (pitches in bytes), ordered on
+ * `stream`: a run of K rows and the matching V rows (two planes of one region) move as one
+ * 2-D copy instead of two. */
+FCPB_API int fcpb_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                          size_t height, void* stream);
+
+/* Workspace queries: bytes the caller provides for
+ *  - the backward preprocess outputs lse2_t + delta_t ([Hq, t_pad] fp32 each, t_pad = T
+ *    rounded up to 4);
+ *  - the forward partials o_partial [P, Hq, D] fp32 + lse_partial [P, Hq] fp32 of the Q
+ *    chunks whose KV list spans several exchange stages (merged by fcpb_lse_merge);
+ *  - the materialised-dS tiles (bf16 128x128 per (KV block, Q block, q-head) pair) that
+ *    fcpb_attn_bwd writes and fcpb_attn_bwd_dq_ds reads. */
+FCPB_API size_t fcpb_bwd_preprocess_bytes(int64_t tokens, int32_t num_q_heads);
+FCPB_API size_t fcpb_fwd_partial_bytes(int64_t partial_rows, int32_t num_q_heads, int32_t head_dim);
+FCPB_API size_t fcpb_ds_tile_bytes(int64_t ds_pairs, int32_t num_q_heads);
+
+/* Test hook: out[0] = warp-level lazy O-rescale events of fcpb_attn_fwd since the last
+ * reset (synchronous; not for the hot path). */
+FCPB_API int fcpb_debug_counters(uint64_t* out, int n, int reset);
 
 FCPB_API const char* fcpb_last_error(void);
 FCPB_API int fcpb_version(void);

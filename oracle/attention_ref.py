@@ -128,6 +128,42 @@ def mono_bwd(q, k, v, o, lse, do, rows, scale, causal=True, dtype=torch.float64)
     return dq, dk, dv
 
 
+def chunk_fwd_bwd(q, k, v, do, q_rows, kv_rows, diag_from, scale, dtype=torch.float32):
+    """One Q chunk's whole fwd+bwd against its concatenated KV list, head by head (the CPU
+    timing sample of ``bench.py``; the reference's unit of work is a Q chunk with its
+    ``q_to_kv`` list, ``sharding.py:172-201``).  ``q_rows``/``kv_rows``: row indices into the
+    packed buffers; the last ``len(kv_rows) - diag_from`` KV rows are the diagonal chunk
+    (inclusive causal mask ``j <= i``, ``costmodel.py:141-149``), the ones before it are fully
+    visible.  Returns (O, LSE, dQ, dK_part, dV_part) for those rows."""
+    H, Hk = q.shape[1], k.shape[1]
+    group = H // Hk
+    qn, kn = q_rows.numel(), kv_rows.numel()
+    keep = torch.ones(qn, kn, dtype=torch.bool)
+    keep[:, diag_from:] = torch.ones(qn, kn - diag_from, dtype=torch.bool).tril()
+    D = q.shape[2]
+    o = torch.empty((qn, H, D), dtype=dtype)
+    lse = torch.empty((qn, H), dtype=dtype)
+    dq = torch.empty((qn, H, D), dtype=dtype)
+    dk = torch.zeros((kn, Hk, D), dtype=dtype)
+    dv = torch.zeros((kn, Hk, D), dtype=dtype)
+    for h in range(H):
+        kh = h // group
+        qs, dos = q[q_rows, h].to(dtype), do[q_rows, h].to(dtype)
+        ks, vs = k[kv_rows, kh].to(dtype), v[kv_rows, kh].to(dtype)
+        s = (torch.matmul(qs, ks.T) * scale).masked_fill(~keep, -math.inf)
+        m = s.amax(dim=-1, keepdim=True)
+        p = torch.exp(s - m)
+        l = p.sum(dim=-1, keepdim=True)
+        p = p / l
+        oh = torch.matmul(p, vs)
+        o[:, h], lse[:, h] = oh, (m + torch.log(l)).squeeze(-1)
+        ds = p * (torch.matmul(dos, vs.T) - (dos * oh).sum(-1, keepdim=True))
+        dq[:, h] = torch.matmul(ds, ks) * scale
+        dk[:, kh] += torch.matmul(ds.T, qs) * scale
+        dv[:, kh] += torch.matmul(p.T, dos)
+    return o, lse, dq, dk, dv
+
+
 # ---------------------------------------------------------------------------- level 2: tiles
 def tiled_fwd(q, k, v, deps, offset, scale, dtype=torch.float64):
     """Attention evaluated tile by tile over ``deps.q_to_kv`` with an LSE merge."""

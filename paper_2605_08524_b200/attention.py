@@ -77,11 +77,12 @@ class BlockAttention:
         # grouped GEMM over them (attn_dqg_sm100.cuh) instead of recomputing S, dP and the
         # softmax.  Used when the tiles fit the budget (FCPB_DS=0/1 forces, FCPB_DS_BUDGET_GB).
         import os as _os
-        ds_bytes = work.ds_pairs * cfg.q_heads * 128 * 128 * 2
+        ds_bytes = self.lib.fcpb_ds_tile_bytes(work.ds_pairs, cfg.q_heads)   # workspace query
         budget = float(_os.environ.get("FCPB_DS_BUDGET_GB", min(40.0, props.total_memory / 4 / 1e9))) * 1e9
         force = _os.environ.get("FCPB_DS")
         self.ds_mode = (force == "1") if force is not None else (0 < ds_bytes <= budget)
         self._ds = None
+        self.ds_bytes = ds_bytes if self.ds_mode else 0
         if self.ds_mode:
             self._ds_pairs_base = [_dev_i32(b.pair_base, dev) for b in work.bwd]
             self._dq_pairs = (_dev_i32(work.dq.pair_ids, dev), _dev_i32(work.dq.pair_off, dev))

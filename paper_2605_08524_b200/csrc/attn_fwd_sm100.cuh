@@ -35,6 +35,12 @@ __device__ unsigned long long g_trace[kFwEvents * kTraceTiles];
 #define FCPB_FWTR(ev, j) do {} while (0)
 #endif
 
+// Test hook: warp-level O-rescale events of the lazy (thresholded) softmax rescale, read
+// through fcpb_debug_counters() so parity tests can prove the rescale path ran.  The branch
+// is rare in practice (the row max must grow by > 2^8 in the exp2 domain), so the atomic is
+// off the hot path.
+__device__ unsigned long long g_rescales;
+
 constexpr int kD = 128;          // head dim
 constexpr int kBM = 128;         // query rows per tile
 constexpr int kBN = 128;         // kv rows per tile
@@ -396,6 +402,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.
           if (!first && __any_sync(0xffffffffu, alpha != 1.f)) {
             // O_h(j-1) is final here: S_h(j) completed after PV_h(j-1) in the tensor pipe.
+            if (lane_id() == 0) atomicAdd(&g_rescales, 1ull);
 #pragma unroll
             for (int c = 0; c < kD / 32; ++c) {
               uint32_t v[32];

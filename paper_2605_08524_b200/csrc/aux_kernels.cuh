@@ -79,11 +79,12 @@ __global__ void __launch_bounds__(256) lse_merge_kernel(const FcpbMergeArgs a) {
 
 // Backward preprocess: -delta = -rowsum(dO * O) and -lse * log2(e), written head-major
 // [H, t_pad], and (recompute-dQ mode) dq_accum[row,:] = 0.  A block owns 32 consecutive
-// tokens x all heads: half-warps stream the (token, head) rows (256 B of O and of dO each,
-// 16 B per lane), park the 32 x H results in shared memory, and write every head's 32 tokens
-// as one coalesced 128 B row (a warp-per-row layout wrote one scattered 4 B word per row and
-// ran at half the HBM rate).  C2 size: 170 us, 94% of measured HBM bandwidth (one uint2 per
-// lane, a warp per row: 225 us; scripts/micro/prep_ab.py).
+// tokens x up to kPrepMaxHeads heads (blockIdx.y picks the head group, so any Hq works):
+// half-warps stream the (token, head) rows (256 B of O and of dO each, 16 B per lane), park
+// the 32 x heads results in shared memory, and write every head's 32 tokens as one coalesced
+// 128 B row (a warp-per-row layout wrote one scattered 4 B word per row and ran at half the
+// HBM rate).  C2 size: 170 us, 94% of measured HBM bandwidth (one uint2 per lane, a warp per
+// row: 225 us; scripts/micro/prep_ab.py).
 #ifndef FCPB_PREP_TOKENS
 #define FCPB_PREP_TOKENS 32
 #endif
@@ -103,19 +104,24 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kPrepTokens;
   const int nt = static_cast<int>(tokens - t0 < kPrepTokens ? tokens - t0 : kPrepTokens);
-  const int nrows = nt * heads;
+  const int h0 = blockIdx.y * kPrepMaxHeads;
+  const int hc = heads - h0 < kPrepMaxHeads ? heads - h0 : kPrepMaxHeads;   // heads of this block
+  const int nrows = nt * hc;
   constexpr int kU = FCPB_PREP_U;           // row pairs in flight per warp
-  // The block's rows are contiguous ((t0 + r / H) * H + r % H == t0 * H + r): a half-warp
-  // reads one 256 B row as 16 B per lane, so one warp load covers two rows.
+  // Row r of the block is (token t0 + r / hc, head h0 + r % hc); with hc == heads the rows
+  // are contiguous.  A half-warp reads one 256 B row as 16 B per lane, so one warp load
+  // covers two rows.
   const int half = lane >> 4, hl = lane & 15;
-  const int64_t base = t0 * heads;
+  auto row_of = [&](int r) -> int64_t {
+    return (t0 + r / hc) * heads + h0 + r % hc;
+  };
   for (int r0 = warp * 2 * kU; r0 < nrows; r0 += nwarps * 2 * kU) {
     uint4 ov[kU], dv[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int r = r0 + 2 * u + half;
-      ov[u] = r < nrows ? reinterpret_cast<const uint4*>(o + (base + r) * 128)[hl] : make_uint4(0, 0, 0, 0);
-      dv[u] = r < nrows ? reinterpret_cast<const uint4*>(dout + (base + r) * 128)[hl] : make_uint4(0, 0, 0, 0);
+      ov[u] = r < nrows ? reinterpret_cast<const uint4*>(o + row_of(r) * 128)[hl] : make_uint4(0, 0, 0, 0);
+      dv[u] = r < nrows ? reinterpret_cast<const uint4*>(dout + row_of(r) * 128)[hl] : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
@@ -133,9 +139,9 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
 #pragma unroll
       for (int off = 8; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
       if (r < nrows) {
-        if (hl == 0) sd[r % heads][r / heads] = -s;
+        if (hl == 0) sd[r % hc][r / hc] = -s;
         if (dq) {
-          float4* row = reinterpret_cast<float4*>(dq + (base + r) * 128);
+          float4* row = reinterpret_cast<float4*>(dq + row_of(r) * 128);
           row[hl] = make_float4(0.f, 0.f, 0.f, 0.f);
           row[hl + 16] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -143,10 +149,10 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(const __nv_bfloat16
     }
   }
   __syncthreads();
-  for (int h = warp; h < heads; h += nwarps) {
+  for (int h = warp; h < hc; h += nwarps) {
     for (int i = lane; i < nt; i += 32) {
-      delta_t[h * t_pad + t0 + i] = sd[h][i];
-      lse2_t[h * t_pad + t0 + i] = -lse[(t0 + i) * heads + h] * 1.4426950408889634f;
+      delta_t[(h0 + h) * t_pad + t0 + i] = sd[h][i];
+      lse2_t[(h0 + h) * t_pad + t0 + i] = -lse[(t0 + i) * heads + h0 + h] * 1.4426950408889634f;
     }
   }
 }

@@ -2,6 +2,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -92,6 +93,21 @@ static_assert(kDqSmem <= 232448, "dq smem budget");
 static_assert(kFwdSmem <= 232448, "fwd smem budget");
 static_assert(kBwdSmem <= 232448, "bwd smem budget");
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per device (context): remember, per kernel,
+// the devices it has been set on (bit d), so a process that drives several GPUs sets it on
+// each.  Racing threads at worst both set it, which is harmless.
+int ensure_smem(const void* kernel, size_t bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  FCPB_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = dev < 64 ? (uint64_t{1} << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return FCPB_OK;
+  FCPB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.fetch_or(bit, std::memory_order_release);
+  return FCPB_OK;
+}
+
+std::atomic<uint64_t> g_attr_fwd{0}, g_attr_bwd{0}, g_attr_dq{0}, g_attr_dqg{0};
+
 }  // namespace
 
 extern "C" {
@@ -145,12 +161,8 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
-  static bool attr = false;
-  if (!attr) {
-    FCPB_CUDA(cudaFuncSetAttribute(fcpb::fwd::attn_fwd_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem));
-    attr = true;
-  }
+  if ((rc = ensure_smem(reinterpret_cast<const void*>(&fcpb::fwd::attn_fwd_kernel), kFwdSmem, g_attr_fwd)))
+    return rc;
   const int total = a->num_items * (a->num_q_heads / 2);
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
@@ -209,12 +221,8 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
-  static bool attr = false;
-  if (!attr) {
-    FCPB_CUDA(cudaFuncSetAttribute(fcpb::bwd::attn_bwd_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBwdSmem));
-    attr = true;
-  }
+  if ((rc = ensure_smem(reinterpret_cast<const void*>(&fcpb::bwd::attn_bwd_kernel), kBwdSmem, g_attr_bwd)))
+    return rc;
   const int total = a->num_items * Hk;
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
@@ -264,12 +272,8 @@ int fcpb_attn_bwd_dq(const FcpbDqArgs* a, void* stream) {
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
-  static bool attr = false;
-  if (!attr) {
-    FCPB_CUDA(cudaFuncSetAttribute(fcpb::dq::attn_dq_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqSmem));
-    attr = true;
-  }
+  if ((rc = ensure_smem(reinterpret_cast<const void*>(&fcpb::dq::attn_dq_kernel), kDqSmem, g_attr_dq)))
+    return rc;
   const int total = a->num_items * H;
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
@@ -312,12 +316,8 @@ int fcpb_attn_bwd_dq_ds(const FcpbDqDsArgs* a, void* stream) {
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
-  static bool attr = false;
-  if (!attr) {
-    FCPB_CUDA(cudaFuncSetAttribute(fcpb::dqg::attn_dqg_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDqgSmem));
-    attr = true;
-  }
+  if ((rc = ensure_smem(reinterpret_cast<const void*>(&fcpb::dqg::attn_dqg_kernel), kDqgSmem, g_attr_dqg)))
+    return rc;
   const int total = a->num_items * H;
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
@@ -346,12 +346,12 @@ int fcpb_bwd_preprocess(const void* o, const void* dout, const float* lse, float
                         int32_t num_q_heads, int32_t head_dim, void* stream) {
   if (head_dim != 128) return fail(FCPB_ERR_UNSUPPORTED, "head_dim %d", head_dim);
   if (t_pad < tokens || t_pad % 4) return fail(FCPB_ERR_INVALID, "bad t_pad %lld", (long long)t_pad);
-  if (num_q_heads <= 0 || num_q_heads > fcpb::aux::kPrepMaxHeads)
-    return fail(FCPB_ERR_UNSUPPORTED, "num_q_heads %d (max %d)", num_q_heads, fcpb::aux::kPrepMaxHeads);
+  if (num_q_heads <= 0) return fail(FCPB_ERR_INVALID, "num_q_heads %d", num_q_heads);
   if (tokens == 0) return FCPB_OK;
   const int block = 256;
-  const int64_t grid = (tokens + fcpb::aux::kPrepTokens - 1) / fcpb::aux::kPrepTokens;
-  fcpb::aux::bwd_preprocess_kernel<<<static_cast<unsigned>(grid), block, 0,
+  const dim3 grid(static_cast<unsigned>((tokens + fcpb::aux::kPrepTokens - 1) / fcpb::aux::kPrepTokens),
+                  static_cast<unsigned>((num_q_heads + fcpb::aux::kPrepMaxHeads - 1) / fcpb::aux::kPrepMaxHeads));
+  fcpb::aux::bwd_preprocess_kernel<<<grid, block, 0,
                                      static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse, lse2_t,
       delta_t, t_pad, dq_accum, tokens, num_q_heads);
@@ -443,6 +443,98 @@ int fcpb_dkv_reduce(float* dst, const float* src, const int32_t* dst_rows, int64
       reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(src), dst_rows, n_rows,
       row_elems / 4);
   FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+// ---- peer-memory regions (K5/K6 transport): cudaMalloc + CUDA IPC handles.  Every call
+// names its device explicitly and restores the caller's current device.
+namespace {
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+static_assert(sizeof(FcpbIpcHandle) == sizeof(cudaIpcMemHandle_t), "IPC handle size");
+}  // namespace
+
+int fcpb_ipc_alloc(int device, size_t bytes, void** ptr, FcpbIpcHandle* handle) {
+  if (!ptr || !handle || bytes == 0) return fail(FCPB_ERR_INVALID, "ipc_alloc: null pointer or zero size");
+  DeviceGuard g(device);
+  FCPB_CUDA(g.err);
+  void* p = nullptr;
+  FCPB_CUDA(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return fail(FCPB_ERR_CUDA, "ipc_alloc: %s", cudaGetErrorString(e));
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return FCPB_OK;
+}
+
+int fcpb_ipc_open(int device, const FcpbIpcHandle* handle, void** ptr) {
+  if (!ptr || !handle) return fail(FCPB_ERR_INVALID, "ipc_open: null pointer");
+  DeviceGuard g(device);
+  FCPB_CUDA(g.err);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  FCPB_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return FCPB_OK;
+}
+
+int fcpb_ipc_close(int device, void* ptr) {
+  DeviceGuard g(device);
+  FCPB_CUDA(g.err);
+  FCPB_CUDA(cudaIpcCloseMemHandle(ptr));
+  return FCPB_OK;
+}
+
+int fcpb_ipc_free(int device, void* ptr) {
+  DeviceGuard g(device);
+  FCPB_CUDA(g.err);
+  FCPB_CUDA(cudaFree(ptr));
+  return FCPB_OK;
+}
+
+int fcpb_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                 size_t height, void* stream) {
+  if (width == 0 || height == 0) return FCPB_OK;
+  if (!dst || !src) return fail(FCPB_ERR_INVALID, "copy_2d: null pointer");
+  FCPB_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToDevice,
+                              static_cast<cudaStream_t>(stream)));
+  return FCPB_OK;
+}
+
+size_t fcpb_bwd_preprocess_bytes(int64_t tokens, int32_t num_q_heads) {
+  const int64_t t_pad = (tokens + 3) / 4 * 4;
+  return static_cast<size_t>(2) * num_q_heads * t_pad * sizeof(float);
+}
+
+size_t fcpb_fwd_partial_bytes(int64_t partial_rows, int32_t num_q_heads, int32_t head_dim) {
+  return static_cast<size_t>(partial_rows) * num_q_heads * (static_cast<size_t>(head_dim) + 1) * sizeof(float);
+}
+
+size_t fcpb_ds_tile_bytes(int64_t ds_pairs, int32_t num_q_heads) {
+  return static_cast<size_t>(ds_pairs) * num_q_heads * 128 * 128 * 2;
+}
+
+int fcpb_debug_counters(uint64_t* out, int n, int reset) {
+  unsigned long long v = 0;
+  FCPB_CUDA(cudaMemcpyFromSymbol(&v, fcpb::fwd::g_rescales, sizeof(v)));
+  if (out && n > 0) out[0] = v;
+  if (reset) {
+    const unsigned long long z = 0;
+    FCPB_CUDA(cudaMemcpyToSymbol(fcpb::fwd::g_rescales, &z, sizeof(z)));
+  }
   return FCPB_OK;
 }
 

@@ -1,21 +1,16 @@
-"""K5/K6: execute the coalesced Delta-matching plan as point-to-point transfers.
+"""K5/K6 plan bookkeeping: which rows the coalesced Delta-matching plan moves.
 
-Each coalesced stage of ``ScheduleResult.plan`` (reference ``planner.py:234-248``)
-becomes one grouped send/recv batch: this rank sends every KV chunk it owns on
-an edge ``src == rank`` and receives every chunk on an edge ``dst == rank`` into
-that chunk's receive-arena slot (``worklist.rank_layout``).  Every round of a
-stage is a matching, so within a stage each GPU sends at most ``degree`` and
-receives at most ``degree`` chunks -- over NVSwitch (uniform 900 GB/s per
-direction to every peer) this is the congestion-free schedule the reference
-models with its flat full-duplex NIC (``simulator.py:136-151``).
+Each coalesced stage of ``ScheduleResult.plan`` (reference ``planner.py:234-248``) moves
+every KV chunk on an edge ``dst == rank`` into that chunk's receive-arena slot
+(``worklist.rank_layout``).  Every round of a stage is a matching, so within a stage each
+GPU sends at most ``degree`` and receives at most ``degree`` chunks -- over NVSwitch
+(uniform 900 GB/s per direction to every peer) this is the congestion-free schedule the
+reference models with its flat full-duplex NIC (``simulator.py:136-151``).
 
-The backward return (K6) walks the same edges reversed: the receiver sends the
-chunk's dK/dV partial back to the owner, which adds it with K4.
-
-The transport is ``torch.distributed`` P2P (NCCL on GPUs; gloo in the CPU tests),
-issued on a dedicated communication stream and ordered against compute with
-CUDA events; the ops only describe *which rows* move, so the same plan object
-drives both backends.
+The backward return (K6) walks the same edges reversed: the consumer's dK/dV partial of a
+chunk goes back to the owner, which adds it with K4.  ``owner_returns`` and
+``return_staging_layout`` describe that traffic; ``p2p.py`` turns both directions into
+copy-engine pulls.
 """
 
 from __future__ import annotations
@@ -69,26 +64,6 @@ def build_stage_ops(result: ScheduleResult, lay: RankLayout, all_layouts=None) -
     return out
 
 
-def _p2p(ops, group=None):
-    if not ops:
-        return []
-    return dist.batch_isend_irecv(ops)
-
-
-def run_stage(stage: StageOps, send_bufs, recv_bufs, group=None):
-    """Post one stage's grouped sends/recvs.  ``send_bufs``/``recv_bufs`` are
-    lists of [tokens, ...] tensors moved together (e.g. (K, V)); returns works."""
-    ops = []
-    for t in stage.sends:
-        for buf, rbuf in zip(send_bufs, recv_bufs):
-            src = rbuf if t.from_recv else buf
-            ops.append(dist.P2POp(dist.isend, src[t.row:t.row + t.tokens], t.peer, group))
-    for t in stage.recvs:
-        for buf in recv_bufs:
-            ops.append(dist.P2POp(dist.irecv, buf[t.row:t.row + t.tokens], t.peer, group))
-    return _p2p(ops, group)
-
-
 def owner_returns(layouts, owner, rank: int) -> list[Transfer]:
     """K6, owner side: one transfer per (my chunk, rank that consumed it), in consumer rank
     order then that rank's receive order.  ``row`` is the chunk's row in my local buffer,
@@ -102,24 +77,6 @@ def owner_returns(layouts, owner, rank: int) -> list[Transfer]:
             if c in lay.consumed and owner[c] == rank:
                 out.append(Transfer(q, layouts[rank].offset[c], lay.chunk_tokens[c], c))
     return out
-
-
-def run_return(lay, layouts, owner, partial_bufs, staging_bufs, staging_rows, group=None):
-    """Reverse traffic of K6 over torch.distributed P2P: every rank sends the partials of
-    the chunks it consumed but does not own to their owners; owners receive them into
-    ``staging_bufs`` at ``staging_rows[(chunk, consumer)]``."""
-    rank = lay.rank
-    ops = []
-    for c in lay.recv_chunks:               # my partials of foreign chunks
-        if c in lay.consumed and owner[c] != rank:
-            a, n = lay.recv_offset[c], lay.chunk_tokens[c]
-            for buf in partial_bufs:
-                ops.append(dist.P2POp(dist.isend, buf[a:a + n], owner[c], group))
-    for t in owner_returns(layouts, owner, rank):
-        r = staging_rows[(t.chunk, t.peer)]
-        for buf in staging_bufs:
-            ops.append(dist.P2POp(dist.irecv, buf[r:r + t.tokens], t.peer, group))
-    return _p2p(ops, group)
 
 
 def return_staging_layout(returns: list[Transfer]):
@@ -150,11 +107,6 @@ def exchange_bytes(stages: list[StageOps], bytes_per_token: int) -> tuple[int, i
     sent = sum(t.tokens for st in stages for t in st.sends) * bytes_per_token
     got = sum(t.tokens for st in stages for t in st.recvs) * bytes_per_token
     return sent, got
-
-
-def wait_all(works):
-    for w in works:
-        w.wait()
 
 
 def sync_plan_digest(digest: str, group=None) -> None:

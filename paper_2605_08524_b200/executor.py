@@ -14,8 +14,8 @@ backward  compute: preprocess -> K2 dK/dV over *received* KV chunks (partials la
           symmetric memory) -> K2 dK/dV over local KV chunks -> K2b dQ over all resident KV;
           comm:    barrier, then every owner pulls the partials of its chunks back along
           the reversed plan edges (K6) while the local kernels run; K4 adds them.
-Transport: copy-engine pulls from symmetric (IPC-mapped) peer memory (``p2p.py``) --
-no SMs taken from the persistent kernels; measured ~5x faster than NCCL send/recv here.
+Transport: copy-engine pulls from IPC-mapped peer memory (``p2p.py``) -- no SMs taken
+from the persistent kernels; measured ~5x faster than NCCL send/recv here.
 
 Built once per batch from the ``ScheduleResult``; ``step`` can be called for
 every layer.  One process per GPU (torchrun); ``group`` is the NCCL group.
@@ -84,8 +84,10 @@ class FcpExecutor:
         self.wave_of_stage = {self.op.wave_stage(i): i for i in range(self.op.num_waves)}
         H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
         R = self.layout.recv_tokens
-        self.k_recv = torch.empty((R, Hk, D), dtype=torch.bfloat16, device=self.device) if R else None
-        self.v_recv = torch.empty((R, Hk, D), dtype=torch.bfloat16, device=self.device) if R else None
+        # receive arena: K plane then V plane, so one 2-D copy moves a run of both
+        self.kv_recv = torch.empty((2, R, Hk, D), dtype=torch.bfloat16, device=self.device) if R else None
+        self.k_recv = self.kv_recv[0] if R else None
+        self.v_recv = self.kv_recv[1] if R else None
         self.kv_bytes_per_token = 2 * Hk * D * 2
         self._marks = None          # optional per-phase CUDA-event timeline (see timeline())
 
@@ -106,6 +108,19 @@ class FcpExecutor:
         local = sum(w.pairs for w in waves if w.stage == LOCAL_WAVE)
         local_s = local * cfg.flops_per_token_pair / 600e12
         return recv_s <= local_s
+
+    def kv_input_buffers(self):
+        """(k, v) [T, Hkv, D] bf16 buffers to write this rank's K/V into before ``forward``.
+        At N > 1 they are the K/V planes of the exchange region, so the peers read them in
+        place and the step skips the publish copy; at N = 1 plain tensors.  Writes issued on
+        the current stream after this call are ordered after the peers' pulls of the previous
+        step (the comm stream ends each forward with the "K/V consumed" barrier)."""
+        if self.xchg is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.comm)
+            return self.xchg.kv_views()
+        shape = (self.layout.tokens, self.cfg.kv_heads, self.cfg.head_dim)
+        return (torch.empty(shape, dtype=torch.bfloat16, device=self.device),
+                torch.empty(shape, dtype=torch.bfloat16, device=self.device))
 
     # ------------------------------------------------------------------ timeline
     def timeline(self, enabled: bool = True):
@@ -166,7 +181,7 @@ class FcpExecutor:
             with torch.cuda.stream(self.comm):
                 x.barrier("kv", 0)                      # everyone's K/V readable
                 for s_idx in range(len(self.stages)):
-                    x.pull_stage(s_idx, self.k_recv, self.v_recv)
+                    x.pull_stage(s_idx, self.kv_recv)
                     ev = torch.cuda.Event()
                     ev.record(self.comm)
                     events.append(ev)
@@ -202,18 +217,18 @@ class FcpExecutor:
             op.backward_launch(True, *args)
             self._mark("bwd_dkv_recv", cur)
             Hk, D = self.cfg.kv_heads, self.cfg.head_dim
-            sk = torch.empty((self.ret_tokens, Hk, D), dtype=torch.float32, device=self.device)
-            sv = torch.empty_like(sk)
+            staging = torch.empty((2, self.ret_tokens, Hk, D), dtype=torch.float32, device=self.device)
+            sk, sv = staging[0], staging[1]
             self.comm.wait_stream(cur)
             with torch.cuda.stream(self.comm):
                 if x.BARRIER == "kernel":
                     x.barrier("part", 0)                # every rank's partials written
-                    x.pull_returns(self.returns, sk, sv, self.ret_rows)
+                    x.pull_returns(self.returns, staging, self.ret_rows)
                 else:
                     # my partials are written; each owner pulls a consumer's partials as
                     # soon as that consumer has signalled (no wait for the slowest rank)
                     x.signal_all("part", 0)
-                    x.pull_returns(self.returns, sk, sv, self.ret_rows, per_peer_ready=True)
+                    x.pull_returns(self.returns, staging, self.ret_rows, per_peer_ready=True)
                 x.barrier("part", 1)                    # pulled: partial buffers reusable
                 self._mark("comm_return_done", self.comm)
             staged = (sk, sv)
@@ -232,12 +247,15 @@ class FcpExecutor:
         dq = op.backward_dq(q, k, v, self.k_recv, self.v_recv, prep, do, cur)
         self._mark("bwd_dq", cur)
         if staged is not None:
+            # the comm stream's return pulls and barriers order the reuse of the partial
+            # buffers, even on a rank none of whose chunks was consumed remotely
             cur.wait_stream(self.comm)
             self._mark("bwd_wait_return", cur)
-            # K4: local rows + every returned partial, rounded once to bf16 (one launch)
-            dk_b, dv_b = op.finalize_dkv(dk, dv, staged[0], staged[1], self.ret_row_ptr,
-                                         self.ret_src_rows, cur)
-            final = True
+            if not final:
+                # K4: local rows + every returned partial, rounded once to bf16 (one launch)
+                dk_b, dv_b = op.finalize_dkv(dk, dv, staged[0], staged[1], self.ret_row_ptr,
+                                             self.ret_src_rows, cur)
+                final = True
         out = (dq, dk_b, dv_b) if final else (dq, op.to_bf16(dk, cur), op.to_bf16(dv, cur))
         self._mark("bwd_reduce_convert", cur)
         return out
@@ -252,8 +270,7 @@ class FcpExecutor:
         if x is None or not self.stages:
             return None
         Hk, D = self.cfg.kv_heads, self.cfg.head_dim
-        sk = torch.empty((max(self.ret_tokens, 1), Hk, D), dtype=torch.float32, device=self.device)
-        sv = torch.empty_like(sk)
+        staging = torch.empty((2, max(self.ret_tokens, 1), Hk, D), dtype=torch.float32, device=self.device)
         b = self.exchange_bytes()
         out = {}
         for name, nbytes in (("fwd_kv_pull", b["fwd_recv"]), ("bwd_dkv_return", b["bwd_recv"])):
@@ -267,9 +284,9 @@ class FcpExecutor:
                     s0.record(self.comm)
                     if which == "kv":
                         for s_idx in range(len(self.stages)):
-                            x.pull_stage(s_idx, self.k_recv, self.v_recv)
+                            x.pull_stage(s_idx, self.kv_recv)
                     else:
-                        x.pull_returns(self.returns, sk, sv, self.ret_rows)
+                        x.pull_returns(self.returns, staging, self.ret_rows)
                     e0.record(self.comm)
                     x.barrier(which, 1)
                 torch.cuda.synchronize(self.device)
@@ -344,7 +361,7 @@ class FcpExecutor:
                 with torch.cuda.stream(self.comm):
                     self.xchg.barrier("kv", 0)
                     s0.record(self.comm)
-                    self.xchg.pull_stage(s_idx, self.k_recv, self.v_recv)
+                    self.xchg.pull_stage(s_idx, self.kv_recv)
                     e0.record(self.comm)
                     self.xchg.barrier("kv", 1)
                 torch.cuda.synchronize(self.device)

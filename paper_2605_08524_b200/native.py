@@ -87,7 +87,11 @@ class DqDsArgs(ctypes.Structure):
 EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_dq_ds",
            "fcpb_lse_merge", "fcpb_bwd_preprocess",
            "fcpb_f32_to_bf16", "fcpb_dkv_reduce", "fcpb_dkv_finalize", "fcpb_stream_signal", "fcpb_stream_wait",
-           "fcpb_last_error", "fcpb_version", "fcpb_device_supported")
+           "fcpb_last_error", "fcpb_version", "fcpb_device_supported",
+           "fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes",
+           "fcpb_debug_counters", "fcpb_ipc_alloc", "fcpb_ipc_open", "fcpb_ipc_close", "fcpb_ipc_free",
+           "fcpb_copy_2d")
+_SIZE_T = ("fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes")
 
 _lib = None
 
@@ -115,8 +119,19 @@ def load(path: str | None = None):
     lib.fcpb_stream_wait.argtypes = [c_vp, ctypes.c_uint32, c_vp]
     lib.fcpb_last_error.restype = ctypes.c_char_p
     lib.fcpb_device_supported.argtypes = [ctypes.c_int]
+    lib.fcpb_bwd_preprocess_bytes.argtypes = [c_i64, c_i32]
+    lib.fcpb_fwd_partial_bytes.argtypes = [c_i64, c_i32, c_i32]
+    lib.fcpb_ds_tile_bytes.argtypes = [c_i64, c_i32]
+    lib.fcpb_ipc_alloc.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(c_vp), ctypes.c_char_p]
+    lib.fcpb_ipc_open.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(c_vp)]
+    lib.fcpb_ipc_close.argtypes = [ctypes.c_int, c_vp]
+    lib.fcpb_ipc_free.argtypes = [ctypes.c_int, c_vp]
+    lib.fcpb_copy_2d.argtypes = [c_vp, ctypes.c_size_t, c_vp, ctypes.c_size_t, ctypes.c_size_t,
+                                 ctypes.c_size_t, c_vp]
+    lib.fcpb_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:
-        getattr(lib, name).restype = ctypes.c_char_p if name == "fcpb_last_error" else ctypes.c_int
+        getattr(lib, name).restype = (ctypes.c_char_p if name == "fcpb_last_error" else
+                                      ctypes.c_size_t if name in _SIZE_T else ctypes.c_int)
     if path is None:
         _lib = lib
     return lib
@@ -140,6 +155,11 @@ def stream_handle(stream) -> int:
     return stream.cuda_stream if stream is not None else 0
 
 
+def copy_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream) -> None:
+    """Device-to-device 2-D copy on `stream` (one copy-engine operation)."""
+    check(load().fcpb_copy_2d(dst, dpitch, src, spitch, width, height, stream_handle(stream)))
+
+
 def stream_signal(flag_addr: int, value: int, stream) -> None:
     """Write `value` to a (peer-mapped) 32-bit flag after the stream's prior work."""
     check(load().fcpb_stream_signal(flag_addr, value & 0xFFFFFFFF, stream_handle(stream)))
@@ -148,3 +168,11 @@ def stream_signal(flag_addr: int, value: int, stream) -> None:
 def stream_wait(flag_addr: int, value: int, stream) -> None:
     """Later work on `stream` waits until the local 32-bit flag reaches `value`."""
     check(load().fcpb_stream_wait(flag_addr, value & 0xFFFFFFFF, stream_handle(stream)))
+
+
+def fwd_rescale_events(reset: bool = True) -> int:
+    """Test hook (synchronous): warp-level lazy O-rescale events of the forward kernel since
+    the last reset (``fcpb_debug_counters``)."""
+    out = (ctypes.c_uint64 * 1)()
+    check(load().fcpb_debug_counters(out, 1, 1 if reset else 0))
+    return int(out[0])

@@ -1,56 +1,179 @@
-"""K5/K6 transport: copy-engine pulls from symmetric (IPC-mapped) peer memory over NVLink.
+"""K5/K6 transport: copy-engine pulls from peer-mapped memory over NVLink.
 
 Measured on the B200 box: NCCL grouped send/recv moved the FCP stages at ~45 GB/s
 (2 MB messages, and its kernels compete with the persistent attention kernels for
 SMs), while ``cudaMemcpyAsync`` pulls from a peer's mapped buffer reach ~250 GB/s
 per direction for the same 2 MB chunks with *no* SM use.  Per the north star
 ("NCCL grouped send/recv, or in-kernel P2P, whichever measures faster") the executor
-uses the pulls; ``exchange.run_stage`` (torch.distributed P2P) stays as the
-transport-agnostic reference of the same plan that the gloo CPU tests exercise.
+uses the pulls.
 
-Buffers (torch symmetric memory, same size on every rank):
+The plan -> copy lists translation is pure host code (``stage_pulls``, ``return_pulls``),
+tested on CPU against the reference's arrival semantics (``simulator.py:112-133``).
 
-* ``kv``   bf16 [2, T_max, Hkv, D] -- each rank's own K and V (copied in at step start)
+Buffers (one peer-memory region each, the same size on every rank; ``ipc.IpcRegion`` --
+``fcpb_ipc_*`` in the C ABI -- or torch symmetric memory with FCPB_TRANSPORT=symm):
+
+* ``kv``   bf16 [2, T_max, Hkv, D] -- each rank's own K and V planes.  The executor hands
+  these planes out as its K/V input buffers, so writing K/V there costs no publish copy.
 * ``part`` fp32 [2, R_max, Hkv, D] -- dK/dV partials of the chunks a rank *received*
   (written directly by the dK/dV kernel), pulled back by the chunk owners.
+* ``flags`` int32 [4, world] -- readiness words written by the peers' streams
+  (``FlagBarrier``).
 
-* ``flags`` int32 [4, world] -- readiness words written by the peers' streams.
+Every pull of a run of rows moves its K rows and V rows (or dK and dV partial rows) as ONE
+2-D copy (``fcpb_copy_2d``): the two planes of the source region and of the destination
+arena sit at fixed pitches.
 
-Ordering: an all-rank barrier after the K/V copy (everyone's K/V is readable), after
+Ordering: an all-rank barrier after the K/V are in place (everyone's K/V is readable), after
 the forward pulls (K/V may be overwritten next step), after the partials are written,
 and after the return pulls.  The barrier is stream memory operations on the flag words
-(``fcpb_stream_signal`` / ``fcpb_stream_wait``), executed without an SM.  Each plan edge (reference
-``planner.py:81-102``) becomes exactly one pull of K and one of V in its coalesced
-stage; the Delta-matching guarantees each GPU reads from at most ``degree`` peers
-and is read by at most ``degree`` peers per stage.
+(``fcpb_stream_signal`` / ``fcpb_stream_wait``), executed without an SM.  Each plan edge
+(reference ``planner.py:81-102``) becomes exactly one pull in its coalesced stage; the
+Delta-matching guarantees each GPU reads from at most ``degree`` peers and is read by at
+most ``degree`` peers per stage.
 """
 
 from __future__ import annotations
 
 import os
+from typing import NamedTuple
 
 import torch
 import torch.distributed as dist
-import torch.distributed._symmetric_memory as symm
 
 from . import native
 from .distributor import chunk_placement
 from .worklist import rank_layout
 
 
-def _append_merged(pulls, pull):
-    """Append (peer, src, dst, n), coalescing with the previous pull when both ranges
-    continue contiguously on the same peer (fewer, larger copy-engine transfers)."""
+class Pull(NamedTuple):
+    peer: int      # rank whose region is read
+    src: int       # first row in the peer's region plane
+    dst: int       # first row in my destination plane
+    rows: int
+
+
+def _append_merged(pulls: list, pull: Pull) -> None:
+    """Append a pull, coalescing it with the previous one when both ranges continue
+    contiguously on the same peer (fewer, larger copy-engine transfers)."""
     if pulls:
-        pp, ps, pd, pn = pulls[-1]
-        peer, src, dst, n = pull
-        if pp == peer and ps + pn == src and pd + pn == dst:
-            pulls[-1] = (pp, ps, pd, pn + n)
+        last = pulls[-1]
+        if last.peer == pull.peer and last.src + last.rows == pull.src and last.dst + last.rows == pull.dst:
+            pulls[-1] = Pull(last.peer, last.src, last.dst, last.rows + pull.rows)
             return
     pulls.append(pull)
 
 
+def stage_pulls(result, rank: int, layouts=None, owner=None) -> list[list[Pull]]:
+    """K5, per coalesced stage: the pulls that fill this rank's receive arena.  Every chunk
+    that arrives in stage s (``RankLayout.recv_stage``, the reference's arrival stage,
+    ``simulator.py:112-133``) is read from its *owner's* K/V plane, even when the plan's
+    edge comes from a relay (ring / ByteScale): over NVSwitch every peer is one hop away,
+    so a relay edge only fixes when the chunk arrives.  Pure host code."""
+    world = result.assignment.n_workers
+    layouts = layouts or [rank_layout(result, r) for r in range(world)]
+    owner = owner or chunk_placement(result.assignment, result.units)
+    me = layouts[rank]
+    out: list[list[Pull]] = []
+    for s, stage in enumerate(result.plan.stages):
+        pulls: list[Pull] = []
+        for e in stage:
+            if e.dst != rank:
+                continue
+            for c in e.chunks:
+                if me.recv_stage.get(c) == s:
+                    o = owner[c]
+                    _append_merged(pulls, Pull(o, layouts[o].offset[c], me.recv_offset[c], me.chunk_tokens[c]))
+        out.append(pulls)
+    return out
+
+
+def return_pulls(returns, layouts, staging_rows) -> list[Pull]:
+    """K6, owner side: one pull per (my chunk, consuming rank) -- ``exchange.owner_returns``
+    -- from the consumer's partial plane (the chunk's receive-arena row there) into my
+    staging rows ``staging_rows[(chunk, consumer)]``.  Pure host code."""
+    out: list[Pull] = []
+    for t in returns:
+        _append_merged(out, Pull(t.peer, layouts[t.peer].recv_offset[t.chunk],
+                                 staging_rows[(t.chunk, t.peer)], t.tokens))
+    return out
+
+
+# ---------------------------------------------------------------------------- regions
+class _Regions:
+    """One peer-memory buffer per rank: ``local`` (a torch view of mine) and ``peers[p]``
+    (a view of rank p's), through the C-ABI IPC regions or torch symmetric memory."""
+
+    def __init__(self, numel: int, dtype, shape, device, group, backend: str):
+        self.backend = backend
+        self._keep = None
+        if backend == "symm":
+            import torch.distributed._symmetric_memory as symm
+            buf = symm.empty(numel, dtype=dtype, device=device)
+            h = symm.rendezvous(buf, group)
+            world = dist.get_world_size(group)
+            self.local = buf.view(shape)
+            self.peers = [h.get_buffer(p, tuple(shape), dtype) for p in range(world)]
+            self.ptrs = [int(x) for x in h.buffer_ptrs]
+            self._keep = (buf, h)
+        else:
+            from .ipc import IpcRegion
+            esz = torch.empty((), dtype=dtype).element_size()
+            reg = IpcRegion(numel * esz, device)
+            regions = reg.exchange(group)
+            self.local = reg.tensor(dtype, shape)
+            self.peers = [r.tensor(dtype, shape) for r in regions]
+            self.ptrs = [r.ptr for r in regions]
+            self._keep = regions
+
+
+TRANSPORT = os.environ.get("FCPB_TRANSPORT", "ipc")   # "symm": torch symmetric memory (A/B)
+
+
+class FlagBarrier:
+    """All-rank barriers and per-peer readiness signals on int32 flag words in peer memory,
+    executed by the streams' front ends (``fcpb_stream_signal`` / ``fcpb_stream_wait``, i.e.
+    cuStreamWriteValue32 / cuStreamWaitValue32 with monotonically increasing epochs) -- no
+    kernel, so no SM: a barrier kernel cannot become resident while a persistent attention
+    kernel fills every SM's shared memory (K2 uses all 227 KB) and used to wait for whole
+    launches (C3 at N=4: 657 -> 629 ms when these flags replaced it).
+    Flag word [channel][src] of rank r is written by rank src."""
+
+    def __init__(self, channels: int, device, group, backend: str = TRANSPORT):
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = device
+        self.channels = channels
+        reg = _Regions(channels * self.world, torch.int32, (channels * self.world,), device, group, backend)
+        reg.local.zero_()
+        self.base = reg.ptrs
+        self._reg = reg
+        self.epoch = [0] * channels
+
+    def signal_all(self, ch: int, stream=None) -> None:
+        """Open a new epoch on channel ch and tell every peer (after `stream`'s prior work)."""
+        stream = stream or torch.cuda.current_stream(self.device)
+        self.epoch[ch] += 1
+        w, me = self.world, self.rank
+        for p in range(w):
+            if p != me:
+                native.stream_signal(self.base[p] + 4 * (ch * w + me), self.epoch[ch], stream)
+
+    def wait_peer(self, ch: int, peer: int, stream) -> None:
+        """Work queued on `stream` after this waits for peer's signal of the current epoch."""
+        native.stream_wait(self.base[self.rank] + 4 * (ch * self.world + peer), self.epoch[ch], stream)
+
+    def barrier(self, ch: int, stream=None) -> None:
+        stream = stream or torch.cuda.current_stream(self.device)
+        self.signal_all(ch, stream)
+        for p in range(self.world):
+            if p != self.rank:
+                self.wait_peer(ch, p, stream)
+
+
 class SymmetricExchange:
+    TRANSPORT = TRANSPORT
+
     def __init__(self, result, rank: int, cfg, device, group=None, layouts=None):
         self.rank = rank
         self.world = result.assignment.n_workers
@@ -60,23 +183,16 @@ class SymmetricExchange:
         layouts = layouts or [rank_layout(result, r) for r in range(self.world)]
         self.layouts = layouts
         me = layouts[rank]
-        t_max = max(l.tokens for l in layouts)
-        r_max = max(max(l.recv_tokens for l in layouts), 1)
-        self.kv = symm.empty(2 * t_max * H * D, dtype=torch.bfloat16, device=device).view(2, t_max, H, D)
-        self.part = symm.empty(2 * r_max * H * D, dtype=torch.float32, device=device).view(2, r_max, H, D)
-        self.h_kv = symm.rendezvous(self.kv, self.group)
-        self.h_part = symm.rendezvous(self.part, self.group)
-        self.peer_kv = [self.h_kv.get_buffer(p, (2, t_max, H, D), torch.bfloat16)
-                        for p in range(self.world)]
-        self.peer_part = [self.h_part.get_buffer(p, (2, r_max, H, D), torch.float32)
-                          for p in range(self.world)]
-        # Readiness flags: [channel][src rank] int32 words in symmetric memory, written by
-        # the peers' stream front ends (native.stream_signal) and waited on locally.
-        self.flags = symm.empty(self.N_CHANNELS * self.world, dtype=torch.int32, device=device)
-        self.flags.zero_()
-        self.h_flags = symm.rendezvous(self.flags, self.group)
-        self.flag_base = [int(a) for a in self.h_flags.buffer_ptrs]
-        self.epoch = [0] * self.N_CHANNELS
+        self.t_max = t_max = max(max(l.tokens for l in layouts), 1)
+        self.r_max = r_max = max(max(l.recv_tokens for l in layouts), 1)
+        be = self.TRANSPORT
+        kv = _Regions(2 * t_max * H * D, torch.bfloat16, (2, t_max, H, D), device, self.group, be)
+        part = _Regions(2 * r_max * H * D, torch.float32, (2, r_max, H, D), device, self.group, be)
+        self.kv, self.peer_kv = kv.local, kv.peers
+        self.part, self.peer_part = part.local, part.peers
+        # Readiness flags: [channel][src rank] int32 words in peer memory
+        self.flags = FlagBarrier(self.N_CHANNELS, device, self.group, be)
+        self._regions = (kv, part)
         torch.cuda.synchronize(device)
         dist.barrier(group=self.group)                  # every rank's flags are zero
         # Pulls from different peers go to different streams so several copy engines run
@@ -86,110 +202,99 @@ class SymmetricExchange:
         self.part_row_bytes = H * D * 4            # one fp32 partial row (dK or dV)
         self.t_local = me.tokens
         self.r_local = me.recv_tokens
-        # forward pulls, per coalesced stage: (peer, src_row in peer's K/V, dst_row in my arena, n)
-        # Every chunk is pulled from its owner's buffer: over NVSwitch any peer is one hop
-        # away, so a relay edge (ring / ByteScale plans) only fixes *when* it arrives.
-        owner = chunk_placement(result.assignment, result.units)
-        self.stage_pulls: list[list[tuple[int, int, int, int]]] = []
-        for s, stage in enumerate(result.plan.stages):
-            pulls: list[tuple[int, int, int, int]] = []
-            for e in stage:
-                if e.dst != rank:
-                    continue
-                for c in e.chunks:
-                    if me.recv_stage.get(c) == s:
-                        o = owner[c]
-                        _append_merged(pulls, (o, layouts[o].offset[c],
-                                               me.recv_offset[c], me.chunk_tokens[c]))
-            self.stage_pulls.append(pulls)
+        self.stage_pulls = stage_pulls(result, rank, layouts)
+        self.publish_copies = 0                   # K/V publish copies issued (0 when zero-copy)
 
     # ------------------------------------------------------------------ forward (K5)
+    def kv_views(self):
+        """This rank's K and V planes in the exchange region ([T, Hkv, D] each, contiguous):
+        the executor's K/V input buffers."""
+        return self.kv[0, :self.t_local], self.kv[1, :self.t_local]
+
     def publish_kv(self, k, v):
-        """Copy this rank's K/V into its symmetric buffer (compute stream)."""
-        self.kv[0, :self.t_local].copy_(k, non_blocking=True)
-        self.kv[1, :self.t_local].copy_(v, non_blocking=True)
+        """Make this rank's K/V readable by the peers (compute stream): free when the caller
+        wrote them into ``kv_views()``, otherwise one copy each."""
+        kk, vv = self.kv_views()
+        if k.data_ptr() != kk.data_ptr():
+            kk.copy_(k, non_blocking=True)
+            self.publish_copies += 1
+        if v.data_ptr() != vv.data_ptr():
+            vv.copy_(v, non_blocking=True)
+            self.publish_copies += 1
 
     N_CHANNELS = 4          # kv ready, kv consumed, partials ready, partials consumed
-    BARRIER = os.environ.get("FCPB_BARRIER", "flags")   # "kernel": torch's barrier (A/B only)
+    BARRIER = os.environ.get("FCPB_BARRIER", "flags")   # "kernel": torch's barrier (symm only, A/B)
 
     def barrier(self, which: str = "kv", channel: int = 0):
-        """All-rank barrier on the current stream.  Stream memory operations, not a kernel:
-        every rank writes epoch e into each peer's flag word [channel][me], then waits for
-        its own [channel][p] words to reach e.  A barrier kernel cannot become resident
-        while a persistent attention kernel fills every SM's shared memory (K2 uses all
-        227 KB), so it used to wait for the whole launch (C2 at N=4: the partial returns
-        started 2 ms late)."""
-        if self.BARRIER == "kernel":
-            (self.h_kv if which == "kv" else self.h_part).barrier(channel=channel)
+        """All-rank barrier on the current stream (``FlagBarrier``)."""
+        if self.BARRIER == "kernel" and self.TRANSPORT == "symm":
+            self._regions[0 if which == "kv" else 1]._keep[1].barrier(channel=channel)
             return
-        self.signal_all(which, channel)
-        cur = torch.cuda.current_stream(self.device)
-        for p in range(self.world):
-            if p != self.rank:
-                self.wait_peer(which, channel, p, cur)
+        self.flags.barrier(self._channel(which, channel))
 
     def _channel(self, which: str, channel: int) -> int:
         return (0 if which == "kv" else 2) + channel
 
     def signal_all(self, which: str, channel: int) -> None:
         """Open a new epoch on the channel and tell every peer (current stream)."""
-        ch = self._channel(which, channel)
-        self.epoch[ch] += 1
-        cur = torch.cuda.current_stream(self.device)
-        w, me = self.world, self.rank
-        for p in range(w):
-            if p != me:
-                native.stream_signal(self.flag_base[p] + 4 * (ch * w + me), self.epoch[ch], cur)
+        self.flags.signal_all(self._channel(which, channel))
 
     def wait_peer(self, which: str, channel: int, peer: int, stream) -> None:
         """Work queued on `stream` after this waits for peer's signal of the current epoch."""
-        ch = self._channel(which, channel)
-        native.stream_wait(self.flag_base[self.rank] + 4 * (ch * self.world + peer), self.epoch[ch], stream)
+        self.flags.wait_peer(self._channel(which, channel), peer, stream)
 
     FANOUT_BYTES = 64 << 20
 
-    def _fanout(self, copies, nbytes, pre=None):
-        """Run (peer, fn) copies with one stream per peer (mod the copy-stream count), ordered
-        after the current stream's prior work; the current stream then waits for all.
-        Measured on C2/C4 at N=4: fan-out lifts large exchanges (C4 returns 411 -> 483 GB/s)
-        but the fork/join costs more than it gains below ~64 MB (C2 pulls 260 -> 171 GB/s),
-        so small copy sets stay on the current stream.
+    def _fanout(self, pulls, nbytes, fn, pre=None):
+        """Issue fn(pull) for every pull, with one stream per peer (mod the copy-stream
+        count), ordered after the current stream's prior work; the current stream then
+        waits for all.  Measured on C2/C4 at N=4: fan-out lifts large exchanges (C4 returns
+        411 -> 483 GB/s) but the fork/join costs more than it gains below ~64 MB (C2 pulls
+        260 -> 171 GB/s), so small copy sets stay on the current stream.
         `pre(peer, stream)`, when given, runs once per peer on the stream that carries its
         copies, before the first of them (a per-peer readiness wait)."""
         cur = torch.cuda.current_stream(self.device)
         seen = set()
         if nbytes < self.FANOUT_BYTES or len(self.copy_streams) == 1:
-            for peer, fn in copies:
-                if pre is not None and peer not in seen:
-                    pre(peer, cur)
-                    seen.add(peer)
-                fn()
+            for p in pulls:
+                if pre is not None and p.peer not in seen:
+                    pre(p.peer, cur)
+                    seen.add(p.peer)
+                fn(p, cur)
             return
         used = set()
-        for peer, fn in copies:
-            i = peer % len(self.copy_streams)
+        for p in pulls:
+            i = p.peer % len(self.copy_streams)
             cs = self.copy_streams[i]
             if i not in used:
                 cs.wait_stream(cur)
                 used.add(i)
-            if pre is not None and peer not in seen:
-                pre(peer, cs)
-                seen.add(peer)
-            with torch.cuda.stream(cs):
-                fn()
+            if pre is not None and p.peer not in seen:
+                pre(p.peer, cs)
+                seen.add(p.peer)
+            fn(p, cs)
         for i in used:
             cur.wait_stream(self.copy_streams[i])
 
-    def pull_stage(self, s: int, k_recv, v_recv):
-        """Copy-engine pulls of stage s's KV chunks into the receive arena (ordered on the
-        current stream)."""
-        def pull(peer, src, dst, n):
-            pk = self.peer_kv[peer]
-            k_recv[dst:dst + n].copy_(pk[0, src:src + n], non_blocking=True)
-            v_recv[dst:dst + n].copy_(pk[1, src:src + n], non_blocking=True)
+    @staticmethod
+    def _planes(dst):
+        """(base pointer, plane pitch in bytes, row bytes) of a [2, R, H, D] destination."""
+        assert dst.dim() == 4 and dst.shape[0] == 2 and dst.is_contiguous()
+        row = dst.shape[2] * dst.shape[3] * dst.element_size()
+        return dst.data_ptr(), dst.shape[1] * row, row
+
+    def pull_stage(self, s: int, kv_recv):
+        """Copy-engine pulls of stage s's KV chunks into the receive arena ``kv_recv``
+        ([2, R, Hkv, D] bf16: the K plane then the V plane), one 2-D copy per merged run
+        (ordered on the current stream)."""
+        base, dpitch, row = self._planes(kv_recv)
+        spitch = self.t_max * row
+
+        def pull(p, stream):
+            native.copy_2d(base + p.dst * row, dpitch, self.peer_kv[p.peer].data_ptr() + p.src * row,
+                           spitch, p.rows * row, 2, stream)
         pulls = self.stage_pulls[s]
-        self._fanout([(peer, (lambda a=(peer, src, dst, n): pull(*a))) for peer, src, dst, n in pulls],
-                     sum(n for _, _, _, n in pulls) * self.kv_row_bytes)
+        self._fanout(pulls, sum(p.rows for p in pulls) * self.kv_row_bytes, pull)
 
     # ------------------------------------------------------------------ backward (K6)
     def partial_views(self):
@@ -198,18 +303,19 @@ class SymmetricExchange:
             return None, None
         return self.part[0, :self.r_local], self.part[1, :self.r_local]
 
-    def pull_returns(self, returns, staging_k, staging_v, staging_rows, per_peer_ready=False):
+    def pull_returns(self, returns, staging, staging_rows, per_peer_ready=False):
         """Owner side: pull every consumer's partial of my chunks (``exchange.owner_returns``)
-        into staging rows.  per_peer_ready: each consumer's pulls wait only for that
-        consumer's "partials ready" signal (``signal_all("part", 0)``), not for all ranks."""
-        def pull(peer, src, r, n):
-            pp = self.peer_part[peer]
-            staging_k[r:r + n].copy_(pp[0, src:src + n], non_blocking=True)
-            staging_v[r:r + n].copy_(pp[1, src:src + n], non_blocking=True)
-        copies = []
-        for t in returns:               # chunk t.chunk of mine, consumed by t.peer
-            a = (t.peer, self.layouts[t.peer].recv_offset[t.chunk], staging_rows[(t.chunk, t.peer)],
-                 t.tokens)
-            copies.append((t.peer, (lambda a=a: pull(*a))))
+        into ``staging`` ([2, rows, Hkv, D] fp32: dK then dV plane), one 2-D copy per merged
+        run.  per_peer_ready: each consumer's pulls wait only for that consumer's "partials
+        ready" signal (``signal_all("part", 0)``), not for all ranks."""
+        pulls = return_pulls(returns, self.layouts, staging_rows)
+        if not pulls:
+            return
+        base, dpitch, row = self._planes(staging)
+        spitch = self.r_max * row
+
+        def pull(p, stream):
+            native.copy_2d(base + p.dst * row, dpitch, self.peer_part[p.peer].data_ptr() + p.src * row,
+                           spitch, p.rows * row, 2, stream)
         pre = (lambda peer, st: self.wait_peer("part", 0, peer, st)) if per_peer_ready else None
-        self._fanout(copies, sum(t.tokens for t in returns) * 2 * self.part_row_bytes, pre)
+        self._fanout(pulls, sum(p.rows for p in pulls) * 2 * self.part_row_bytes, pull, pre)

@@ -13,13 +13,13 @@ touching its data loader.
   the same peer are merged.  A chunk whose two owners coincide is a local copy.  The
   bytes moved are exactly the reference's ``reshuffle_cost`` accounting
   (``simulator.py:294-342``); ``tests/test_reshuffle.py`` checks that.
-* Transport (GPU): one symmetric-memory byte buffer (``torch.distributed._symmetric_memory``)
+* Transport (GPU): one peer-memory byte buffer (``p2p._Regions``: a C-ABI IPC region)
   with one contiguous region per tensor of a call, so each call is:
   1. one contiguous publish per tensor;
-  2. one device barrier;
+  2. one flag barrier (stream memory operations, no kernel);
   3. copy-engine pulls of whole contiguous row runs from the peers' regions, straight into
      the output tensors;
-  4. one barrier.
+  4. one flag barrier.
   This is the same transport as the KV exchange (``p2p.py``).
 """
 
@@ -139,7 +139,7 @@ class Reshuffler:
     def __init__(self, result: ScheduleResult, rank: int, cfg: ModelConfig, device,
                  initial_layout=None, group=None, max_row_bytes: int | None = None):
         import torch.distributed as dist
-        import torch.distributed._symmetric_memory as symm
+        from .p2p import FlagBarrier, _Regions, TRANSPORT
         self.rank = rank
         self.world = result.assignment.n_workers
         self.device = torch.device(device)
@@ -148,10 +148,13 @@ class Reshuffler:
         H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
         self.row_cap = max_row_bytes or ((2 * H + 2 * Hk) * D * 2 + 4 * H)
         self.t_max = max(max(max(p.user_tokens, p.fcp_tokens) for p in self.plans), 1)
-        self.buf = symm.empty(self.t_max * self.row_cap, dtype=torch.uint8, device=self.device)
-        self.h = symm.rendezvous(self.buf, group or dist.group.WORLD)
-        self.peer = [self.h.get_buffer(p, (self.t_max * self.row_cap,), torch.uint8)
-                     for p in range(self.world)]
+        group = group or dist.group.WORLD
+        reg = _Regions(self.t_max * self.row_cap, torch.uint8, (self.t_max * self.row_cap,),
+                       self.device, group, TRANSPORT)
+        self.buf, self.peer, self._reg = reg.local, reg.peers, reg
+        self.flags = FlagBarrier(2, self.device, group)
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=group)                       # every rank's flags are zero
         self.bytes_moved = 0
 
     def _move(self, tensors, pulls, rows_in: int, rows_out: int):
@@ -175,7 +178,7 @@ class Reshuffler:
         for t, w, e, off in zip(tensors, widths, elems, region):           # publish
             self.buf[off:off + rows_in * w].view(rows_in, w).copy_(
                 t.contiguous().reshape(rows_in, e).view(torch.uint8), non_blocking=True)
-        self.h.barrier(channel=0)
+        self.flags.barrier(0)                  # every rank's rows published
         outs = []
         for t, w, e, off in zip(tensors, widths, elems, region):
             o = torch.empty((rows_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device)
@@ -186,7 +189,7 @@ class Reshuffler:
                 if peer != self.rank:
                     self.bytes_moved += n * w
             outs.append(o)
-        self.h.barrier(channel=1)              # every pull done: buffers reusable
+        self.flags.barrier(1)                  # every pull done: buffers reusable
         return outs
 
     def to_fcp(self, *tensors):

@@ -22,11 +22,19 @@ from paper_2605_08524_b200.sharding import ShardingConfig
 from paper_2605_08524_b200.workload import Batch, Sequence
 from paper_2605_08524_b200.worklist import build_rank_work
 
-# Stated tolerance (bf16 inputs/outputs, fp32 accumulation), GPU vs fp64 oracle:
+# Stated tolerance (bf16 inputs/outputs, fp32 accumulation), GPU vs fp64 oracle, per tensor
+# and per case (the FlashAttention convention):
+#   max-abs(gpu - oracle) <= 2 * max-abs(bf16 torch reference - oracle) + ATOL_FRAC * max|oracle|
+#   rel-L2 (gpu - oracle) <= 2 * rel-L2 (bf16 torch reference - oracle) + REL_FLOOR
+# for O, LSE, dQ, dK, dV, where the bf16 torch reference (``bf16_reference``) evaluates the
+# same attention with bf16 operands and bf16-rounded intermediates (cuBLAS, fp32 accumulate).
+# On top of that, fixed ceilings that hold for every case:
 #   relative L2 error  ||gpu - ref|| / ||ref||   <= REL_L2   for O, dQ, dK, dV
-#   LSE max-abs error                             <= LSE_ABS  (natural-log units)
-REL_L2 = 2e-2
-LSE_ABS = 2e-2
+#   LSE max-abs error                             <= LSE_ABS * max(1, max|LSE|)  (natural log)
+REL_L2 = 1e-2
+LSE_ABS = 1e-4
+ATOL_FRAC = 2.0 ** -10
+REL_FLOOR = 1e-4
 
 
 def schedule(lengths, n, block, model, mask="causal", tpw=None):
@@ -145,9 +153,106 @@ def compare(gpu, ref, idx, keys=("o", "lse", "dq", "dk", "dv")):
     return rep
 
 
-def assert_within_tolerance(rep):
+# ---------------------------------------------------------------------------- bf16 reference
+def bf16_chunk_reference(q, k, v, do, q_rows, kv_rows, diag_from, scale, device="cuda"):
+    """The bf16 torch reference of one Q-row block against its KV rows (test infrastructure,
+    FlashAttention's ``attention_ref(upcast=False)`` convention): S = Q K^T with bf16 operands
+    (cuBLAS, fp32 accumulate, bf16 result), softmax in fp32 from the bf16 scores, P rounded to
+    bf16, O = P V (bf16); backward dP = dO V^T (bf16), delta = rowsum(dO * O) in fp32,
+    dS = P (dP - delta) rounded to bf16, dQ = dS K, dK = dS^T Q, dV = P^T dO (bf16 per head,
+    summed over the GQA group in fp32).  KV rows from ``diag_from`` on form the diagonal chunk
+    (inclusive causal ``j <= i``); the ones before it are fully visible.
+    Returns fp64 CPU tensors (o, lse, dq, dk, dv) for those rows."""
+    H, Hk, D = q.shape[1], k.shape[1], q.shape[2]
+    G = H // Hk
+    qn, kn = q_rows.numel(), kv_rows.numel()
+    dev = torch.device(device)
+    keep = torch.ones(qn, kn, dtype=torch.bool, device=dev)
+    keep[:, diag_from:] = torch.ones(qn, kn - diag_from, dtype=torch.bool, device=dev).tril()
+    out = {"o": torch.empty((qn, H, D), dtype=torch.float64), "lse": torch.empty((qn, H), dtype=torch.float64),
+           "dq": torch.empty((qn, H, D), dtype=torch.float64),
+           "dk": torch.zeros((kn, Hk, D), dtype=torch.float64), "dv": torch.zeros((kn, Hk, D), dtype=torch.float64)}
+    qr, kr = q_rows.to(torch.long), kv_rows.to(torch.long)
+    for kh in range(Hk):
+        ks = k[kr, kh].to(dev, torch.bfloat16)
+        vs = v[kr, kh].to(dev, torch.bfloat16)
+        dk32 = torch.zeros((kn, D), dtype=torch.float32, device=dev)
+        dv32 = torch.zeros((kn, D), dtype=torch.float32, device=dev)
+        for h in range(kh * G, (kh + 1) * G):
+            qs = q[qr, h].to(dev, torch.bfloat16)
+            dos = do[qr, h].to(dev, torch.bfloat16)
+            s = torch.matmul(qs, ks.T).float() * scale
+            s = s.masked_fill(~keep, -math.inf)
+            lse = torch.logsumexp(s, dim=-1)
+            p = torch.exp(s - lse.unsqueeze(1)).to(torch.bfloat16)
+            del s
+            o = torch.matmul(p, vs)
+            dp = torch.matmul(dos, vs.T)
+            delta = (dos.float() * o.float()).sum(-1, keepdim=True)
+            ds = (p.float() * (dp.float() - delta)).to(torch.bfloat16)
+            del dp
+            dq = torch.matmul(ds, ks).float() * scale
+            dk32 += (torch.matmul(ds.T, qs).float() * scale).to(torch.bfloat16).float()
+            dv32 += torch.matmul(p.T, dos).float()
+            out["o"][:, h] = o.double().cpu()
+            out["lse"][:, h] = lse.double().cpu()
+            out["dq"][:, h] = dq.to(torch.bfloat16).double().cpu()
+            del p, ds
+        out["dk"][:, kh] = dk32.to(torch.bfloat16).double().cpu()
+        out["dv"][:, kh] = dv32.to(torch.bfloat16).double().cpu()
+    return out
+
+
+def bf16_reference(result, model, q, k, v, do, seq_ids=None, device="cuda"):
+    """``bf16_chunk_reference`` over whole sequences, laid out like ``oracle``."""
+    rows = global_sequence_rows(result)
+    if seq_ids is not None:
+        rows = {sid: rows[sid] for sid in seq_ids}
+    scale = 1.0 / math.sqrt(model.head_dim)
+    causal = result.deps.mask == "causal"
+    T = q.shape[0]
+    H, Hk, D = model.q_heads, model.kv_heads, model.head_dim
+    out = {"o": torch.zeros((T, H, D), dtype=torch.float64), "lse": torch.zeros((T, H), dtype=torch.float64),
+           "dq": torch.zeros((T, H, D), dtype=torch.float64), "dk": torch.zeros((T, Hk, D), dtype=torch.float64),
+           "dv": torch.zeros((T, Hk, D), dtype=torch.float64)}
+    for idx in rows.values():
+        r = bf16_chunk_reference(q, k, v, do, idx, idx, 0 if causal else idx.numel(), scale, device)
+        for key in ("o", "lse", "dq"):
+            out[key][idx] = r[key]
+        out["dk"][idx] = r["dk"]
+        out["dv"][idx] = r["dv"]
+    return out
+
+
+def tolerance_report(rep, brep):
+    """Per tensor: the GPU error, the bf16 torch reference's error and the derived bounds."""
+    out = {}
     for key, e in rep.items():
+        b = brep[key]
+        out[key] = dict(e, bf16_max_abs=b["max_abs"], bf16_rel_l2=b["rel_l2"],
+                        bound_max_abs=2 * b["max_abs"] + ATOL_FRAC * e["ref_max"],
+                        bound_rel_l2=2 * b["rel_l2"] + REL_FLOOR)
+    return out
+
+
+def within_fixed_caps(rep) -> bool:
+    """The fixed ceilings of ``assert_within_tolerance`` as a predicate (multi-process checks)."""
+    return all((e["max_abs"] <= LSE_ABS * max(1.0, e["ref_max"])) if key == "lse" else
+               (e["rel_l2"] <= REL_L2) for key, e in rep.items())
+
+
+def assert_within_tolerance(rep, brep=None, fixed_caps=True):
+    """The fixed ceilings (N(0,1) inputs; ``fixed_caps=False`` for deliberately
+    ill-conditioned inputs) and the per-case FlashAttention-convention bounds when the bf16
+    torch reference's errors ``brep`` are given."""
+    for key, e in rep.items():
+        if not fixed_caps:
+            break
         if key == "lse":
-            assert e["max_abs"] <= LSE_ABS, (key, e)
+            assert e["max_abs"] <= LSE_ABS * max(1.0, e["ref_max"]), (key, e)
         else:
             assert e["rel_l2"] <= REL_L2, (key, e)
+    if brep is not None:
+        for key, t in tolerance_report(rep, brep).items():
+            assert t["max_abs"] <= t["bound_max_abs"], (key, t)
+            assert t["rel_l2"] <= t["bound_rel_l2"], (key, t)

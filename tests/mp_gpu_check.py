@@ -1,5 +1,10 @@
-"""Multi-GPU executor check, run under torchrun (one process per GPU, NCCL):
-the FcpExecutor's fwd+bwd with the real NVLink exchange vs the fp64 oracle.
+"""Multi-rank executor check, run under torchrun: the FcpExecutor's fwd+bwd with the real
+exchange (IPC peer regions, copy-engine pulls, flag barriers) vs the fp64 oracle.
+
+One process per GPU over NVLink (NCCL group), or -- when the box has fewer GPUs than ranks,
+or FCPB_SHARED_GPU=1 -- every rank a separate process on GPU 0 (gloo group): the same
+product code path (IPC regions opened by another process, stream-memory-op flags, 2-D
+copy-engine pulls), time-sliced on one device.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \\
         --master-port P tests/mp_gpu_check.py [lengths] [block]
@@ -18,19 +23,26 @@ from oracle.attention_ref import mono_bwd, mono_fwd  # noqa: E402
 from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows  # noqa: E402
 from paper_2605_08524_b200.costmodel import ModelConfig  # noqa: E402
 from paper_2605_08524_b200.executor import FcpExecutor  # noqa: E402
-from tests.gpu_harness import REL_L2, LSE_ABS, err, make_inputs, schedule  # noqa: E402
+from tests.gpu_harness import err, make_inputs, schedule, within_fixed_caps  # noqa: E402
 
 
 def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    shared = os.environ.get("FCPB_SHARED_GPU") == "1" or torch.cuda.device_count() < world
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     lengths = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3523,2702,2219,1292,1438,413,544,319").split(",")]
     block = int(sys.argv[2]) if len(sys.argv) > 2 else 512
-    model = ModelConfig(q_heads=8, kv_heads=2, head_dim=128)
+    hq, hk = (int(x) for x in os.environ.get("FCPB_CHECK_HEADS", "8,2").split(","))
+    model = ModelConfig(q_heads=hq, kv_heads=hk, head_dim=128)
     sched = os.environ.get("FCPB_CHECK_SCHED", "fcp")
     if sched == "fcp":
         r = schedule(lengths, world, block, model)
@@ -55,7 +67,7 @@ def main():
     rep = {}
     for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))
-    ok = all((e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2) for n, e in rep.items())
+    ok = within_fixed_caps(rep)
     # transparent reshuffler (§8f): user layout -> FCP layout equals the executor's inputs
     # exactly, and the round trip is the identity (symmetric-memory copy-engine pulls)
     from paper_2605_08524_b200.reshuffle import Reshuffler, user_layouts
@@ -76,12 +88,12 @@ def main():
     mr = ex.measured_report(*loc, reps=2)
     ok = ok and len(mr.per_worker) == world and len(mr.stages) == len(ex.stages) \
         and mr.total_time > 0 and all(w.compute_time > 0 for w in mr.per_worker) and mr.total_flops > 0
-    print(json.dumps({"rank": rank, "world": world, "recv_tokens": lay.recv_tokens,
+    print(json.dumps({"rank": rank, "world": world, "shared_gpu": shared, "recv_tokens": lay.recv_tokens,
                       "stages": len(ex.stages), "ok": ok, "errors": rep,
                       "measured_total_ms": mr.total_time * 1e3,
                       "reshuffle_ok": reshuffle_ok, "reshuffle_to_fcp_ms": t0.elapsed_time(t1),
                       "measured_eta": [round(w.eta, 3) for w in mr.per_worker]}), flush=True)
-    flag = torch.tensor([1 if ok else 0], device=dev)
+    flag = torch.tensor([1 if ok else 0], device="cpu" if shared else dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
     sys.exit(0 if flag.item() == 1 else 1)

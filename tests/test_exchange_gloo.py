@@ -1,10 +1,12 @@
 """Multi-process exchange on CPU (gloo, world_size 2 and 3, 127.0.0.1).
 
-Executes the coalesced Delta-matching plan stage by stage with real
-point-to-point messages and checks that (a) every rank's receive arena ends up
-holding exactly the KV rows of the chunks the plan delivers to it and (b) the
-reversed-edge return brings every receiver's partial back to the owner's
-staging rows.  This is the host logic of K5/K6 that the NCCL path reuses.
+Executes the product transport's copy lists -- ``p2p.stage_pulls`` per coalesced stage and
+``p2p.return_pulls`` for the reversed-edge dK/dV return, each run moving two planes (K and
+V, dK and dV) exactly as the executor's 2-D copy-engine pulls do -- with real
+point-to-point messages between processes: a pull (peer, src, dst, rows) becomes a message
+the peer serves from its own plane rows [src, src+rows).  Checks that (a) every rank's
+two-plane receive arena ends up holding exactly the K/V rows of the chunks the plan delivers
+to it and (b) the return brings every consumer's partial back to the owner's staging rows.
 """
 
 import os
@@ -17,6 +19,7 @@ import torch.multiprocessing as mp
 
 from oracle.simworkers import gather_rank, global_offsets
 from paper_2605_08524_b200 import exchange
+from paper_2605_08524_b200.p2p import return_pulls, stage_pulls
 from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, ModelConfig
 from paper_2605_08524_b200.pipeline import fcp_schedule, plan_digest
 from paper_2605_08524_b200.sharding import ShardingConfig
@@ -43,6 +46,26 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def _serve_and_pull(rank, world, pulls_of, s, src_planes, dst_planes):
+    """One stage of pulls as gloo messages: serve every peer's pulls from my planes, receive
+    mine into ``dst_planes``; both sides walk the same lists in the same order."""
+    ops, landing = [], []
+    for q in range(world):
+        if q == rank:
+            continue
+        for p in pulls_of[q][s]:
+            if p.peer == rank:
+                ops.append(dist.P2POp(dist.isend, src_planes[:, p.src:p.src + p.rows].contiguous(), q))
+    for p in pulls_of[rank][s]:
+        buf = torch.empty_like(dst_planes[:, p.dst:p.dst + p.rows])
+        ops.append(dist.P2POp(dist.irecv, buf, p.peer))
+        landing.append((p, buf))
+    for w in (dist.batch_isend_irecv(ops) if ops else []):
+        w.wait()
+    for p, buf in landing:
+        dst_planes[:, p.dst:p.dst + p.rows] = buf
+
+
 def _worker(rank, world, port, errq, sched="fcp"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -56,25 +79,27 @@ def _worker(rank, world, port, errq, sched="fcp"):
         vg = torch.randn((T, MODEL.kv_heads, MODEL.head_dim), generator=g)
         k = gather_rank(kg, lay, goff, r.deps)
         v = gather_rank(vg, lay, goff, r.deps)
-        kr = torch.full((lay.recv_tokens, MODEL.kv_heads, MODEL.head_dim), float("nan"))
-        vr = kr.clone()
-        stages = exchange.build_stage_ops(r, lay)
-        for st in stages:
-            exchange.wait_all(exchange.run_stage(st, (k, v), (kr, vr)))
-        assert torch.equal(kr, gather_rank(kg, lay, goff, r.deps, recv=True))
-        assert torch.equal(vr, gather_rank(vg, lay, goff, r.deps, recv=True))
-        # reverse: each consumer returns (its rank + chunk data) as the "partial", to the owner
-        part = kr + 1000.0 * (rank + 1)
         layouts = [rank_layout(r, q) for q in range(world)]
         owner = chunk_placement(r.assignment, r.units)
-        returns = exchange.owner_returns(layouts, owner, rank)
-        rows, rounds, n_stage = exchange.return_staging_layout(returns)
-        staged = torch.zeros((n_stage, MODEL.kv_heads, MODEL.head_dim))
-        exchange.wait_all(exchange.run_return(lay, layouts, owner, (part,), (staged,), rows))
-        for t in returns:
-            got = staged[rows[(t.chunk, t.peer)]:rows[(t.chunk, t.peer)] + t.tokens]
-            want = k[t.row:t.row + t.tokens] + 1000.0 * (t.peer + 1)
-            assert torch.equal(got, want), (rank, t)
+        kv = torch.stack([k, v])                                # my two planes
+        kv_recv = torch.full((2, lay.recv_tokens, MODEL.kv_heads, MODEL.head_dim), float("nan"))
+        pulls_of = [stage_pulls(r, q, layouts, owner) for q in range(world)]
+        for s_idx in range(len(r.plan.stages)):
+            _serve_and_pull(rank, world, pulls_of, s_idx, kv, kv_recv)
+        assert torch.equal(kv_recv[0], gather_rank(kg, lay, goff, r.deps, recv=True))
+        assert torch.equal(kv_recv[1], gather_rank(vg, lay, goff, r.deps, recv=True))
+        # reverse: each consumer's "partial" = (its rank + chunk data); owners pull them home
+        part = kv_recv + 1000.0 * (rank + 1)
+        rets = [exchange.owner_returns(layouts, owner, q) for q in range(world)]
+        staging = [exchange.return_staging_layout(t) for t in rets]
+        rpulls = [[return_pulls(rets[q], layouts, staging[q][0])] for q in range(world)]
+        rows, rounds, n_stage = staging[rank]
+        staged = torch.zeros((2, n_stage, MODEL.kv_heads, MODEL.head_dim))
+        _serve_and_pull(rank, world, rpulls, 0, part, staged)
+        for t in rets[rank]:
+            a_ = rows[(t.chunk, t.peer)]
+            want = kv[:, t.row:t.row + t.tokens] + 1000.0 * (t.peer + 1)
+            assert torch.equal(staged[:, a_:a_ + t.tokens], want), (rank, t)
         # rounds: every staged row used once; destinations unique within a round
         srcs = sorted(x for src, _ in rounds for x in src)
         assert srcs == list(range(n_stage))

@@ -1,5 +1,10 @@
-"""Multi-GPU executor parity (NCCL over NVLink): runs tests/mp_gpu_check.py under
-torchrun on 2 GPUs (and 4 if present).  Skipped on boxes with fewer GPUs."""
+"""Multi-rank executor parity: runs tests/mp_gpu_check.py under torchrun.
+
+* one process per GPU (NVLink, NCCL group) on 2 and 4 GPUs when the box has them;
+* two or three processes sharing GPU 0 (gloo group) on any box: the product transport --
+  IPC peer regions opened by another process, flag barriers, 2-D copy-engine pulls, the
+  dK/dV return and K4 -- runs exactly as across GPUs, time-sliced on one device.  This is
+  the case a one-GPU box runs."""
 
 import os
 import socket
@@ -19,15 +24,33 @@ def _port():
         return s.getsockname()[1]
 
 
+def _run(n, sched="fcp", shared=False, args=(), heads="8,2"):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mp_gpu_check.py"), *args]
+    env = dict(os.environ, FCPB_CHECK_SCHED=sched, FCPB_CHECK_HEADS=heads,
+               FCPB_SHARED_GPU="1" if shared else "0")
+    proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    print(proc.stdout[-4000:])
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+
+
 @pytest.mark.parametrize("n,sched", [(2, "fcp"), (4, "fcp"), (4, "ring")])
 def test_executor_nccl_parity(n, sched):
     """FCP plans, and the ring plan of baselines.py (relay edges, relayed-only chunks)."""
     if torch.cuda.device_count() < n:
         pytest.skip(f"needs {n} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tests", "mp_gpu_check.py")]
-    proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
-                          env=dict(os.environ, FCPB_CHECK_SCHED=sched))
-    print(proc.stdout[-4000:])
-    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    _run(n, sched)
+
+
+@pytest.mark.parametrize("n,sched,args,heads", [
+    (2, "fcp", (), "8,2"),
+    (3, "fcp", (), "8,2"),
+    (3, "ring", (), "8,2"),
+    # ADVICE r1: ranks none of whose chunks is consumed remotely (no dK/dV comes back)
+    (4, "fcp", ("2048,2048,4096", "2048"), "8,2"),
+    (2, "fcp", ("9000,4100,3000,2100,1500,700,129", "2048"), "32,8"),   # Llama-3-8B heads
+])
+def test_executor_shared_gpu_parity(n, sched, args, heads):
+    """N ranks as N processes on GPU 0: the multi-rank product path on a one-GPU box."""
+    _run(n, sched, shared=True, args=args, heads=heads)

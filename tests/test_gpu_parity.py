@@ -1,7 +1,10 @@
 """GPU parity: sm_100a kernels (through the C ABI) vs the CPU fp64 oracle.
 
-Tolerance (stated in tests/gpu_harness.py): rel-L2 <= 2e-2 for O, dQ, dK, dV and
-LSE max-abs <= 2e-2; every test prints max-abs and rel-L2 per tensor.
+Tolerance (stated in tests/gpu_harness.py), per tensor and per case: max-abs and rel-L2 of
+the GPU result against the oracle at most twice those of a bf16 torch reference of the same
+attention plus a small floor (the FlashAttention convention), and under fixed
+ceilings (rel-L2 <= 1e-2 for O, dQ, dK, dV; LSE max-abs <= 1e-4 * max(1, |LSE|)).  Every test
+prints the GPU and bf16-reference errors and the bounds per tensor.
 """
 
 import json
@@ -11,8 +14,9 @@ import torch
 
 from paper_2605_08524_b200 import configs
 from paper_2605_08524_b200.costmodel import ModelConfig
-from tests.gpu_harness import (assert_within_tolerance, compare, make_inputs, oracle,
-                               run_plan_on_gpu, schedule)
+from tests.gpu_harness import (assert_within_tolerance, bf16_chunk_reference, bf16_reference,
+                               compare, err, make_inputs, oracle, run_plan_on_gpu, schedule,
+                               tolerance_report)
 
 pytestmark = pytest.mark.gpu
 
@@ -25,66 +29,147 @@ def _report(name, rep):
 
 
 def _full_check(lengths, n, block, model, mask="causal", seq_ids=None, backward=True,
-                fuse_remote=False):
+                fuse_remote=False, inputs=None, name="case", fixed_caps=True):
+    """GPU (simulated ranks on one device) vs the fp64 oracle, with the bf16 torch reference's
+    errors beside it; asserts the stated tolerance and returns the report."""
     r = schedule(lengths, n, block, model, mask)
     from oracle.simworkers import global_offsets
     _, T = global_offsets(r)
-    q, k, v, do = make_inputs(T, model)
+    q, k, v, do = inputs(T, model, r) if inputs else make_inputs(T, model)
     gpu = run_plan_on_gpu(r, model, q, k, v, do, backward=backward, fuse_remote=fuse_remote)
     ref, idx = oracle(r, model, q, k, v, do, seq_ids)
     keys = ("o", "lse", "dq", "dk", "dv") if backward else ("o", "lse")
     rep = compare(gpu, ref, idx, keys)
+    brep = compare(bf16_reference(r, model, q, k, v, do, seq_ids), ref, idx, keys)
+    _report(name, tolerance_report(rep, brep))
+    assert_within_tolerance(rep, brep, fixed_caps)
     return rep
 
 
 def test_forward_single_tile():
-    rep = _full_check([128], 1, 256, GQA_SMALL, backward=False)
-    _report("fwd 128 tokens", rep)
-    assert_within_tolerance(rep)
+    _full_check([128], 1, 256, GQA_SMALL, backward=False, name="fwd 128 tokens")
 
 
 def test_forward_ragged_small():
-    rep = _full_check([1, 127, 129, 300, 513], 1, 256, GQA_SMALL, backward=False)
-    _report("fwd ragged", rep)
-    assert_within_tolerance(rep)
+    _full_check([1, 127, 129, 300, 513], 1, 256, GQA_SMALL, backward=False, name="fwd ragged")
 
 
 def test_fwd_bwd_c1_lengths_single_rank():
     w = configs.c1_tiny(2)
-    rep = _full_check(list(w.lengths), 1, 512, GQA_SMALL)
-    _report("C1 lengths N=1", rep)
-    assert_within_tolerance(rep)
+    _full_check(list(w.lengths), 1, 512, GQA_SMALL, name="C1 lengths N=1")
 
 
 def test_fwd_bwd_c1_two_simulated_ranks():
     w = configs.c1_tiny(2)
-    rep = _full_check(list(w.lengths), 2, 512, GQA_SMALL)
-    _report("C1 lengths N=2 (merge + dKV return)", rep)
-    assert_within_tolerance(rep)
+    _full_check(list(w.lengths), 2, 512, GQA_SMALL, name="C1 lengths N=2 (merge + dKV return)")
 
 
 def test_fwd_bwd_four_simulated_ranks_ragged():
-    rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 1024, GQA_SMALL)
-    _report("ragged N=4", rep)
-    assert_within_tolerance(rep)
+    _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 1024, GQA_SMALL, name="ragged N=4")
 
 
 def test_full_mask():
-    rep = _full_check([700, 300, 64], 2, 256, GQA_SMALL, mask="full")
-    _report("full mask N=2", rep)
-    assert_within_tolerance(rep)
+    _full_check([700, 300, 64], 2, 256, GQA_SMALL, mask="full", name="full mask N=2")
 
 
-def test_c2_llama8b_n1_sampled():
-    """C2 (Llama-3-8B GQA 32/8, 64K packed, block 2K) at N=1; the oracle checks a
-    sample of sequences including the longest (bounded CPU time)."""
+def test_c2_llama8b_n1_every_sequence():
+    """C2 (Llama-3-8B GQA 32/8, 62,956-token packed batch, block 2K) at N=1, every sequence
+    against the fp64 oracle, including the 16,561-token one whose last Q chunk has an
+    18-chunk KV list (materialised-dS backward, the bench path)."""
     w = configs.c2_llama8b_64k(1)
-    lengths = list(w.lengths)
-    # a 3-pair zigzag sequence (5487), a 2-pair one (2091) and a varlen-pack member (1520)
-    pick = [lengths.index(5487), lengths.index(2091), lengths.index(1520)]
-    rep = _full_check(lengths, 1, 2048, LLAMA, seq_ids=pick)
-    _report("C2 N=1 sampled", rep)
-    assert_within_tolerance(rep)
+    _full_check(list(w.lengths), 1, 2048, LLAMA, name="C2 N=1 all 15 sequences")
+
+
+def _planted_max_inputs(T, model, r):
+    """Scores that climb by ~80 raw units (> the 62.7-unit lazy-rescale threshold,
+    8 / (scale * log2 e)) from one 128-key tile to the next along every sequence: every
+    query gets +8 u and key j of a sequence +10 * (j // 128) u, u a unit vector."""
+    from oracle.simworkers import global_sequence_rows
+    g = torch.Generator().manual_seed(99)
+    H, Hk, D = model.q_heads, model.kv_heads, model.head_dim
+    q, k, v, do = (torch.randn((T, h, D), generator=g) for h in (H, Hk, Hk, H))
+    u = torch.randn(D, generator=g)
+    u = u / u.norm()
+    q += 8.0 * u
+    for idx in global_sequence_rows(r).values():
+        k[idx] += (10.0 * (torch.arange(idx.numel()) // 128)).float()[:, None, None] * u
+    return tuple(x.to(torch.bfloat16) for x in (q, k, v, do))
+
+
+def test_forward_lazy_rescale_path():
+    """K1 rescales O in TMEM only when a row max grows by > 2^8 in the exp2 domain; N(0,1)
+    inputs never trigger it.  Planted scores force it on every KV tile step, and the kernel's
+    rescale counter proves the branch ran (fcpb_debug_counters)."""
+    from paper_2605_08524_b200 import native
+    native.fwd_rescale_events(reset=True)
+    # scores of ~100 nats and |K| up to ~110 make dQ ill-conditioned (the bf16 reference is
+    # off by 5% rel-L2 there), so only the bf16-relative bound applies
+    _full_check([1500, 700, 300], 1, 512, GQA_SMALL, inputs=_planted_max_inputs,
+                name="fwd+bwd forced lazy O rescale", fixed_caps=False)
+    torch.cuda.synchronize()
+    n = native.fwd_rescale_events(reset=True)
+    _report("lazy rescale events (warp level)", {"events": n})
+    assert n > 0
+    # and N(0,1) inputs do not take the branch (it stays off the hot path)
+    _full_check([1500, 700], 1, 512, GQA_SMALL, backward=False, name="fwd N(0,1)")
+    torch.cuda.synchronize()
+    assert native.fwd_rescale_events(reset=True) == 0
+
+
+def _last_chunk_check(lengths, block, model, name, env=None, monkeypatch=None, expect_ds=None):
+    """A long sequence's last Q chunk (the longest KV list of the batch) at N=1 against the
+    fp64 oracle of that chunk: O, LSE and dQ of its rows, and dK/dV of its rows -- complete
+    there, since under the causal mask only the last Q chunk attends to the last KV chunk."""
+    import math
+    from oracle.attention_ref import chunk_fwd_bwd
+    from oracle.simworkers import global_offsets, global_sequence_rows
+    from paper_2605_08524_b200.attention import BlockAttention
+    from paper_2605_08524_b200.worklist import build_rank_work
+    for key, val in (env or {}).items():
+        monkeypatch.setenv(key, val)
+    r = schedule(lengths, 1, block, model)
+    goff, T = global_offsets(r)
+    if expect_ds is not None:
+        assert BlockAttention(build_rank_work(r, 0), model, torch.device("cuda", 0)).ds_mode == expect_ds
+    q, k, v, do = make_inputs(T, model)
+    gpu = run_plan_on_gpu(r, model, q, k, v, do)
+    sid = max(range(len(lengths)), key=lambda i: lengths[i])
+    idx = global_sequence_rows(r)[sid]
+    last = max(c for (s_, c) in r.deps.chunk_tokens if s_ == sid)
+    m = r.deps.chunk_tokens[(sid, last)]
+    L = idx.numel()
+    q_rows, kv_rows = idx[L - m:], idx
+    scale = 1.0 / math.sqrt(model.head_dim)
+    o, lse, dq, dk, dv = chunk_fwd_bwd(q, k, v, do, q_rows, kv_rows, L - m, scale, torch.float64)
+    ref = {"o": o, "lse": lse, "dq": dq, "dk": dk[L - m:], "dv": dv[L - m:]}
+    b = bf16_chunk_reference(q, k, v, do, q_rows, kv_rows, L - m, scale)
+    b["dk"], b["dv"] = b["dk"][L - m:], b["dv"][L - m:]
+    rep = {key: err(gpu[key][q_rows], ref[key]) for key in ref}
+    brep = {key: err(b[key], ref[key]) for key in ref}
+    _report(f"{name} (last chunk: {m} q rows x {L} kv rows)", tolerance_report(rep, brep))
+    assert_within_tolerance(rep, brep)
+
+
+def test_c3_shape_long_sequence_recompute_dq(monkeypatch):
+    """C3's 256K sequence at Llama-3-8B 32/8, block 2K: its last Q chunk has a 256-entry KV
+    list.  dS (about 1 TB) does not fit, so dQ runs the recompute kernel K2b."""
+    _last_chunk_check([262144], 2048, LLAMA, "C3 256K seq, K2b recompute dQ", monkeypatch=monkeypatch,
+                      expect_ds=False)
+
+
+def test_c4_shape_block_4k(monkeypatch):
+    """C4's 128K sequence, block 4K (2,048-token chunks), 32/8 heads (recompute dQ)."""
+    _last_chunk_check([131072], 4096, LLAMA, "C4 128K seq, block 4K", monkeypatch=monkeypatch,
+                      expect_ds=False)
+
+
+def test_c5_shape_block_6k_both_dq_modes(monkeypatch):
+    """C5's largest block (6K: 3,072-token chunks) with a varlen pack beside it, 32/8 heads,
+    with materialised dS (default here) and with the recompute kernel forced."""
+    _full_check([30000, 5000, 700], 1, 6144, LLAMA, seq_ids=[1, 2], name="C5 block 6K packed seqs")
+    _last_chunk_check([30000, 5000, 700], 6144, LLAMA, "C5 block 6K, materialised dS", expect_ds=True)
+    _last_chunk_check([30000, 5000, 700], 6144, LLAMA, "C5 block 6K, K2b recompute dQ",
+                      env={"FCPB_DS": "0"}, monkeypatch=monkeypatch, expect_ds=False)
 
 
 def test_measured_report_single_rank():
@@ -115,7 +200,6 @@ def test_executor_single_rank_parity():
     from oracle.attention_ref import mono_bwd, mono_fwd
     from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows
     from paper_2605_08524_b200.executor import FcpExecutor
-    from tests.gpu_harness import err, REL_L2, LSE_ABS
     model = GQA_SMALL
     r = schedule([1500, 700, 300, 129, 40], 1, 512, model)
     goff, T = global_offsets(r)
@@ -132,33 +216,37 @@ def test_executor_single_rank_parity():
     rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
     rep = {n: err(g.cpu(), gather_rank(ref, ex.layout, goff, r.deps))
            for n, g, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv))}
-    _report("executor N=1", rep)
-    for n, e in rep.items():
-        assert (e["max_abs"] <= LSE_ABS) if n == "lse" else (e["rel_l2"] <= REL_L2), (n, e)
+    b = bf16_reference(r, model, q, k, v, do)
+    brep = {n: err(gather_rank(b[n], ex.layout, goff, r.deps), gather_rank(ref, ex.layout, goff, r.deps))
+            for n, ref in (("o", ro), ("lse", rl), ("dq", rdq), ("dk", rdk), ("dv", rdv))}
+    _report("executor N=1", tolerance_report(rep, brep))
+    assert_within_tolerance(rep, brep)
 
 
 def test_fwd_bwd_eight_simulated_ranks():
     """N=8 plan structures on one GPU (simulated workers): many stages, chunks with several
     receivers (race-free K4 rounds), merges of multi-stage partials."""
-    rep = _full_check([4000, 3100, 2100, 1500, 1000, 700, 520, 300, 129, 128, 64, 5], 8, 512, GQA_SMALL)
-    _report("ragged N=8", rep)
-    assert_within_tolerance(rep)
+    _full_check([4000, 3100, 2100, 1500, 1000, 700, 520, 300, 129, 128, 64, 5], 8, 512, GQA_SMALL,
+                name="ragged N=8")
 
 
 def test_fwd_bwd_four_simulated_ranks_fused_remote_wave():
     """All received KV of a rank in one forward wave (the executor's fused-remote policy)."""
-    rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 512, GQA_SMALL, fuse_remote=True)
-    _report("ragged N=4 fused remote wave", rep)
-    assert_within_tolerance(rep)
+    _full_check([4000, 2100, 1000, 700, 129, 128, 5], 4, 512, GQA_SMALL, fuse_remote=True,
+                name="ragged N=4 fused remote wave")
 
 
 def test_fwd_bwd_recompute_dq(monkeypatch):
     """The recompute dQ kernel (K2b), used when dS does not fit in HBM (C3, C4): forced
     here on a case the default would run with materialised dS."""
     monkeypatch.setenv("FCPB_DS", "0")
-    rep = _full_check([4000, 2100, 1000, 700, 129, 128, 5], 2, 512, GQA_SMALL)
-    _report("recompute dQ N=2", rep)
-    assert_within_tolerance(rep)
+    _full_check([4000, 2100, 1000, 700, 129, 128, 5], 2, 512, GQA_SMALL, name="recompute dQ N=2")
+
+    
+def test_fwd_bwd_llama_heads_four_simulated_ranks():
+    """The Llama-3-8B head shape (32/8) through the multi-rank path (partials, merge, dKV
+    return) on simulated ranks."""
+    _full_check([9000, 4100, 3000, 2100, 1500, 700, 129], 4, 2048, LLAMA, name="Llama 32/8 N=4")
 
 
 def test_materialised_ds_is_default_when_it_fits():

@@ -63,3 +63,15 @@ def test_struct_layouts_match_header(tmp_path):
         assert int(out[cname]) == ctypes.sizeof(py), cname
         for fname, _ in py._fields_:
             assert int(out[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
+
+
+def test_workspace_queries():
+    """The workspace-size queries (host arithmetic, no GPU) match the buffers the Python
+    side allocates: preprocess [2, Hq, t_pad] fp32, forward partials [P, Hq, D+1] fp32,
+    dS tiles bf16 128x128 per (pair, q-head)."""
+    lib = native.load()
+    assert lib.fcpb_bwd_preprocess_bytes(10, 32) == 2 * 32 * 12 * 4
+    assert lib.fcpb_bwd_preprocess_bytes(12, 8) == 2 * 8 * 12 * 4
+    assert lib.fcpb_fwd_partial_bytes(1000, 32, 128) == 1000 * 32 * 129 * 4
+    assert lib.fcpb_ds_tile_bytes(3, 32) == 3 * 32 * 128 * 128 * 2
+    assert lib.fcpb_ds_tile_bytes(1 << 20, 64) == (1 << 20) * 64 * 32768   # no int overflow

@@ -11,8 +11,8 @@ import math
 import pytest
 import torch
 
-from oracle.attention_ref import (emulate_backward, emulate_forward, mono_bwd, mono_fwd,
-                                  sequence_rows, tiled_fwd)
+from oracle.attention_ref import (chunk_fwd_bwd, emulate_backward, emulate_forward, mono_bwd,
+                                  mono_fwd, sequence_rows, tiled_fwd)
 from oracle.simworkers import (gather_rank, global_offsets, global_sequence_rows,
                                return_partials, scatter_rank)
 from paper_2605_08524_b200.costmodel import DEFAULT_EFFICIENCY, ModelConfig
@@ -82,6 +82,25 @@ def test_dense_backward_matches_autograd():
     loss.backward()
     for a, b in ((dq, qa.grad), (dk, ka.grad), (dv, va.grad)):
         assert torch.allclose(a, b, atol=1e-10)
+
+
+def test_chunk_fwd_bwd_equals_dense():
+    """The per-Q-chunk evaluator (bench CPU sample, GPU last-chunk checks) against the dense
+    sequence: O/LSE/dQ of the chunk rows; dK/dV of the last chunk's rows are complete."""
+    L, m = 700, 170
+    q, k, v, do = _inputs(L, 3)
+    rows = {0: torch.arange(L)}
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    o, lse = mono_fwd(q, k, v, rows, scale)
+    dq, dk, dv = mono_bwd(q, k, v, o, lse, do, rows, scale)
+    for start in (0, 230, L - m):
+        qr = torch.arange(start, start + m)
+        co, cl, cdq, cdk, cdv = chunk_fwd_bwd(q, k, v, do, qr, torch.arange(start + m), start, scale,
+                                              torch.float64)
+        assert torch.allclose(co, o[qr], atol=1e-12) and torch.allclose(cl, lse[qr], atol=1e-12)
+        assert torch.allclose(cdq, dq[qr], atol=1e-12)
+    assert torch.allclose(cdk[L - m:], dk[L - m:], atol=1e-12)
+    assert torch.allclose(cdv[L - m:], dv[L - m:], atol=1e-12)
 
 
 @pytest.mark.parametrize("mask", ["causal", "full"])
