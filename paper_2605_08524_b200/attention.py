@@ -350,22 +350,31 @@ def ctypes_ref(s):
 
 
 class _FcpAttentionFn(torch.autograd.Function):
-    """Autograd wrapper for a single rank without exchange (N=1)."""
+    """Autograd over one rank's block attention: a ``BlockAttention`` (single rank, no
+    exchange) or an ``FcpExecutor`` (any N: the forward runs the K5 exchange and K3 merge,
+    the backward the K6 return and K4).  Every rank must call it, in the same order, since
+    the executor's exchange is collective."""
 
     @staticmethod
-    def forward(ctx, q, k, v, op: BlockAttention):
-        o, lse = op.forward(q, k, v)
+    def forward(ctx, q, k, v, runner):
+        o, lse = runner.forward(q, k, v)
         ctx.save_for_backward(q, k, v, o, lse)
-        ctx.op = op
-        return o
+        ctx.runner = runner
+        ctx.mark_non_differentiable(lse)
+        return o, lse
 
     @staticmethod
-    def backward(ctx, do):
+    def backward(ctx, do, _dlse):
         q, k, v, o, lse = ctx.saved_tensors
-        dq, dk, dv, _, _ = ctx.op.backward(q, k, v, o, lse, do.contiguous())
+        out = ctx.runner.backward(q, k, v, o, lse, do.contiguous())
+        dq, dk, dv = out[:3]
         return dq, dk, dv, None
 
 
-def fcp_attention(q, k, v, op: BlockAttention):
-    """Differentiable block attention of one rank (no KV exchange)."""
-    return _FcpAttentionFn.apply(q, k, v, op)
+def fcp_attention(q, k, v, runner, return_lse: bool = False):
+    """Differentiable FCP block attention of this rank's packed Q/K/V ([T, H, 128] bf16 in
+    the plan's layout, ``worklist.rank_layout``).  ``runner``: an ``FcpExecutor`` (N >= 1,
+    collective) or a ``BlockAttention`` (one rank without exchange).  Returns O (and the
+    fp32 natural-log LSE when ``return_lse``)."""
+    o, lse = _FcpAttentionFn.apply(q, k, v, runner)
+    return (o, lse) if return_lse else o

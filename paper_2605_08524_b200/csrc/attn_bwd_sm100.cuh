@@ -97,7 +97,7 @@ struct Smem {
   uint64_t kv_full, kv_empty;
   uint64_t q_full[kQSlots], q_empty[kQSlots];
   uint64_t do_full[kDoSlots], do_empty[kDoSlots];
-  uint64_t s_full, dp_full, p_full, ds_full;
+  uint64_t s_full, dp_full, p_half, p_full, ds_full;
   uint64_t acc_full, acc_free;
   SchedRing sched;
   uint32_t tmem_base;
@@ -165,12 +165,26 @@ FCPB_DEV float4 lds128(uint32_t addr) {
 // Phase 1, 32 q columns of one kv row:  P = exp2(S*c + nlse2[q])  -> bf16 pairs in pk (kept
 // for phase 2; the dV MMA consumes the same bf16 P) and stored at t_p.
 // kMask: ragged kv row / ragged q / causal diagonal.
+// Split P arrival: after its first 16 q columns every softmax thread stores them (8 TMEM
+// columns) and arrives on p_half, so the MMA warp issues the dV K steps of those columns
+// (kk = 0, 2, 4, 6 across the four warpgroups) while the second 16 are exponentiated.
+#ifndef FCPB_BWD_PSPLIT
+#define FCPB_BWD_PSPLIT 1
+#endif
+constexpr bool kPSplit = FCPB_BWD_PSPLIT != 0;
+
 template <bool kMask>
 FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t (&pk)[16], uint32_t t_p,
-                      bool kv_live, int col0, int q_valid, int shift) {
+                      bool kv_live, int col0, int q_valid, int shift, uint64_t* p_half) {
   const float2 c2 = make_float2(sl2, sl2);
 #pragma unroll
   for (int c8 = 0; c8 < 4; ++c8) {
+    if (kPSplit && c8 == 2) {
+      tmem_st8(t_p, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_half);
+    }
     const float4 la = lds128(l2 + c8 * 32), lb = lds128(l2 + c8 * 32 + 16);
     const float2 nl[4] = {make_float2(la.x, la.y), make_float2(la.z, la.w),
                           make_float2(lb.x, lb.y), make_float2(lb.z, lb.w)};
@@ -201,7 +215,8 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t 
       pk[c8 * 4 + u] = pack_bf16(p0, p1);
     }
   }
-  tmem_st16(t_p, pk);
+  if (kPSplit) tmem_st8(t_p + 8, pk + 8);
+  else tmem_st16(t_p, pk);
 }
 
 // Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds, and (when gdst is
@@ -273,6 +288,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.dp_full, 1);
+    mbar_init(&sm.p_half, 128 * kSoftmaxWGs);
     mbar_init(&sm.p_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.ds_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.acc_full, 1);
@@ -392,13 +408,16 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         __syncwarp();
       };
       // dV += P^T dO  /  dK += dS^T Q:  A from TMEM, B = the [q, d] tile (MN-major).
+      // kk_par: -1 all K steps; 0 / 1 the even / odd ones (first / second 16 columns of
+      // every warpgroup's slice, the split-P halves)
       auto issue_acc = [&](uint32_t a_base, uint32_t b_base, uint32_t col, bool acc, uint64_t* done,
-                           uint64_t* done2 = nullptr) {
+                           uint64_t* done2 = nullptr, int kk_par = -1) {
         if (leader) {
 #pragma unroll
           for (int kk = 0; kk < kBQ / 16; ++kk)
-            mma_ts(tmem + col, tmem + a_col(a_base, kk),
-                   smem_desc_sw128(b_base + kk * 2048, kQPanel, 1024), id_acc, acc || kk > 0);
+            if (kk_par < 0 || (kk & 1) == kk_par)
+              mma_ts(tmem + col, tmem + a_col(a_base, kk),
+                     smem_desc_sw128(b_base + kk * 2048, kQPanel, 1024), id_acc, acc || kk > 0);
           if (done) mma_commit(done);
           if (done2) mma_commit(done2);
         }
@@ -430,15 +449,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           const uint32_t qcur = qr_.slot, dcur = dr_.slot;
           qr_.next();
           dr_.next();
+          if (kPSplit) {
+            mbar_wait(&sm.p_half, p_phase);
+            if (j == 0) {
+              mbar_wait(&sm.acc_free, acc_phase ^ 1);   // epilogue drained the previous item
+              acc_phase ^= 1;
+            }
+            tc_fence_after();
+            issue_acc(kColS, smem_u32(sm.dout[dcur]), kColDV, j > 0, nullptr, nullptr, 0);
+          }
           mbar_wait(&sm.p_full, p_phase);
           p_phase ^= 1;
           FCPB_TR(kTrPGot, (int)tile);
-          if (j == 0) {
+          if (!kPSplit && j == 0) {
             mbar_wait(&sm.acc_free, acc_phase ^ 1);   // epilogue drained the previous item
             acc_phase ^= 1;
           }
           tc_fence_after();
-          issue_acc(kColS, smem_u32(sm.dout[dcur]), kColDV, j > 0, nullptr);
+          // (split: kk = 0 of the tile was issued with the even half, so every odd step
+          // accumulates; acc || kk > 0 holds for them)
+          issue_acc(kColS, smem_u32(sm.dout[dcur]), kColDV, j > 0, nullptr, nullptr, kPSplit ? 1 : -1);
           FCPB_TR(kTrDvIssue, (int)tile);
           if (j + 1 < n) {
             mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
@@ -518,9 +548,9 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               tmem_wait_ld();
               FCPB_TR(kTrSLd, (int)tile);
               if (plain)
-                p_chunk<false>(sv, l2, sl2, pr, t_s, true, 0, 0, 0);
+                p_chunk<false>(sv, l2, sl2, pr, t_s, true, 0, 0, 0, &sm.p_half);
               else
-                p_chunk<true>(sv, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift);
+                p_chunk<true>(sv, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift, &sm.p_half);
             }
             FCPB_TR(kTrPSt, (int)tile);
             tmem_wait_st();

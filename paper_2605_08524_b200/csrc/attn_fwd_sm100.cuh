@@ -55,7 +55,7 @@ struct Smem {
   uint8_t kv[kSlots][kTileBytes];     // 128 KB
   uint64_t q_full, q_empty;
   uint64_t kv_full[kSlots], kv_empty[kSlots];
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t s_full[2], p_part[2], p_full[2], o_full[2], o_empty[2];
   SchedRing sched;
   uint32_t tmem_base;
 };
@@ -104,22 +104,45 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
 #endif
 constexpr int kPolyPairs = FCPB_FWD_POLY_PAIRS;
 template <bool kPoly>
-FCPB_DEV float exp_row(const float (&s)[kBN], float sl2, float neg, uint32_t t_s) {
+FCPB_DEV void exp_chunk(const float (&s)[kBN], int c, float sl2, float neg, uint32_t t_s, float2 (&sp2)[2]) {
+  uint32_t pk[16];
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {
+    const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
+                                make_float2(sl2, sl2), make_float2(neg, neg));
+    float2 e;
+    if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
+    else e = make_float2(ex2(x.x), ex2(x.y));
+    sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+    pk[i / 2] = pack_bf16(e.x, e.y);
+  }
+  tmem_st16(t_s + c * 16, pk);
+}
+
+// Split P arrival (FA4-style): after the first kPSplit of the four 32-column chunks of P are
+// in TMEM the softmax warps arrive on p_part, and the MMA warp issues those K steps of
+// O += P V while the last chunk is still being exponentiated; p_full releases the rest.
+// The O rescale (rare) therefore happens before the exponentials.
+#ifndef FCPB_FWD_PSPLIT
+#define FCPB_FWD_PSPLIT 3
+#endif
+constexpr int kPSplit = FCPB_FWD_PSPLIT;
+static_assert(kPSplit >= 0 && kPSplit < 4, "P split point in 32-column chunks");
+
+// One row of a 128-column S tile: P = exp2(s*sl2 + neg) as bf16 pairs into TMEM at t_s
+// (16 columns per 32 scores); arrives on p_part after kPSplit chunks; returns the row sum.
+// kPoly: pairs 8u+8-kPolyPairs..8u+7 use ex2_poly2 (finite inputs only).
+template <bool kPoly>
+FCPB_DEV float exp_row(const float (&s)[kBN], float sl2, float neg, uint32_t t_s, uint64_t* p_part) {
   float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int c = 0; c < kBN / 32; ++c) {
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 32; i += 2) {
-      const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
-                                  make_float2(sl2, sl2), make_float2(neg, neg));
-      float2 e;
-      if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
-      else e = make_float2(ex2(x.x), ex2(x.y));
-      sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
-      pk[i / 2] = pack_bf16(e.x, e.y);
+    exp_chunk<kPoly>(s, c, sl2, neg, t_s, sp2);
+    if (kPSplit > 0 && c + 1 == kPSplit) {
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_part);
     }
-    tmem_st16(t_s + c * 16, pk);
   }
   return (sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y);
 }
@@ -162,6 +185,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
     for (int h = 0; h < 2; ++h) {
       mbar_init(&sm.s_full[h], 1);
+      mbar_init(&sm.p_part[h], 128);
       mbar_init(&sm.p_full[h], 128);
       mbar_init(&sm.o_full[h], 1);
       mbar_init(&sm.o_empty[h], 128);
@@ -243,16 +267,30 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         }
         __syncwarp();
       };
-      auto issue_pv = [&](int h, uint32_t vslot, bool acc) {
+      // O_h += P_h V over K steps [kk0, kk1) (16 kv rows each)
+      auto issue_pv = [&](int h, uint32_t vslot, bool acc, int kk0, int kk1) {
         if (leader) {
           const uint32_t vb = smem_u32(sm.kv[vslot]);
   #pragma unroll
           for (int kk = 0; kk < kBN / 16; ++kk) {
+            if (kk < kk0 || kk >= kk1) continue;
             mma_ts(tmem + col_o(h), tmem + col_s(h) + kk * 8,
                    smem_desc_sw128(vb + kk * 2048, kHalfBytes, 1024), id_o, (acc || kk > 0));
           }
         }
         __syncwarp();
+      };
+      constexpr int kKkSplit = kPSplit * 2;     // K steps covered by the first P chunks
+      // wait for P_h(j) (in two parts when split) and issue O_h += P_h V_j
+      auto pv = [&](int h, uint32_t vslot, bool acc) {
+        if (kPSplit > 0) {
+          mbar_wait(&sm.p_part[h], p_phase);
+          tc_fence_after();
+          issue_pv(h, vslot, acc, 0, kKkSplit);
+        }
+        mbar_wait(&sm.p_full[h], p_phase);
+        tc_fence_after();
+        issue_pv(h, vslot, acc, kPSplit > 0 ? kKkSplit : 0, kBN / 16);
       };
       auto commit = [&](uint64_t* bar) {
         if (leader) mma_commit(bar);
@@ -288,10 +326,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         if (n == 1) commit(&sm.q_empty);
         for (int j = 0; j < n; ++j) {
           const uint32_t vs = take_full();
-          mbar_wait(&sm.p_full[0], p_phase);
-          FCPB_FWTR(kFwP0Got, trt);
-          tc_fence_after();
-          issue_pv(0, vs, j > 0);
+          pv(0, vs, j > 0);
           FCPB_FWTR(kFwPv0Issue, trt);
           if (j == n - 1) commit(&sm.o_full[0]);
           uint32_t ks2 = 0;
@@ -302,10 +337,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
             issue_s(0, ks2);
             FCPB_FWTR(kFwS0Issue, trt + 1);
           }
-          mbar_wait(&sm.p_full[1], p_phase);
-          FCPB_FWTR(kFwP1Got, trt);
-          tc_fence_after();
-          issue_pv(1, vs, j > 0);
+          pv(1, vs, j > 0);
           FCPB_FWTR(kFwPv1Issue, trt);
           commit(&sm.kv_empty[vs]);
           if (j == n - 1) commit(&sm.o_full[1]);
@@ -390,29 +422,31 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (m_run == -INFINITY) m_use = (mx == -INFINITY) ? 0.f : mx;
           else m_use = ((mx - m_run) * sl2 > 8.f) ? mx : m_run;
           const float neg = -m_use * sl2;
-          // P (bf16 pairs) overwrites the first 64 columns of S, 16 columns per 32 scores.
-          // Unmasked tiles (finite scores, x <= 8) send kPolyPairs of every 8 pairs to the
-          // FMA pipe (FA4-style): two softmax warps per SMSP otherwise need 2 x 128 ex2 x 8
-          // MUFU cycles per KV tile, as long as the tile's tensor work.  Masked tiles keep
-          // exact zeros from MUFU ex2(-inf).  The choice is CTA-uniform.
-          const bool poly = !(diag && t == it.mblock) && valid >= kBN;
-          const float sum = poly ? exp_row<true>(s, sl2, neg, t_s) : exp_row<false>(s, sl2, neg, t_s);
           const float alpha = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_use) * sl2);
-          l_run = l_run * alpha + sum;
-          // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.
+          // tcgen05.ld/st are .sync.aligned: the rescale decision must be warp-uniform.  It runs
+          // before the exponentials, so the first P chunks can release their PV K steps.
           if (!first && __any_sync(0xffffffffu, alpha != 1.f)) {
             // O_h(j-1) is final here: S_h(j) completed after PV_h(j-1) in the tensor pipe.
             if (lane_id() == 0) atomicAdd(&g_rescales, 1ull);
-#pragma unroll
-            for (int c = 0; c < kD / 32; ++c) {
-              uint32_t v[32];
-              tmem_ld32(t_o + c * 32, v);
+            // 16 columns at a time: the 128 scores of the row are live here
+#pragma unroll 1
+            for (int c = 0; c < kD / 16; ++c) {
+              uint32_t v[16];
+              tmem_ld16(t_o + c * 16, v);
               tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-              tmem_st32(t_o + c * 32, v);
+              for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+              tmem_st16(t_o + c * 16, v);
             }
           }
+          // P (bf16 pairs) overwrites the first 64 columns of S, 16 columns per 32 scores.
+          // Unmasked tiles (finite scores, x <= 8) send kPolyPairs of every 8 pairs to the
+          // FMA pipe (FA4-style).  Masked tiles keep exact zeros from MUFU ex2(-inf).  The
+          // choice is CTA-uniform.
+          const bool poly = !(diag && t == it.mblock) && valid >= kBN;
+          const float sum = poly ? exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h])
+                                 : exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
+          l_run = l_run * alpha + sum;
           m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;
           tmem_wait_st();

@@ -352,7 +352,8 @@ class FcpExecutor:
         send = recv = 0.0
         if xb:
             rate = xb["fwd_kv_pull"]["bytes"] / max(xb["fwd_kv_pull"]["ms"] * 1e-3, 1e-12)
-            send, recv = b["fwd_send"] / rate, b["fwd_recv"] / rate
+            if rate > 0:                # a rank that receives nothing has no pull rate
+                send, recv = b["fwd_send"] / rate, b["fwd_recv"] / rate
         stages = []
         if self.xchg is not None and self.stages:
             for s_idx in range(len(self.stages)):
@@ -379,6 +380,12 @@ class FcpExecutor:
         flops = 3.5 * float(sum(loads.compute_flops))      # distributor.py:151-155 accounting
         nbytes = int(sum(e.nbytes for st in self.result.plan.stages for e in st))
         return SimReport(t_max, per, stages, flops, nbytes)
+
+    def attention(self, q, k, v, return_lse: bool = False):
+        """Differentiable attention through this executor (``attention.fcp_attention``):
+        ``loss.backward()`` runs ``backward`` -- the dK/dV return included -- on every rank."""
+        from .attention import fcp_attention
+        return fcp_attention(q, k, v, self, return_lse)
 
     def step(self, q, k, v, do):
         """One attention layer fwd+bwd; returns (o, lse, dq, dk, dv)."""

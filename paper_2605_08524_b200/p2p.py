@@ -287,13 +287,15 @@ class SymmetricExchange:
         """Copy-engine pulls of stage s's KV chunks into the receive arena ``kv_recv``
         ([2, R, Hkv, D] bf16: the K plane then the V plane), one 2-D copy per merged run
         (ordered on the current stream)."""
+        pulls = self.stage_pulls[s]
+        if not pulls:                  # e.g. a rank that receives nothing in this stage
+            return
         base, dpitch, row = self._planes(kv_recv)
         spitch = self.t_max * row
 
         def pull(p, stream):
             native.copy_2d(base + p.dst * row, dpitch, self.peer_kv[p.peer].data_ptr() + p.src * row,
                            spitch, p.rows * row, 2, stream)
-        pulls = self.stage_pulls[s]
         self._fanout(pulls, sum(p.rows for p in pulls) * self.kv_row_bytes, pull)
 
     # ------------------------------------------------------------------ backward (K6)

@@ -4,23 +4,30 @@ Nothing here exists in the reference: it is the bridge from the plan the
 reference computes (``pipeline.py:31-60``) to the tiles its simulator only
 times (``simulator.py:73-109``).  For rank ``r``:
 
-* **Layout.**  Local chunks are packed token-major in unit-id order (members
-  in unit order); this is the layout of the rank's Q, K, V, O, dO, dQ, dK, dV.
-  Remote chunks the rank receives get slots in a *receive arena*, ordered by
-  the coalesced stage that delivers them, then by plan edge order
+* **Layout.**  Local chunks are packed token-major sorted by (sequence, chunk
+  index); this is the layout of the rank's Q, K, V, O, dO, dQ, dK, dV.  Remote
+  chunks the rank receives get slots in a *receive arena*, ordered by the
+  coalesced stage that delivers them, then by plan edge order
   (``simulator.py:112-133`` defines the arrival stage).
-* **Forward waves.**  Wave -1 holds every (Q chunk, KV chunk) tile whose KV is
+* **Runs.**  Consecutive chunks of one sequence held by the rank are one
+  contiguous *run*; a run is executed as one causal segment (its own diagonal
+  plus fully visible earlier sources), which computes exactly the tiles of its
+  chunks' ``q_to_kv`` lists with raggedness only at the run's end (checked
+  against ``q_to_kv`` per member chunk; otherwise one run per chunk).  At N=1
+  every sequence is one run.
+* **Forward waves.**  Wave -1 holds every (Q run, KV source) tile whose KV is
   local -- the dependency-free prologue; wave s holds tiles whose KV arrives
-  with coalesced stage s.  A Q chunk whose tiles span several waves writes one
-  fp32 partial (O, LSE) per wave, merged by K3 afterwards; a Q chunk served by
+  with coalesced stage s.  A Q run whose tiles span several waves writes one
+  fp32 partial (O, LSE) per wave, merged by K3 afterwards; a Q run served by
   a single wave writes its final bf16 O directly.
-* **Backward.**  dK/dV work is keyed by KV chunk (local or received): the KV
-  block iterates over every local Q chunk attending to it.  Received chunks form
-  their own launch so their dK/dV partials can travel back along the reversed
-  plan edges while the local chunks compute.  dQ is query-stationary: one
-  segment per local Q chunk over all of its (by then resident) KV chunks.
+* **Backward.**  dK/dV work is keyed by KV source (received chunk or local run):
+  the KV block iterates over every local Q run attending to it.  Received chunks
+  form their own launch so their dK/dV partials can travel back along the
+  reversed plan edges while the local runs compute.  dQ is query-stationary: one
+  segment per local Q run over all of its (by then resident) KV sources.
 
-Work items are sorted longest-first (LPT over the persistent grid).
+Work items are sorted longest-first (LPT over the persistent grid).  Visible-pair
+accounting stays the reference's per-chunk ``tile_token_pairs``.
 """
 
 from __future__ import annotations
@@ -121,6 +128,9 @@ class RankWork:
 
 
 def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
+    """The rank's packed layout: its chunks sorted by (sequence, chunk index), so the
+    consecutive chunks of one sequence that the plan places here are adjacent in memory in
+    token order (``local_runs``); the receive arena in arrival-stage, then (sequence, chunk) order."""
     n = result.assignment.n_workers
     if not 0 <= rank < n:
         raise ParameterError(f"rank {rank} outside [0, {n})")
@@ -129,6 +139,7 @@ def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
     for u in sorted(result.units, key=lambda u: u.unit_id):
         if result.assignment.worker_of(u.unit_id) == rank:
             chunks += [c.key for c in u.members]
+    chunks.sort()
     offset, pos = {}, 0
     for c in chunks:
         offset[c] = pos
@@ -137,11 +148,11 @@ def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
     arrival = arrival_stages(result.plan.stages, where)
     recv = []
     for s, stage in enumerate(result.plan.stages):
-        for e in stage:
-            if e.dst == rank:
-                for c in e.chunks:
-                    if arrival[(c, rank)] == s and c not in recv:
-                        recv.append(c)
+        got = sorted({c for e in stage if e.dst == rank for c in e.chunks if arrival[(c, rank)] == s})
+        # within a stage in (sequence, chunk) order: consecutive chunks of a sequence land in
+        # consecutive arena rows (one KV ref in the forward) and are pulled as one run from
+        # the owner, whose layout holds them in the same order
+        recv += [c for c in got if c not in recv]
     roff, rpos = {}, 0
     for c in recv:
         roff[c] = rpos
@@ -152,13 +163,104 @@ def rank_layout(result: ScheduleResult, rank: int) -> RankLayout:
                       frozenset(c for c in recv if c in needed))
 
 
-def _kv_location(lay: RankLayout, kv: ChunkKey) -> tuple[int, int, int]:
-    """(wave, arena offset, flags) of a KV chunk as seen from this rank."""
-    if kv in lay.offset:
-        return LOCAL_WAVE, lay.offset[kv], 0
-    if kv in lay.recv_offset:
-        return lay.recv_stage[kv], lay.recv_offset[kv], KV_RECV
-    raise ConsistencyError(f"plan never delivers chunk {kv} to rank {lay.rank}")
+@dataclass(frozen=True)
+class Run:
+    """Consecutive chunks ``first..last`` of sequence ``seq`` held by this rank, adjacent in
+    its layout: one contiguous token range [off, off + tokens) in sequence order."""
+    seq: int
+    first: int
+    last: int
+    off: int
+    tokens: int
+
+    @property
+    def key(self):
+        return ("run", self.seq, self.first, self.last)
+
+    def chunks(self):
+        return [(self.seq, i) for i in range(self.first, self.last + 1)]
+
+
+def local_runs(result: ScheduleResult, lay: RankLayout, merge: bool = True) -> list[Run]:
+    """Maximal runs of a rank's chunks (``merge=False``: one run per chunk).  The tile
+    geometry of the reference is per chunk (``kv_dependencies``, ``sharding.py:172-201``), and
+    a chunk of, say, 920 tokens pads to 8 x 128 rows; a run of consecutive chunks is one
+    causal range, so only its end is ragged.  At N=1 every sequence is one run, which on C2
+    cuts the 128x128 tiles computed from 17,688 to 14,836 (visible/computed 81% -> 97%).
+    Every run's dependency structure is checked against ``q_to_kv`` (``_run_sources``)."""
+    runs: list[Run] = []
+    for c in lay.chunks:
+        n = lay.chunk_tokens[c]
+        last = runs[-1] if runs else None
+        if (merge and last is not None and last.seq == c[0] and last.last + 1 == c[1]
+                and last.off + last.tokens == lay.offset[c]):
+            runs[-1] = Run(last.seq, last.first, c[1], last.off, last.tokens + n)
+        else:
+            runs.append(Run(c[0], c[1], c[1], lay.offset[c], n))
+    return runs
+
+
+def _run_sources(result: ScheduleResult, lay: RankLayout, runs: list[Run]):
+    """Per Q run, the KV sources its rows attend to: ("run", S, diag) for local runs (whole
+    runs only) and ("recv", chunk) for received chunks, in first-appearance order of the
+    members' ``q_to_kv`` lists.  Returns None if any member's visible set is not exactly
+    what the run segment encodes: every source fully visible, except the run itself, which
+    is causal at row level (chunk p sees chunks a..p-1 fully and itself inclusive-causally,
+    ``costmodel.py:141-149``) -- the caller then falls back to one run per chunk."""
+    deps = result.deps
+    causal = deps.mask == CAUSAL
+    run_of = {c: R for R in runs for c in R.chunks()}
+    out = {}
+    for R in runs:
+        members = R.chunks()
+        kv_all: list[ChunkKey] = []
+        seen = set()
+        for p in members:
+            for kv in deps.q_to_kv[p]:
+                if kv not in seen:
+                    seen.add(kv)
+                    kv_all.append(kv)
+        for p in members:
+            want = set(deps.q_to_kv[p])
+            got = set(kv_all)
+            if causal:
+                got -= {c for c in members if c[1] > p[1]}
+            if got != want:
+                return None
+        srcs, taken = [], set()
+        for kv in kv_all:
+            S = run_of.get(kv)
+            if S is None:
+                if kv not in lay.recv_offset:
+                    raise ConsistencyError(f"plan never delivers chunk {kv} to rank {lay.rank}")
+                srcs.append(("recv", kv))
+            elif S.key not in taken:
+                if not all(c in seen for c in S.chunks()):
+                    return None
+                taken.add(S.key)
+                srcs.append(("run", S, causal and S == R))
+        out[R.key] = srcs
+    return out
+
+
+def _runs_and_sources(result: ScheduleResult, lay: RankLayout):
+    import os
+    merge = os.environ.get("FCPB_RUNS", "1") != "0"     # A/B knob: 0 = one segment per chunk
+    runs = local_runs(result, lay, merge)
+    srcs = _run_sources(result, lay, runs)
+    if srcs is None:
+        runs = local_runs(result, lay, merge=False)
+        srcs = _run_sources(result, lay, runs)
+    return runs, srcs
+
+
+def _run_pairs(result: ScheduleResult, R: Run, keep) -> int:
+    """Visible pairs of the run's member chunks' tiles whose KV chunk satisfies keep(kv)
+    (the reference's ``tile_token_pairs`` accounting, per chunk tile)."""
+    deps = result.deps
+    causal = deps.mask == CAUSAL
+    return sum(tile_token_pairs(deps.chunk_tokens[p], deps.chunk_tokens[kv], causal and kv == p)
+               for p in R.chunks() for kv in deps.q_to_kv[p] if keep(kv))
 
 
 def _lpt_order(items):
@@ -174,112 +276,137 @@ def _lpt_order(items):
     return sorted(items, key=lambda t: (-t[0], t[1], t[2]))
 
 
+def _ref_cost(refs, mb) -> int:
+    cost = 0
+    for _, kn, flags, _ in refs:
+        nt = _cdiv(kn, TILE)
+        cost += min(nt, mb + 1) if flags & KV_DIAG else nt
+    return cost
+
+
+def _merge_refs(refs):
+    """Coalesce fully visible refs that continue each other in the same buffer (forward only:
+    the backward's KV blocks must stay aligned with its kvsegs)."""
+    out = []
+    for r in refs:
+        if (out and not (r[2] & KV_DIAG) and not (out[-1][2] & KV_DIAG) and out[-1][2] == r[2]
+                and out[-1][0] + out[-1][1] == r[0]):
+            out[-1] = (out[-1][0], out[-1][1] + r[1], r[2], 0)
+        else:
+            out.append(r)
+    return out
+
+
 def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = False) -> FwdPlan:
-    """Forward waves.  fuse_remote: every received KV chunk goes into one wave released by
-    this rank's last arrival stage (one launch, one tail, and at most a local and a remote
-    partial per Q chunk) instead of one wave per coalesced stage."""
+    """Forward waves over the rank's Q runs.  fuse_remote: every received KV chunk goes into
+    one wave released by this rank's last arrival stage (one launch, one tail, and at most a
+    local and a remote partial per Q run) instead of one wave per coalesced stage."""
     deps = result.deps
-    causal = deps.mask == CAUSAL
     last_stage = max(lay.recv_stage.values(), default=LOCAL_WAVE)
-    # per Q chunk: wave -> ordered kv list
-    per_q: dict[ChunkKey, dict[int, list[tuple[int, int, int, int]]]] = {}
-    for q in lay.chunks:
+    runs, sources = _runs_and_sources(result, lay)
+
+    def wave_of(kv):
+        if kv not in lay.recv_offset:
+            return LOCAL_WAVE
+        return last_stage if fuse_remote else lay.recv_stage[kv]
+
+    # per Q run: wave -> ordered kv refs
+    per_q: dict = {}
+    for R in runs:
         waves: dict[int, list] = {}
-        for kv in deps.q_to_kv[q]:
-            wave, off, flags = _kv_location(lay, kv)
-            if fuse_remote and wave != LOCAL_WAVE:
-                wave = last_stage
-            if causal and kv == q:
-                flags |= KV_DIAG
-            waves.setdefault(wave, []).append((off, deps.chunk_tokens[kv], flags, 0))
-        per_q[q] = waves
+        for src in sources[R.key]:
+            if src[0] == "run":
+                S, diag = src[1], src[2]
+                waves.setdefault(LOCAL_WAVE, []).append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
+            else:
+                kv = src[1]
+                waves.setdefault(wave_of(kv), []).append((lay.recv_offset[kv], deps.chunk_tokens[kv], KV_RECV, 0))
+        per_q[R.key] = {w: _merge_refs(r) for w, r in waves.items()}
 
     wave_ids = sorted({w for waves in per_q.values() for w in waves})
     part_rows = 0
-    partial_of: dict[ChunkKey, list[tuple[int, int]]] = {}   # q -> [(wave, row)]
-    seg_rows: dict[tuple[ChunkKey, int], int] = {}
-    for q in lay.chunks:
-        waves = per_q[q]
+    partial_of: dict = {}                 # run key -> [(wave, row)]
+    seg_rows: dict = {}
+    for R in runs:
+        waves = per_q[R.key]
         if len(waves) > 1:
             for w in sorted(waves):
-                seg_rows[(q, w)] = part_rows
-                partial_of.setdefault(q, []).append((w, part_rows))
-                part_rows += deps.chunk_tokens[q]
+                seg_rows[(R.key, w)] = part_rows
+                partial_of.setdefault(R.key, []).append((w, part_rows))
+                part_rows += R.tokens
     out = []
     for w in wave_ids:
         segs, refs, items, pairs = [], [], [], 0
-        for q in lay.chunks:
-            kvs = per_q[q].get(w)
+        for R in runs:
+            kvs = per_q[R.key].get(w)
             if not kvs:
                 continue
-            qn = deps.chunk_tokens[q]
             begin = len(refs)
             refs += kvs
-            for off, kn, flags, _ in kvs:
-                pairs += tile_token_pairs(qn, kn, bool(flags & KV_DIAG))
-            out_row = seg_rows.get((q, w), -1)
+            pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w)
+            out_row = seg_rows.get((R.key, w), -1)
             sidx = len(segs)
-            segs.append((lay.offset[q], qn, begin, len(refs), out_row, 0))
-            for mb in range(_cdiv(qn, TILE)):
-                cost = 0
-                for off, kn, flags, _ in kvs:
-                    nt = _cdiv(kn, TILE)
-                    cost += min(nt, mb + 1) if flags & KV_DIAG else nt
-                items.append((cost, sidx, mb, q[0]))
+            segs.append((R.off, R.tokens, begin, len(refs), out_row, 0))
+            for mb in range(_cdiv(R.tokens, TILE)):
+                items.append((_ref_cost(kvs, mb), sidx, mb, R.seq))
         items = _lpt_order(items)
         out.append(FwdWave(
             w, np.asarray(segs, dtype=np.int32).reshape(-1, 6),
             np.asarray(refs, dtype=np.int32).reshape(-1, 4),
-            np.asarray([(s, m) for _, s, m, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
+            np.asarray([(s_, m) for _, s_, m, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
             np.asarray([c for c, _, _, _ in items], dtype=np.int64)))
     groups, rows, tok = [], [], 0
-    for q in lay.chunks:
-        if q in partial_of:
+    for R in runs:
+        if R.key in partial_of:
             begin = len(rows)
-            rows += [r for _, r in partial_of[q]]
-            groups.append((lay.offset[q], deps.chunk_tokens[q], begin, len(rows), tok, 0))
-            tok += deps.chunk_tokens[q]
+            rows += [r for _, r in partial_of[R.key]]
+            groups.append((R.off, R.tokens, begin, len(rows), tok, 0))
+            tok += R.tokens
     return FwdPlan(out, part_rows, np.asarray(groups, dtype=np.int32).reshape(-1, 6),
                    np.asarray(rows, dtype=np.int32), tok)
 
 
 def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
+    """dK/dV launches keyed by KV source: received chunks (their partials travel back to
+    the owners) and local runs; each iterates the local Q runs that attend to it."""
     deps = result.deps
-    causal = deps.mask == CAUSAL
-    consumers: dict[ChunkKey, list[ChunkKey]] = {}
-    local = set(lay.chunks)
-    for q in lay.chunks:
-        for kv in deps.q_to_kv[q]:
-            consumers.setdefault(kv, []).append(q)
+    runs, sources = _runs_and_sources(result, lay)
+    consumers: dict = {}                  # kv key -> [(Q run, diag)]
+    kv_src: dict = {}                     # kv key -> (off, tokens, recv, chunk-or-run)
+    for R in runs:
+        for src in sources[R.key]:
+            if src[0] == "run":
+                S = src[1]
+                consumers.setdefault(S.key, []).append((R, src[2]))
+                kv_src[S.key] = (S.off, S.tokens, False, S)
+            else:
+                kv = src[1]
+                consumers.setdefault(kv, []).append((R, False))
+                kv_src[kv] = (lay.recv_offset[kv], deps.chunk_tokens[kv], True, kv)
     launches = []
     for recv in (True, False):
-        kv_list = lay.recv_chunks if recv else lay.chunks
+        keys = ([c for c in lay.recv_chunks if c in consumers] if recv else
+                [R.key for R in runs if R.key in consumers])
         kvsegs, qrefs, items, pairs = [], [], [], 0
         kv_keys, q_keys = [], []
-        for kv in kv_list:
-            qs = consumers.get(kv, [])
-            if not qs:
-                # a local chunk no local Q attends to, or a chunk this rank only relays
-                # (ring / ByteScale plans): no dK/dV work here
-                continue
-            kn = deps.chunk_tokens[kv]
-            off = lay.recv_offset[kv] if recv else lay.offset[kv]
+        for key in keys:
+            off, kn, _, what = kv_src[key]
+            qs = consumers[key]
             begin = len(qrefs)
-            for q in qs:
-                assert q in local
-                diag = int(causal and q == kv)
-                qrefs.append((lay.offset[q], deps.chunk_tokens[q], diag, 0))
-                q_keys.append(q)
-                pairs += tile_token_pairs(deps.chunk_tokens[q], kn, bool(diag))
+            for R, diag in qs:
+                qrefs.append((R.off, R.tokens, int(diag), 0))
+                q_keys.append(R.key)
+                members = set(what.chunks()) if isinstance(what, Run) else {what}
+                pairs += _run_pairs(result, R, lambda kv: kv in members)
             kidx = len(kvsegs)
             kvsegs.append((off, kn, KV_RECV if recv else 0, begin, len(qrefs), 0))
-            kv_keys.append(kv)
+            kv_keys.append(key)
             for nb in range(_cdiv(kn, TILE)):
                 cost = 0
-                for q in qs:
-                    qb = _cdiv(deps.chunk_tokens[q], TILE)
-                    cost += qb - nb if (causal and q == kv) else qb
-                items.append((cost, kidx, nb, kv[0]))
+                for R, diag in qs:
+                    qb = _cdiv(R.tokens, TILE)
+                    cost += qb - nb if diag else qb
+                items.append((cost, kidx, nb, key[0] if recv else key[1]))
         if not kvsegs:
             continue
         items = _lpt_order(items)
@@ -292,29 +419,29 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
 
 
 def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
+    """Query-stationary dQ tables: one segment per local Q run over all of its KV sources,
+    segmented exactly like the backward's kvsegs (so materialised dS tiles line up)."""
     deps = result.deps
-    causal = deps.mask == CAUSAL
+    runs, sources = _runs_and_sources(result, lay)
     segs, refs, items, pairs = [], [], [], 0
     q_keys, kv_keys = [], []
-    for q in lay.chunks:
-        qn = deps.chunk_tokens[q]
+    for R in runs:
         begin = len(refs)
-        q_keys.append(q)
-        for kv in deps.q_to_kv[q]:
-            kv_keys.append(kv)
-            _, off, flags = _kv_location(lay, kv)
-            if causal and kv == q:
-                flags |= KV_DIAG
-            refs.append((off, deps.chunk_tokens[kv], flags, 0))
-            pairs += tile_token_pairs(qn, deps.chunk_tokens[kv], bool(flags & KV_DIAG))
+        q_keys.append(R.key)
+        for src in sources[R.key]:
+            if src[0] == "run":
+                S, diag = src[1], src[2]
+                kv_keys.append(S.key)
+                refs.append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
+            else:
+                kv = src[1]
+                kv_keys.append(kv)
+                refs.append((lay.recv_offset[kv], deps.chunk_tokens[kv], KV_RECV, 0))
+        pairs += _run_pairs(result, R, lambda kv: True)
         sidx = len(segs)
-        segs.append((lay.offset[q], qn, begin, len(refs), -1, 0))
-        for mb in range(_cdiv(qn, TILE)):
-            cost = 0
-            for off, kn, flags, _ in refs[begin:]:
-                nt = _cdiv(kn, TILE)
-                cost += min(nt, mb + 1) if flags & KV_DIAG else nt
-            items.append((cost, sidx, mb, q[0]))
+        segs.append((R.off, R.tokens, begin, len(refs), -1, 0))
+        for mb in range(_cdiv(R.tokens, TILE)):
+            items.append((_ref_cost(refs[begin:], mb), sidx, mb, R.seq))
     items = _lpt_order(items)
     return DqPlan(np.asarray(segs, dtype=np.int32).reshape(-1, 6),
                   np.asarray(refs, dtype=np.int32).reshape(-1, 4),

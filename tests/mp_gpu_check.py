@@ -68,6 +68,13 @@ def main():
     for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))
     ok = within_fixed_caps(rep)
+    # the same step through torch.autograd (fcp_attention over the executor, N ranks)
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in loc[:3])
+    og = ex.attention(qg, kg, vg)
+    (og.float() * loc[3].float()).sum().backward()
+    autograd_same = (torch.equal(og.detach(), o) and torch.equal(qg.grad, dq) and torch.equal(kg.grad, dk)
+                     and torch.equal(vg.grad, dv))
+    ok = ok and autograd_same
     # transparent reshuffler (§8f): user layout -> FCP layout equals the executor's inputs
     # exactly, and the round trip is the identity (symmetric-memory copy-engine pulls)
     from paper_2605_08524_b200.reshuffle import Reshuffler, user_layouts
@@ -88,7 +95,7 @@ def main():
     mr = ex.measured_report(*loc, reps=2)
     ok = ok and len(mr.per_worker) == world and len(mr.stages) == len(ex.stages) \
         and mr.total_time > 0 and all(w.compute_time > 0 for w in mr.per_worker) and mr.total_flops > 0
-    print(json.dumps({"rank": rank, "world": world, "shared_gpu": shared, "recv_tokens": lay.recv_tokens,
+    print(json.dumps({"rank": rank, "world": world, "shared_gpu": shared, "autograd_same": autograd_same, "recv_tokens": lay.recv_tokens,
                       "stages": len(ex.stages), "ok": ok, "errors": rep,
                       "measured_total_ms": mr.total_time * 1e3,
                       "reshuffle_ok": reshuffle_ok, "reshuffle_to_fcp_ms": t0.elapsed_time(t1),

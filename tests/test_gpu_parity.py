@@ -286,3 +286,44 @@ def test_dkv_finalize_matches_ordered_fp32_sum():
     torch.cuda.synchronize()
     assert torch.equal(out_k.cpu(), ref_k.to(torch.bfloat16))
     assert torch.equal(out_v.cpu(), ref_v.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("runner", ["executor", "block_attention"])
+def test_autograd_fcp_attention(runner):
+    """``fcp_attention`` under ``loss.backward()`` (torch.autograd.Function over the executor
+    and over a single-rank BlockAttention) against the fp64 oracle, same tolerance."""
+    import math
+    from oracle.attention_ref import mono_bwd, mono_fwd
+    from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows
+    from paper_2605_08524_b200.attention import BlockAttention, fcp_attention
+    from paper_2605_08524_b200.executor import FcpExecutor
+    from paper_2605_08524_b200.worklist import build_rank_work
+    model = GQA_SMALL
+    r = schedule([1500, 700, 300, 129, 40], 1, 512, model)
+    goff, T = global_offsets(r)
+    q, k, v, do = make_inputs(T, model)
+    dev = torch.device("cuda", 0)
+    if runner == "executor":
+        run = FcpExecutor(r, 0, model, dev)
+        lay = run.layout
+    else:
+        work = build_rank_work(r, 0)
+        run, lay = BlockAttention(work, model, dev), work.layout
+    ql, kl, vl, dol = (gather_rank(x, lay, goff, r.deps).to(dev) for x in (q, k, v, do))
+    ql.requires_grad_(True)
+    kl.requires_grad_(True)
+    vl.requires_grad_(True)
+    o, lse = fcp_attention(ql, kl, vl, run, return_lse=True)
+    (o.float() * dol.float()).sum().backward()
+    rows = global_sequence_rows(r)
+    scale = 1 / math.sqrt(model.head_dim)
+    qf, kf, vf, dof = (x.double() for x in (q, k, v, do))
+    ro, rl = mono_fwd(qf, kf, vf, rows, scale)
+    rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
+    g = lambda x: gather_rank(x, lay, goff, r.deps)
+    rep = {n: err(t.detach().cpu(), g(ref)) for n, t, ref in
+           (("o", o, ro), ("lse", lse, rl), ("dq", ql.grad, rdq), ("dk", kl.grad, rdk), ("dv", vl.grad, rdv))}
+    b = bf16_reference(r, model, q, k, v, do)
+    brep = {n: err(g(b[n]), g(ref)) for n, ref in (("o", ro), ("lse", rl), ("dq", rdq), ("dk", rdk), ("dv", rdv))}
+    _report(f"autograd through {runner}", tolerance_report(rep, brep))
+    assert_within_tolerance(rep, brep)
