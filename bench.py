@@ -492,7 +492,12 @@ def main():
     # Energy per step: the NVML energy counter needs a window of about a second, so it is read
     # over a separate untimed loop of at least 1.5 s (the timed region may be shorter).
     energy = None
-    e_steps = max(args.steps, int(math.ceil(1500.0 / max(ms, 1e-3))))
+    # every rank must run the same number of steps (the exchange's flag barriers are
+    # collective): size the loop from the max-over-ranks step time
+    t_e = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+    e_steps = max(args.steps, int(math.ceil(1500.0 / max(t_e.item(), 1e-3))))
     with ClockSampler(local) as eclk:
         torch.cuda.synchronize()
         for _ in range(e_steps):

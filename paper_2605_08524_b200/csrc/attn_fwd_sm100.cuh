@@ -103,8 +103,15 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
 #define FCPB_FWD_POLY_PAIRS 0    // measured: 2/3/4 pairs cost +1/+3/+6% fwd cycles (issue-bound)
 #endif
 constexpr int kPolyPairs = FCPB_FWD_POLY_PAIRS;
+// Row sum off the P chain (FA4-style): the exponentials overwrite the scores in registers
+// and are summed after P is released to the MMA warp (FCPB_FWD_LATESUM=0: summed inline).
+#ifndef FCPB_FWD_LATESUM
+#define FCPB_FWD_LATESUM 0    // 1: +8% K1 cycles on C2 (ncu A/B r02), so off
+#endif
+constexpr bool kLateSum = FCPB_FWD_LATESUM != 0;
+
 template <bool kPoly>
-FCPB_DEV void exp_chunk(const float (&s)[kBN], int c, float sl2, float neg, uint32_t t_s, float2 (&sp2)[2]) {
+FCPB_DEV void exp_chunk(float (&s)[kBN], int c, float sl2, float neg, uint32_t t_s, float2 (&sp2)[2]) {
   uint32_t pk[16];
 #pragma unroll
   for (int i = 0; i < 32; i += 2) {
@@ -113,10 +120,24 @@ FCPB_DEV void exp_chunk(const float (&s)[kBN], int c, float sl2, float neg, uint
     float2 e;
     if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
     else e = make_float2(ex2(x.x), ex2(x.y));
-    sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+    if (kLateSum) {
+      s[c * 32 + i] = e.x;
+      s[c * 32 + i + 1] = e.y;
+    } else {
+      sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+    }
     pk[i / 2] = pack_bf16(e.x, e.y);
   }
   tmem_st16(t_s + c * 16, pk);
+}
+
+// Sum of the 128 exponentials left in s by exp_chunk (kLateSum), 4 independent chains.
+FCPB_DEV float row_sum(const float (&s)[kBN]) {
+  float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int i = 0; i < kBN; i += 2) a[(i >> 1) & 3] = __fadd2_rn(a[(i >> 1) & 3], make_float2(s[i], s[i + 1]));
+  const float2 b = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+  return b.x + b.y;
 }
 
 // Split P arrival (FA4-style): after the first kPSplit of the four 32-column chunks of P are
@@ -124,7 +145,7 @@ FCPB_DEV void exp_chunk(const float (&s)[kBN], int c, float sl2, float neg, uint
 // O += P V while the last chunk is still being exponentiated; p_full releases the rest.
 // The O rescale (rare) therefore happens before the exponentials.
 #ifndef FCPB_FWD_PSPLIT
-#define FCPB_FWD_PSPLIT 3
+#define FCPB_FWD_PSPLIT 2    // ncu A/B on C2 (r02): 2 chunks -1.8% cycles, 3 chunks +0.8%, off 0
 #endif
 constexpr int kPSplit = FCPB_FWD_PSPLIT;
 static_assert(kPSplit >= 0 && kPSplit < 4, "P split point in 32-column chunks");
@@ -133,7 +154,7 @@ static_assert(kPSplit >= 0 && kPSplit < 4, "P split point in 32-column chunks");
 // (16 columns per 32 scores); arrives on p_part after kPSplit chunks; returns the row sum.
 // kPoly: pairs 8u+8-kPolyPairs..8u+7 use ex2_poly2 (finite inputs only).
 template <bool kPoly>
-FCPB_DEV float exp_row(const float (&s)[kBN], float sl2, float neg, uint32_t t_s, uint64_t* p_part) {
+FCPB_DEV float exp_row(float (&s)[kBN], float sl2, float neg, uint32_t t_s, uint64_t* p_part) {
   float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
   for (int c = 0; c < kBN / 32; ++c) {
@@ -289,6 +310,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           issue_pv(h, vslot, acc, 0, kKkSplit);
         }
         mbar_wait(&sm.p_full[h], p_phase);
+        if (h == 0) FCPB_FWTR(kFwP0Got, trt); else FCPB_FWTR(kFwP1Got, trt);
         tc_fence_after();
         issue_pv(h, vslot, acc, kPSplit > 0 ? kKkSplit : 0, kBN / 16);
       };
@@ -446,13 +468,13 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           const bool poly = !(diag && t == it.mblock) && valid >= kBN;
           const float sum = poly ? exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h])
                                  : exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
-          l_run = l_run * alpha + sum;
           m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&sm.p_full[h]);
           if (h == 0) FCPB_FWTR(kFwP0Arrive, trt); else FCPB_FWTR(kFwP1Arrive, trt);
+          l_run = l_run * alpha + (kLateSum ? row_sum(s) : sum);
           ++trt;
         }
       }
