@@ -567,11 +567,39 @@ def main():
             torch.cuda.synchronize()
             tms.append((a.elapsed_time(b), b.elapsed_time(c)))
         to_ms, from_ms = sorted(tms)[len(tms) // 2]
-        t = torch.tensor([to_ms, from_ms], device=device)
+        # measured hiding of the to-FCP reshuffle behind the PRE_WAVE tiles (rows that stay
+        # on their rank): sequential (reshuffle Q/K/V, then forward) vs forward_user
+        ex_u = FcpExecutor(result, rank, cfg, device, resident=rs.resident_chunks())
+        pre_pairs = sum(wv.pairs for wv in ex_u.work.fwd.waves if wv.stage == -2)
+        seq_t, ovl_t, to3_t = [], [], []
+        for it in range(5):
+            for mode in ("to3", "seq", "ovl"):
+                barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                if mode == "to3":
+                    rs.to_fcp(*usr[:3])
+                elif mode == "seq":
+                    qf, kf, vf = rs.to_fcp(*usr[:3])
+                    ex_u.forward(qf, kf, vf)
+                else:
+                    ex_u.forward_user(rs, *usr[:3])
+                b.record(stream)
+                torch.cuda.synchronize()
+                if it:
+                    {"to3": to3_t, "seq": seq_t, "ovl": ovl_t}[mode].append(a.elapsed_time(b))
+        med = lambda xs: sorted(xs)[len(xs) // 2]
+        t = torch.tensor([to_ms, from_ms, med(seq_t), med(ovl_t), med(to3_t)], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rc = reshuffle_cost(default_contiguous_layout(result.units, n), result.assignment, result.units,
                             result.deps, B200_HARDWARE, cfg, _EFF)
         reshuffle = {"to_fcp_ms_max_over_ranks": t[0].item(), "from_fcp_ms_max_over_ranks": t[1].item(),
+                     "fwd_after_to_fcp_ms": t[2].item(), "fwd_user_overlapped_ms": t[3].item(),
+                     "to_fcp_qkv_ms": t[4].item(),
+                     "hidden_fraction_measured": max(0.0, min(1.0, (t[2].item() - t[3].item()) / t[4].item()))
+                     if t[4].item() > 0 else None,
+                     "pre_wave_pairs_rank0": pre_pairs,
                      "reference_model": {"to_fcp_ms_at_900GBps": rc.time * 1e3,
                                          "hidden_fraction": rc.hidden_fraction,
                                          "total_bytes": rc.total_bytes}}

@@ -30,13 +30,13 @@ from . import exchange
 from .attention import BlockAttention
 from .costmodel import ModelConfig
 from .pipeline import ScheduleResult, plan_digest
-from .worklist import LOCAL_WAVE, build_rank_work
+from .worklist import LOCAL_WAVE, PRE_WAVE, build_rank_work
 
 
 class FcpExecutor:
     def __init__(self, result: ScheduleResult, rank: int, cfg: ModelConfig, device=None,
                  group=None, softmax_scale=None, num_ctas: int = 0, check_plan: bool = True,
-                 comm_sms: int | None = None):
+                 comm_sms: int | None = None, resident=None):
         self.result = result
         self.rank = rank
         self.world = result.assignment.n_workers
@@ -45,10 +45,13 @@ class FcpExecutor:
         self.group = group
         if check_plan and self.world > 1:
             exchange.sync_plan_digest(plan_digest(result, cfg), group)
-        self.work = build_rank_work(result, rank)
+        # resident: chunks whose rows are in place before a reshuffle into the FCP layout
+        # completes (Reshuffler.resident_chunks); their local tiles form PRE_WAVE
+        self.resident = frozenset(resident or ())
+        self.work = build_rank_work(result, rank, resident=self.resident)
         self.fuse_remote = self._fuse_remote_waves(result, rank, cfg)
         if self.fuse_remote:
-            self.work = build_rank_work(result, rank, fuse_remote=True)
+            self.work = build_rank_work(result, rank, fuse_remote=True, resident=self.resident)
         self.layout = self.work.layout
         self.op = BlockAttention(self.work, cfg, self.device, softmax_scale, num_ctas)
         # The exchange runs on copy engines (p2p.SymmetricExchange), so the persistent
@@ -90,6 +93,7 @@ class FcpExecutor:
         self.v_recv = self.kv_recv[1] if R else None
         self.kv_bytes_per_token = 2 * Hk * D * 2
         self._marks = None          # optional per-phase CUDA-event timeline (see timeline())
+        self._rs_stream = None      # forward_user: the reshuffle's remote pulls
 
     def _fuse_remote_waves(self, result, rank, cfg) -> bool:
         """One remote forward wave instead of one per stage when this rank's pulls are
@@ -166,11 +170,19 @@ class FcpExecutor:
         return {"fwd_send": s, "fwd_recv": r, "bwd_send": 2 * r, "bwd_recv": 2 * s}
 
     # ------------------------------------------------------------------ forward
-    def forward(self, q, k, v):
+    def forward(self, q, k, v, pre_event=None):
+        """O, LSE of this rank's Q rows.  pre_event: the inputs are complete only once this
+        event has fired (a reshuffle still in flight, ``forward_user``); the PRE_WAVE tiles,
+        whose rows were in place before, run first, then the stream waits for it."""
         op = self.op
         cur = torch.cuda.current_stream(self.device)
         outs = op.alloc_forward_outputs()
         self._mark("step_begin", cur)
+        if PRE_WAVE in self.wave_of_stage:
+            op.forward_wave(self.wave_of_stage[PRE_WAVE], q, k, v, self.k_recv, self.v_recv, outs, cur)
+            self._mark("fwd_pre", cur)
+        if pre_event is not None:
+            cur.wait_event(pre_event)
         x = self.xchg
         events = []
         if x is not None and self.stages:
@@ -380,6 +392,23 @@ class FcpExecutor:
         flops = 3.5 * float(sum(loads.compute_flops))      # distributor.py:151-155 accounting
         nbytes = int(sum(e.nbytes for st in self.result.plan.stages for e in st))
         return SimReport(t_max, per, stages, flops, nbytes)
+
+    def forward_user(self, rs, q_u, k_u, v_u):
+        """Forward from the user's layout: the reshuffler
+        copies the rows that stay on this rank, its remote pulls into the FCP layout run on a
+        side stream, and the PRE_WAVE tiles (rows in place, build the executor with
+        ``resident=rs.resident_chunks()``) compute meanwhile.  K/V land directly in
+        ``kv_input_buffers`` (no publish copy at N > 1).  Returns the FCP-layout (q, k, v)
+        and (o, lse)."""
+        if self._rs_stream is None:
+            self._rs_stream = torch.cuda.Stream(device=self.device)
+        H, D = self.cfg.q_heads, self.cfg.head_dim
+        q = torch.empty((self.layout.tokens, H, D), dtype=q_u.dtype, device=self.device)
+        k, v = self.kv_input_buffers()
+        (q, k, v), ev = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens,
+                                 rs.plan.fcp_tokens, outs=[q, k, v], remote_stream=self._rs_stream)
+        o, lse = self.forward(q, k, v, pre_event=ev)
+        return (q, k, v), (o, lse)
 
     def attention(self, q, k, v, return_lse: bool = False):
         """Differentiable attention through this executor (``attention.fcp_attention``):

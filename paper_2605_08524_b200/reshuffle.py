@@ -145,6 +145,9 @@ class Reshuffler:
         self.device = torch.device(device)
         self.plans = reshuffle_plans(result, initial_layout)
         self.plan = self.plans[rank]
+        from .distributor import chunk_placement
+        owner = chunk_placement(result.assignment, result.units)
+        self._resident = {c for c in user_layouts(result, initial_layout)[rank].chunks if owner[c] == rank}
         H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
         self.row_cap = max_row_bytes or ((2 * H + 2 * Hk) * D * 2 + 4 * H)
         self.t_max = max(max(max(p.user_tokens, p.fcp_tokens) for p in self.plans), 1)
@@ -157,7 +160,13 @@ class Reshuffler:
         dist.barrier(group=group)                       # every rank's flags are zero
         self.bytes_moved = 0
 
-    def _move(self, tensors, pulls, rows_in: int, rows_out: int):
+    def _move(self, tensors, pulls, rows_in: int, rows_out: int, outs=None, remote_stream=None):
+        """Move rows of every tensor along `pulls`.  Rows that stay on this rank are copied
+        straight from the inputs on the current stream; the others go through the peers'
+        regions (publish, flag barrier, copy-engine pulls, flag barrier).  With
+        `remote_stream` that remote part runs there, concurrently with whatever the caller
+        queues next on the current stream, and the method returns (outs, event): the
+        outputs are complete once the current stream has also waited for the event."""
         widths, elems = [], []
         for t in tensors:
             if t.shape[0] != rows_in:
@@ -169,28 +178,52 @@ class Reshuffler:
             widths.append(row * t.element_size())
         if sum(widths) > self.row_cap:
             raise ParameterError(f"{sum(widths)} bytes per row exceed the reshuffler's {self.row_cap}")
+        if outs is None:
+            outs = [torch.empty((rows_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device)
+                    for t in tensors]
+        flat_in = [t.contiguous().reshape(rows_in, e) for t, e in zip(tensors, elems)]
+        flat_out = [o.view(rows_out, e) for o, e in zip(outs, elems)]
+        for src, dst in zip(flat_in, flat_out):           # rows that stay here: direct copies
+            for peer, s0, d, n in pulls:
+                if peer == self.rank:
+                    dst[d:d + n].copy_(src[s0:s0 + n], non_blocking=True)
         # one contiguous region per tensor (capacity t_max rows each): publish and pulls are
         # plain contiguous copies and the pulls land directly in the outputs (no unpack)
         region, acc = [], 0
         for w in widths:
             region.append(acc)
             acc += self.t_max * w
-        for t, w, e, off in zip(tensors, widths, elems, region):           # publish
-            self.buf[off:off + rows_in * w].view(rows_in, w).copy_(
-                t.contiguous().reshape(rows_in, e).view(torch.uint8), non_blocking=True)
-        self.flags.barrier(0)                  # every rank's rows published
-        outs = []
-        for t, w, e, off in zip(tensors, widths, elems, region):
-            o = torch.empty((rows_out,) + tuple(t.shape[1:]), dtype=t.dtype, device=self.device)
-            ob = o.view(rows_out, e).view(torch.uint8)
-            for peer, s0, d, n in pulls:
-                src = self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w)
-                ob[d:d + n].copy_(src, non_blocking=True)
-                if peer != self.rank:
+        cur = torch.cuda.current_stream(self.device)
+        st = remote_stream or cur
+        if remote_stream is not None:
+            remote_stream.wait_stream(cur)
+        with torch.cuda.stream(st):
+            for src, w, off in zip(flat_in, widths, region):                # publish
+                self.buf[off:off + rows_in * w].view(rows_in, w).copy_(src.view(torch.uint8),
+                                                                        non_blocking=True)
+            self.flags.barrier(0, st)              # every rank's rows published
+            for dst, w, off in zip(flat_out, widths, region):
+                ob = dst.view(torch.uint8)
+                for peer, s0, d, n in pulls:
+                    if peer == self.rank:
+                        continue
+                    ob[d:d + n].copy_(self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w),
+                                      non_blocking=True)
                     self.bytes_moved += n * w
-            outs.append(o)
-        self.flags.barrier(1)                  # every pull done: buffers reusable
-        return outs
+            self.flags.barrier(1, st)              # every pull done: buffers reusable
+        if remote_stream is None:
+            return outs
+        ev = torch.cuda.Event()
+        ev.record(remote_stream)
+        for t in list(tensors) + list(outs):
+            t.record_stream(remote_stream)
+        return outs, ev
+
+    def resident_chunks(self) -> frozenset:
+        """Chunks that stay on this rank (their to-FCP pull is local): build the executor with
+        ``FcpExecutor(..., resident=rs.resident_chunks())`` so their tiles run while the
+        remote pulls of ``FcpExecutor.forward_user`` are in flight."""
+        return frozenset(self._resident)
 
     def to_fcp(self, *tensors):
         """User-layout [T_user, ...] tensors -> FCP-layout [T_fcp, ...] tensors."""

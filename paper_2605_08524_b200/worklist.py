@@ -47,6 +47,7 @@ TILE = 128
 KV_DIAG = 1
 KV_RECV = 2
 LOCAL_WAVE = -1
+PRE_WAVE = -2        # local tiles whose data is already in place before a reshuffle completes
 
 
 def _cdiv(a: int, b: int) -> int:
@@ -297,27 +298,40 @@ def _merge_refs(refs):
     return out
 
 
-def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = False) -> FwdPlan:
+def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = False,
+                  resident=None) -> FwdPlan:
     """Forward waves over the rank's Q runs.  fuse_remote: every received KV chunk goes into
     one wave released by this rank's last arrival stage (one launch, one tail, and at most a
-    local and a remote partial per Q run) instead of one wave per coalesced stage."""
+    local and a remote partial per Q run) instead of one wave per coalesced stage.
+    resident: chunks whose Q/K/V rows are in place before the reshuffle into the FCP layout
+    completes (they stay on this rank); tiles of a resident Q run against a resident local run
+    form PRE_WAVE, which runs while the reshuffle pulls the other rows."""
     deps = result.deps
     last_stage = max(lay.recv_stage.values(), default=LOCAL_WAVE)
     runs, sources = _runs_and_sources(result, lay)
+    resident = frozenset(resident or ())
 
     def wave_of(kv):
         if kv not in lay.recv_offset:
             return LOCAL_WAVE
         return last_stage if fuse_remote else lay.recv_stage[kv]
 
+    def is_resident(run):
+        return all(c in resident for c in run.chunks())
+
+    pre_pairs: set = set()                 # (Q run key, KV chunk) tiles in PRE_WAVE
     # per Q run: wave -> ordered kv refs
     per_q: dict = {}
     for R in runs:
         waves: dict[int, list] = {}
+        r_res = is_resident(R)
         for src in sources[R.key]:
             if src[0] == "run":
                 S, diag = src[1], src[2]
-                waves.setdefault(LOCAL_WAVE, []).append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
+                w = PRE_WAVE if (r_res and is_resident(S)) else LOCAL_WAVE
+                if w == PRE_WAVE:
+                    pre_pairs.update((R.key, c) for c in S.chunks())
+                waves.setdefault(w, []).append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
             else:
                 kv = src[1]
                 waves.setdefault(wave_of(kv), []).append((lay.recv_offset[kv], deps.chunk_tokens[kv], KV_RECV, 0))
@@ -343,7 +357,12 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
                 continue
             begin = len(refs)
             refs += kvs
-            pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w)
+            if w == PRE_WAVE:
+                pairs += _run_pairs(result, R, lambda kv: (R.key, kv) in pre_pairs)
+            elif w == LOCAL_WAVE:
+                pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w and (R.key, kv) not in pre_pairs)
+            else:
+                pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w)
             out_row = seg_rows.get((R.key, w), -1)
             sidx = len(segs)
             segs.append((R.off, R.tokens, begin, len(refs), out_row, 0))
@@ -488,9 +507,10 @@ def build_ds_tiles(bwd: list[BwdLaunch], dq: DqPlan, causal: bool) -> int:
     return nxt
 
 
-def build_rank_work(result: ScheduleResult, rank: int, fuse_remote: bool = False) -> RankWork:
+def build_rank_work(result: ScheduleResult, rank: int, fuse_remote: bool = False,
+                    resident=None) -> RankWork:
     lay = rank_layout(result, rank)
-    fwd = build_forward(result, lay, fuse_remote)
+    fwd = build_forward(result, lay, fuse_remote, resident)
     bwd = build_backward(result, lay)
     dq = build_dq(result, lay)
     n_pairs = build_ds_tiles(bwd, dq, result.deps.mask == CAUSAL)

@@ -91,11 +91,23 @@ def main():
     reshuffle_ok = all(torch.equal(a, b) for a, b in zip(fcp_in, loc)) and \
         all(torch.equal(a, b) for a, b in zip(back, usr))
     ok = ok and reshuffle_ok
+    # forward from the user layout: remote reshuffle pulls overlapped with the PRE_WAVE tiles
+    # of the rows that stay here (an executor built with the reshuffler's resident chunks)
+    ex_u = FcpExecutor(r, rank, model, dev, resident=rs.resident_chunks())
+    usr3 = [x.clone() for x in usr[:3]]
+    (qf, kf, vf), (o_u, lse_u) = ex_u.forward_user(rs, *usr3)
+    torch.cuda.synchronize()
+    user_fwd_ok = torch.equal(qf, loc[0]) and torch.equal(kf, loc[1]) and torch.equal(vf, loc[2])
+    rep_u = {"o": err(o_u.cpu(), gather_rank(ro, lay, goff, r.deps)),
+             "lse": err(lse_u.cpu(), gather_rank(rl, lay, goff, r.deps))}
+    user_fwd_ok = user_fwd_ok and within_fixed_caps(rep_u)
+    ok = ok and user_fwd_ok
     # measured SimReport-shaped record (collective): one WorkerStats per rank, one record per stage
     mr = ex.measured_report(*loc, reps=2)
     ok = ok and len(mr.per_worker) == world and len(mr.stages) == len(ex.stages) \
         and mr.total_time > 0 and all(w.compute_time > 0 for w in mr.per_worker) and mr.total_flops > 0
-    print(json.dumps({"rank": rank, "world": world, "shared_gpu": shared, "autograd_same": autograd_same, "recv_tokens": lay.recv_tokens,
+    print(json.dumps({"rank": rank, "world": world, "shared_gpu": shared, "autograd_same": autograd_same, "user_fwd_ok": user_fwd_ok,
+                      "pre_wave": any(w.stage == -2 for w in ex_u.work.fwd.waves), "recv_tokens": lay.recv_tokens,
                       "stages": len(ex.stages), "ok": ok, "errors": rep,
                       "measured_total_ms": mr.total_time * 1e3,
                       "reshuffle_ok": reshuffle_ok, "reshuffle_to_fcp_ms": t0.elapsed_time(t1),

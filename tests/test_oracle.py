@@ -174,6 +174,38 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
         assert any(wk.fwd.partial_rows for wk in works)   # the merge path was exercised
 
 
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_prewave_for_reshuffle_matches_dense(n):
+    """Forward with a PRE_WAVE (the tiles whose chunks stay on their user-layout rank, run
+    while the reshuffle into the FCP layout is in flight): emulated == dense, and the pre
+    wave is non-empty, so its partials and the extra merge are exercised."""
+    from paper_2605_08524_b200.reshuffle import user_layouts
+    from paper_2605_08524_b200.worklist import PRE_WAVE
+    r = _schedule([1100, 513, 300, 129, 128, 127, 40, 1], n, 256)
+    owner = chunk_placement(r.assignment, r.units)
+    users = user_layouts(r)
+    goff, T = global_offsets(r)
+    q, k, v, _ = _inputs(T, 5)
+    scale = 1 / math.sqrt(MODEL.head_dim)
+    o_ref, l_ref = mono_fwd(q, k, v, global_sequence_rows(r), scale)
+    o = torch.zeros_like(q)
+    lse = torch.zeros_like(l_ref)
+    pre = 0
+    for w in range(n):
+        resident = {c for c in users[w].chunks if owner[c] == w}
+        work = build_rank_work(r, w, resident=resident)
+        pre += sum(1 for wv in work.fwd.waves if wv.stage == PRE_WAVE)
+        lay = work.layout
+        ql, kl, vl = (gather_rank(x, lay, goff, r.deps) for x in (q, k, v))
+        kr, vr = (gather_rank(x, lay, goff, r.deps, recv=True) for x in (k, v))
+        ow, lw = emulate_forward(work, ql, kl, vl, kr, vr, scale)
+        scatter_rank(ow, o, lay, goff, r.deps)
+        scatter_rank(lw, lse, lay, goff, r.deps)
+        assert work.pairs == build_rank_work(r, w).pairs       # same tiles, regrouped
+    assert pre > 0
+    assert torch.allclose(o, o_ref, atol=1e-9) and torch.allclose(lse, l_ref, atol=1e-9)
+
+
 def test_worklist_pairs_match_reference_accounting():
     """Visible pairs of all tiles == batch_token_pairs (reference costmodel.py:196-200)."""
     from paper_2605_08524_b200.costmodel import batch_token_pairs
