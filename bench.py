@@ -570,6 +570,10 @@ def main():
         # measured hiding of the to-FCP reshuffle behind the PRE_WAVE tiles (rows that stay
         # on their rank): sequential (reshuffle Q/K/V, then forward) vs forward_user
         ex_u = FcpExecutor(result, rank, cfg, device, resident=rs.resident_chunks())
+        # user-layout Q/K/V written where the reshuffler publishes them (no publish copy)
+        usr_qkv = rs.input_views([(tuple(x.shape[1:]), x.dtype) for x in usr[:3]])
+        for dst_, src_ in zip(usr_qkv, usr[:3]):
+            dst_.copy_(src_)
         pre_pairs = sum(wv.pairs for wv in ex_u.work.fwd.waves if wv.stage == -2)
         seq_t, ovl_t, to3_t = [], [], []
         for it in range(5):
@@ -579,12 +583,12 @@ def main():
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(stream)
                 if mode == "to3":
-                    rs.to_fcp(*usr[:3])
+                    rs.to_fcp(*usr_qkv)
                 elif mode == "seq":
-                    qf, kf, vf = rs.to_fcp(*usr[:3])
+                    qf, kf, vf = rs.to_fcp(*usr_qkv)
                     ex_u.forward(qf, kf, vf)
                 else:
-                    ex_u.forward_user(rs, *usr[:3])
+                    ex_u.forward_user(rs, *usr_qkv)
                 b.record(stream)
                 torch.cuda.synchronize()
                 if it:

@@ -199,8 +199,10 @@ class Reshuffler:
             remote_stream.wait_stream(cur)
         with torch.cuda.stream(st):
             for src, w, off in zip(flat_in, widths, region):                # publish
-                self.buf[off:off + rows_in * w].view(rows_in, w).copy_(src.view(torch.uint8),
-                                                                        non_blocking=True)
+                dst = self.buf[off:off + rows_in * w]
+                if src.data_ptr() == dst.data_ptr():    # written in place (input_views)
+                    continue
+                dst.view(rows_in, w).copy_(src.view(torch.uint8), non_blocking=True)
             self.flags.barrier(0, st)              # every rank's rows published
             for dst, w, off in zip(flat_out, widths, region):
                 ob = dst.view(torch.uint8)
@@ -218,6 +220,26 @@ class Reshuffler:
         for t in list(tensors) + list(outs):
             t.record_stream(remote_stream)
         return outs, ev
+
+    def input_views(self, specs, rows: int | None = None):
+        """Tensors of shapes [rows, *shape] / dtypes ``specs`` that live in this rank's
+        region exactly where ``_move`` publishes the same tensor list: a caller that writes its
+        user-layout inputs there (e.g. the QKV projection's output) skips the publish copy, a
+        same-device copy that would otherwise wait for the SMs the overlapped compute holds.
+        Valid until the next move."""
+        rows = self.plan.user_tokens if rows is None else rows
+        out, off = [], 0
+        for shape, dtype in specs:
+            esz = torch.empty((), dtype=dtype).element_size()
+            e = 1
+            for x in shape:
+                e *= x
+            w = e * esz
+            if off + rows * w > self.buf.numel():
+                raise ParameterError("input views exceed the reshuffler's region")
+            out.append(self.buf[off:off + rows * w].view(dtype).view((rows,) + tuple(shape)))
+            off += self.t_max * w
+        return out
 
     def resident_chunks(self) -> frozenset:
         """Chunks that stay on this rank (their to-FCP pull is local): build the executor with
