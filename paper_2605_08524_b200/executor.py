@@ -51,7 +51,7 @@ class FcpExecutor:
         self.work = build_rank_work(result, rank, resident=self.resident)
         self.fuse_remote = self._fuse_remote_waves(result, rank, cfg)
         if self.fuse_remote:
-            self.work = build_rank_work(result, rank, fuse_remote=True, resident=self.resident)
+            self.work = build_rank_work(result, rank, fuse_remote=self.fuse_remote, resident=self.resident)
         self.layout = self.work.layout
         self.op = BlockAttention(self.work, cfg, self.device, softmax_scale, num_ctas)
         # The exchange runs on copy engines (p2p.SymmetricExchange), so the persistent
@@ -104,7 +104,7 @@ class FcpExecutor:
         import os
         env = os.environ.get("FCPB_FUSE_REMOTE")
         if env is not None:
-            return env == "1"
+            return "all" if env == "all" else env == "1"
         waves = self.work.fwd.waves
         if self.world == 1 or sum(1 for w in waves if w.stage != LOCAL_WAVE) < 2:
             return False

@@ -302,7 +302,9 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
                   resident=None) -> FwdPlan:
     """Forward waves over the rank's Q runs.  fuse_remote: every received KV chunk goes into
     one wave released by this rank's last arrival stage (one launch, one tail, and at most a
-    local and a remote partial per Q run) instead of one wave per coalesced stage.
+    local and a remote partial per Q run) instead of one wave per coalesced stage;
+    fuse_remote="all": the local tiles join that wave too (no partials, no merge) -- for ranks
+    whose exchange is short next to their compute.
     resident: chunks whose Q/K/V rows are in place before the reshuffle into the FCP layout
     completes (they stay on this rank); tiles of a resident Q run against a resident local run
     form PRE_WAVE, which runs while the reshuffle pulls the other rows."""
@@ -313,7 +315,7 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
 
     def wave_of(kv):
         if kv not in lay.recv_offset:
-            return LOCAL_WAVE
+            return last_stage if fuse_remote == "all" else LOCAL_WAVE
         return last_stage if fuse_remote else lay.recv_stage[kv]
 
     def is_resident(run):
@@ -328,7 +330,7 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
         for src in sources[R.key]:
             if src[0] == "run":
                 S, diag = src[1], src[2]
-                w = PRE_WAVE if (r_res and is_resident(S)) else LOCAL_WAVE
+                w = PRE_WAVE if (r_res and is_resident(S)) else wave_of(S.chunks()[0])
                 if w == PRE_WAVE:
                     pre_pairs.update((R.key, c) for c in S.chunks())
                 waves.setdefault(w, []).append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
@@ -359,10 +361,8 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
             refs += kvs
             if w == PRE_WAVE:
                 pairs += _run_pairs(result, R, lambda kv: (R.key, kv) in pre_pairs)
-            elif w == LOCAL_WAVE:
-                pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w and (R.key, kv) not in pre_pairs)
             else:
-                pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w)
+                pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w and (R.key, kv) not in pre_pairs)
             out_row = seg_rows.get((R.key, w), -1)
             sidx = len(segs)
             segs.append((R.off, R.tokens, begin, len(refs), out_row, 0))

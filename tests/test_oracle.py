@@ -116,7 +116,7 @@ def test_tiled_equals_dense(mask):
     assert torch.allclose(l1, l2, atol=1e-10)
 
 
-@pytest.mark.parametrize("fuse", [False, True])
+@pytest.mark.parametrize("fuse", [False, True, "all"])
 @pytest.mark.parametrize("n,lengths,block,coalesce,sched", [
     (1, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
     (2, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
@@ -134,6 +134,8 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
     works = [build_rank_work(r, w, fuse_remote=fuse) for w in range(n)]
     if fuse:
         assert all(sum(1 for wv in wk.fwd.waves if wv.stage >= 0) <= 1 for wk in works)
+    if fuse == "all":        # one wave per rank: no partials, no merge
+        assert all(len(wk.fwd.waves) == 1 and wk.fwd.partial_rows == 0 for wk in works)
     goff, T = global_offsets(r)
     q, k, v, do = _inputs(T, 3)
     scale = 1 / math.sqrt(MODEL.head_dim)
@@ -170,7 +172,7 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
         scatter_rank(dv_loc[w], dv, work.layout, goff, deps)
     for a, b in ((o, o_ref), (lse, l_ref), (dq, dq_ref), (dk, dk_ref), (dv, dv_ref)):
         assert torch.allclose(a, b, atol=1e-9), (a - b).abs().max()
-    if n > 1:
+    if n > 1 and fuse != "all":
         assert any(wk.fwd.partial_rows for wk in works)   # the merge path was exercised
 
 
