@@ -95,23 +95,22 @@ class FcpExecutor:
         self._marks = None          # optional per-phase CUDA-event timeline (see timeline())
         self._rs_stream = None      # forward_user: the reshuffle's remote pulls
 
-    def _fuse_remote_waves(self, result, rank, cfg) -> bool:
-        """One remote forward wave instead of one per stage when this rank's pulls are
-        expected to finish while its local wave still runs: copy-engine pulls at ~200 GB/s
-        (measured 260-480 GB/s) against the local wave at ~600 TFLOP/s.  Then waiting for
-        the last stage costs nothing and one launch saves the other waves' tails.
-        FCPB_FUSE_REMOTE=0/1 overrides (experiments)."""
+    def _fuse_remote_waves(self, result, rank, cfg):
+        """How the forward groups a rank's tiles into waves.  With the copy-engine exchange
+        (550-700 GB/s per rank at N=2, 2-D pulls of merged runs) a rank's pulls are short
+        next to its compute, so by default every tile goes into ONE wave released by the
+        last arrival stage ("all"): no fp32 partials, no LSE merge and one launch tail, for
+        the price of the exposed exchange.  Measured at N=4 (`gpurun_out/abm1_*`): C2 4.78 vs
+        4.80-4.88 ms, C3 621.4-621.7 vs 621.9-623.6 ms against a local wave overlapped with
+        the pulls plus one fused remote wave.  FCPB_FUSE_REMOTE=0/1/all overrides."""
         import os
         env = os.environ.get("FCPB_FUSE_REMOTE")
         if env is not None:
             return "all" if env == "all" else env == "1"
         waves = self.work.fwd.waves
-        if self.world == 1 or sum(1 for w in waves if w.stage != LOCAL_WAVE) < 2:
+        if self.world == 1 or not any(w.stage >= 0 for w in waves):
             return False
-        recv_s = self.work.layout.recv_tokens * 2 * cfg.kv_heads * cfg.head_dim * 2 / 200e9
-        local = sum(w.pairs for w in waves if w.stage == LOCAL_WAVE)
-        local_s = local * cfg.flops_per_token_pair / 600e12
-        return recv_s <= local_s
+        return "all"
 
     def kv_input_buffers(self):
         """(k, v) [T, Hkv, D] bf16 buffers to write this rank's K/V into before ``forward``.
@@ -392,6 +391,14 @@ class FcpExecutor:
         flops = 3.5 * float(sum(loads.compute_flops))      # distributor.py:151-155 accounting
         nbytes = int(sum(e.nbytes for st in self.result.plan.stages for e in st))
         return SimReport(t_max, per, stages, flops, nbytes)
+
+    def close(self) -> None:
+        """Release the peer-memory regions of this batch's exchange (collective at N > 1:
+        every rank calls it, after its last step; the executor is unusable afterwards)."""
+        if self.xchg is not None:
+            torch.cuda.synchronize(self.device)
+            self.xchg.close()
+            self.xchg = None
 
     def forward_user(self, rs, q_u, k_u, v_u):
         """Forward from the user's layout: the reshuffler

@@ -126,6 +126,38 @@ class _Regions:
             self.ptrs = [r.ptr for r in regions]
             self._keep = regions
 
+    def close_peers(self) -> None:
+        """Unmap the peers' regions (first half of a collective close)."""
+        if self.backend == "symm" or self._keep is None:
+            return
+        for r in self._keep:
+            if r._opened:
+                r.close()
+        self.peers = []
+
+    def free_local(self) -> None:
+        """Free this rank's region (after every peer has unmapped it)."""
+        if self.backend == "symm" or self._keep is None:
+            self._keep = None
+            return
+        for r in self._keep:
+            if r._owned:
+                r.close()
+        self._keep = None
+        self.local = None
+
+
+def close_regions(regions, group) -> None:
+    """Collective release of peer-memory regions: every rank unmaps its peers' regions, a
+    barrier, then every rank frees its own (a region must not be freed while a peer still
+    has it mapped)."""
+    torch.cuda.synchronize()
+    for r in regions:
+        r.close_peers()
+    dist.barrier(group=group)
+    for r in regions:
+        r.free_local()
+
 
 TRANSPORT = os.environ.get("FCPB_TRANSPORT", "ipc")   # "symm": torch symmetric memory (A/B)
 
@@ -204,6 +236,13 @@ class SymmetricExchange:
         self.r_local = me.recv_tokens
         self.stage_pulls = stage_pulls(result, rank, layouts)
         self.publish_copies = 0                   # K/V publish copies issued (0 when zero-copy)
+
+    def close(self) -> None:
+        """Release the exchange's peer-memory regions (collective: every rank calls it)."""
+        if self._regions is None:
+            return
+        close_regions(list(self._regions) + [self.flags._reg], self.group)
+        self._regions = None
 
     # ------------------------------------------------------------------ forward (K5)
     def kv_views(self):

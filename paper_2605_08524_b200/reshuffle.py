@@ -152,6 +152,7 @@ class Reshuffler:
         self.row_cap = max_row_bytes or ((2 * H + 2 * Hk) * D * 2 + 4 * H)
         self.t_max = max(max(max(p.user_tokens, p.fcp_tokens) for p in self.plans), 1)
         group = group or dist.group.WORLD
+        self._group = group
         reg = _Regions(self.t_max * self.row_cap, torch.uint8, (self.t_max * self.row_cap,),
                        self.device, group, TRANSPORT)
         self.buf, self.peer, self._reg = reg.local, reg.peers, reg
@@ -240,6 +241,14 @@ class Reshuffler:
             out.append(self.buf[off:off + rows * w].view(dtype).view((rows,) + tuple(shape)))
             off += self.t_max * w
         return out
+
+    def close(self) -> None:
+        """Release the region and flags (collective: every rank calls it)."""
+        if self._reg is None:
+            return
+        from .p2p import close_regions
+        close_regions([self._reg, self.flags._reg], self._group)
+        self._reg = None
 
     def resident_chunks(self) -> frozenset:
         """Chunks that stay on this rank (their to-FCP pull is local): build the executor with

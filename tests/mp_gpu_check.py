@@ -112,6 +112,9 @@ def main():
                       "measured_total_ms": mr.total_time * 1e3,
                       "reshuffle_ok": reshuffle_ok, "reshuffle_to_fcp_ms": t0.elapsed_time(t1),
                       "measured_eta": [round(w.eta, 3) for w in mr.per_worker]}), flush=True)
+    # collective release of every peer-memory region (a new executor per batch must not leak)
+    for obj in (ex_u, ex, rs):
+        obj.close()
     flag = torch.tensor([1 if ok else 0], device="cpu" if shared else dev)
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
