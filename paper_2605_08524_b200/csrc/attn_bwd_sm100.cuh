@@ -98,7 +98,6 @@ struct Smem {
   uint64_t q_full[kQSlots], q_empty[kQSlots];
   uint64_t do_full[kDoSlots], do_empty[kDoSlots];
   uint64_t s_full, dp_full, p_half, p_full, ds_full;
-  uint64_t s_full_h[2], p_full_h[2];   // half tiles (kSHalf)
   uint64_t acc_full, acc_free;
   SchedRing sched;
   uint32_t tmem_base;
@@ -172,14 +171,7 @@ FCPB_DEV float4 lds128(uint32_t addr) {
 #ifndef FCPB_BWD_PSPLIT
 #define FCPB_BWD_PSPLIT 1
 #endif
-// Half tiles: S^T is issued as two N=64 MMAs (q columns 0-63 for warpgroups 0-1, 64-127 for
-// 2-3) with their own barriers, so each half runs its own chain S_h(j+1) -> exp -> dV_h(j+1)
-// -> S_h(j+2) and the tensor pipe works on one half while the other half exponentiates.
-#ifndef FCPB_BWD_SHALF
-#define FCPB_BWD_SHALF 1
-#endif
-constexpr bool kSHalf = FCPB_BWD_SHALF != 0;
-constexpr bool kPSplit = FCPB_BWD_PSPLIT != 0 && !kSHalf;
+constexpr bool kPSplit = FCPB_BWD_PSPLIT != 0;
 
 template <bool kMask>
 FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t (&pk)[16], uint32_t t_p,
@@ -298,10 +290,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
     mbar_init(&sm.dp_full, 1);
     mbar_init(&sm.p_half, 128 * kSoftmaxWGs);
     mbar_init(&sm.p_full, 128 * kSoftmaxWGs);
-    for (int h = 0; h < 2; ++h) {
-      mbar_init(&sm.s_full_h[h], 1);
-      mbar_init(&sm.p_full_h[h], 128 * kSoftmaxWGs / 2);
-    }
     mbar_init(&sm.ds_full, 128 * kSoftmaxWGs);
     mbar_init(&sm.acc_full, 1);
     mbar_init(&sm.acc_free, 128 * kSoftmaxWGs);
@@ -419,32 +407,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         }
         __syncwarp();
       };
-      // S^T half h = K Q_h^T: q rows 64h..64h+63 of the Q slot (8 KB into each SW128 panel),
-      // N = 64, into S columns 64h..64h+63.
-      const uint32_t id_shalf = idesc_bf16_f32(kBK, kBQ / 2, false, false);
-      auto issue_s_half = [&](uint32_t b_base, int h, uint64_t* done) {
-        if (leader) {
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t oa = (kk >> 2) * kKVPanel + (kk & 3) * 32;
-            const uint32_t ob = (kk >> 2) * kQPanel + (kk & 3) * 32 + h * (kQPanel / 2);
-            mma_ss(tmem + kColS + h * (kBQ / 2), smem_desc_sw128(a_k + oa, 16, 1024),
-                   smem_desc_sw128(b_base + ob, 16, 1024), id_shalf, kk > 0);
-          }
-          mma_commit(done);
-        }
-        __syncwarp();
-      };
-      // dV += P^T dO over the K steps of half h (kk 4h..4h+3: warpgroups 2h, 2h+1)
-      auto issue_dv_half = [&](uint32_t b_base, int h, bool acc) {
-        if (leader) {
-#pragma unroll
-          for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-            mma_ts(tmem + kColDV, tmem + a_col(kColS, kk),
-                   smem_desc_sw128(b_base + kk * 2048, kQPanel, 1024), id_acc, acc || kk > 0);
-        }
-        __syncwarp();
-      };
       // dV += P^T dO  /  dK += dS^T Q:  A from TMEM, B = the [q, d] tile (MN-major).
       // kk_par: -1 all K steps; 0 / 1 the even / odd ones (first / second 16 columns of
       // every warpgroup's slice, the split-P halves)
@@ -473,51 +435,6 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         }
         mbar_wait(&sm.kv_full, kv_phase);
         kv_phase ^= 1;
-        if (kSHalf) {
-          // prologue: S_0(0), S_1(0), dP(0)
-          mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
-          tc_fence_after();
-          issue_s_half(smem_u32(sm.q[qr_.slot]), 0, &sm.s_full_h[0]);
-          issue_s_half(smem_u32(sm.q[qr_.slot]), 1, &sm.s_full_h[1]);
-          mbar_wait(&sm.do_full[dr_.slot], dr_.phase);
-          tc_fence_after();
-          issue_kq(a_v, smem_u32(sm.dout[dr_.slot]), kColDP, &sm.dp_full);
-          for (int j = 0; j < n; ++j, ++tile) {
-            const uint32_t qcur = qr_.slot, dcur = dr_.slot;
-            qr_.next();
-            dr_.next();
-            for (int h = 0; h < 2; ++h) {
-              mbar_wait(&sm.p_full_h[h], p_phase);
-              if (h == 0 && j == 0) {
-                mbar_wait(&sm.acc_free, acc_phase ^ 1);   // epilogue drained the previous item
-                acc_phase ^= 1;
-              }
-              tc_fence_after();
-              issue_dv_half(smem_u32(sm.dout[dcur]), h, j > 0);
-              if (j + 1 < n) {
-                if (h == 0) mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
-                tc_fence_after();
-                issue_s_half(smem_u32(sm.q[qr_.slot]), h, &sm.s_full_h[h]);
-              }
-            }
-            p_phase ^= 1;
-            mbar_wait(&sm.ds_full, ds_phase);
-            ds_phase ^= 1;
-            tc_fence_after();
-            issue_acc(kColDP, smem_u32(sm.q[qcur]), kColDK, j > 0, &sm.q_empty[qcur], &sm.do_empty[dcur]);
-            if (j + 1 < n) {
-              mbar_wait(&sm.do_full[dr_.slot], dr_.phase);
-              tc_fence_after();
-              issue_kq(a_v, smem_u32(sm.dout[dr_.slot]), kColDP, &sm.dp_full);
-            }
-          }
-          if (leader) {
-            mma_commit(&sm.acc_full);
-            mma_commit(&sm.kv_empty);
-          }
-          __syncwarp();
-          continue;
-        }
         // prologue: S(0), dP(0).  The S/dP regions are free: the previous item's last
         // dV/dK were issued after its softmax finished with them (in-order pipe).
         mbar_wait(&sm.q_full[qr_.slot], qr_.phase);
@@ -617,7 +534,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               // and the tile is the no-swizzle MN-major canonical layout of the dQ GEMM's A
               gdst = reinterpret_cast<uint4*>(p.ds_out + tid_tile * (kBK * kBQ)) + (wg * 4) * kBK + tid;
             }
-            mbar_wait(kSHalf ? &sm.s_full_h[wg >> 1] : &sm.s_full, s_phase);
+            mbar_wait(&sm.s_full, s_phase);
             s_phase ^= 1;
             FCPB_TR(kTrSGot, (int)tile);
             mbar_wait(&sm.q_full[qr_.slot], qr_.phase);   // lse2 of this tile landed
@@ -638,7 +555,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             FCPB_TR(kTrPSt, (int)tile);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(kSHalf ? &sm.p_full_h[wg >> 1] : &sm.p_full);
+            mbar_arrive(&sm.p_full);
             FCPB_TR(kTrPArrive, (int)tile);
             // phase 2: dS
             mbar_wait(&sm.dp_full, dp_phase);
