@@ -33,6 +33,52 @@ from .pipeline import ScheduleResult, plan_digest
 from .worklist import LOCAL_WAVE, PRE_WAVE, build_rank_work
 
 
+def kernel_config(cfg: ModelConfig):
+    """(config the sm_100a kernels run, q-head replication) for a user config.  The kernels
+    are compiled for head_dim 128 and an even GQA group (a forward CTA serves two q-heads of
+    one K/V head).  Smaller head dims run zero-padded to 128 (the scores, P, O and every
+    gradient are unchanged, the padded columns stay zero), and an odd group runs every q-head
+    twice with a zero dO for the copy (its dS, hence its dK/dV contribution, is exactly zero);
+    the softmax scale stays 1/sqrt(user head_dim).  Exact, at up to 4x the tensor work of a
+    native kernel -- this serves the tiny C1 model (Hq = Hkv = 4, D = 64)."""
+    from .errors import ParameterError
+    if cfg.head_dim > 128 or cfg.head_dim % 8:
+        raise ParameterError(f"head_dim {cfg.head_dim}: the kernels support multiples of 8 up to 128")
+    if cfg.kv_heads <= 0 or cfg.q_heads % cfg.kv_heads:
+        raise ParameterError(f"q_heads {cfg.q_heads} is not a multiple of kv_heads {cfg.kv_heads}")
+    rep = 1 if (cfg.q_heads // cfg.kv_heads) % 2 == 0 else 2
+    if rep == 1 and cfg.head_dim == 128:
+        return cfg, 1
+    return ModelConfig(q_heads=cfg.q_heads * rep, kv_heads=cfg.kv_heads, head_dim=128,
+                       dtype_bytes=cfg.dtype_bytes), rep
+
+
+def pad_head_dim(x, d_to: int = 128):
+    """[..., D] -> [..., 128], zero-padded (kernel_config)."""
+    d = x.shape[-1]
+    return x if d == d_to else torch.nn.functional.pad(x, (0, d_to - d)).contiguous()
+
+
+def replicate_q_heads(x, rep: int, zero_copy: bool = False):
+    """[T, Hq, ...] -> [T, rep*Hq, ...]: every q-head twice, interleaved (heads 2h and 2h+1
+    map to h's K/V head under the doubled group); the copy is zero when zero_copy (the dO and
+    O of the duplicates, whose dS and gradients then vanish exactly)."""
+    if rep == 1:
+        return x
+    if zero_copy:
+        return torch.stack([x, torch.zeros_like(x)], dim=2).flatten(1, 2).contiguous()
+    return x.repeat_interleave(rep, dim=1).contiguous()
+
+
+def unreplicate_q(x, rep: int, d: int):
+    """Kernel-shaped Q-side output ([T, rep*Hq, 128] or [T, rep*Hq]) -> user shape."""
+    if rep > 1:
+        x = x[:, 0::rep]
+    if x.dim() == 3 and x.shape[-1] != d:
+        x = x[..., :d]
+    return x.contiguous()
+
+
 class FcpExecutor:
     def __init__(self, result: ScheduleResult, rank: int, cfg: ModelConfig, device=None,
                  group=None, softmax_scale=None, num_ctas: int = 0, check_plan: bool = True,
@@ -40,11 +86,18 @@ class FcpExecutor:
         self.result = result
         self.rank = rank
         self.world = result.assignment.n_workers
-        self.cfg = cfg
+        self.user_cfg = cfg
+        # the kernels' shapes (kernel_config): D padded to 128, q-heads doubled for odd groups
+        kcfg, self.q_rep = kernel_config(cfg)
+        self.adapt = kcfg is not cfg
+        if self.adapt and softmax_scale is None:
+            import math
+            softmax_scale = 1.0 / math.sqrt(cfg.head_dim)
+        self.cfg = cfg = kcfg
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.group = group
         if check_plan and self.world > 1:
-            exchange.sync_plan_digest(plan_digest(result, cfg), group)
+            exchange.sync_plan_digest(plan_digest(result, self.user_cfg), group)
         # resident: chunks whose rows are in place before a reshuffle into the FCP layout
         # completes (Reshuffler.resident_chunks); their local tiles form PRE_WAVE
         self.resident = frozenset(resident or ())
@@ -118,10 +171,10 @@ class FcpExecutor:
         place and the step skips the publish copy; at N = 1 plain tensors.  Writes issued on
         the current stream after this call are ordered after the peers' pulls of the previous
         step (the comm stream ends each forward with the "K/V consumed" barrier)."""
-        if self.xchg is not None:
+        if self.xchg is not None and not self.adapt:
             torch.cuda.current_stream(self.device).wait_stream(self.comm)
             return self.xchg.kv_views()
-        shape = (self.layout.tokens, self.cfg.kv_heads, self.cfg.head_dim)
+        shape = (self.layout.tokens, self.user_cfg.kv_heads, self.user_cfg.head_dim)
         return (torch.empty(shape, dtype=torch.bfloat16, device=self.device),
                 torch.empty(shape, dtype=torch.bfloat16, device=self.device))
 
@@ -161,18 +214,36 @@ class FcpExecutor:
 
     def flops(self) -> tuple[float, float]:
         """Algorithmic (fwd, bwd) FLOPs of this rank (reference costmodel.py:37-38, 26)."""
-        fwd = self.work.pairs * self.cfg.flops_per_token_pair
-        return fwd, fwd * self.cfg.backward_multiplier
+        fwd = self.work.pairs * self.user_cfg.flops_per_token_pair
+        return fwd, fwd * self.user_cfg.backward_multiplier
 
     def exchange_bytes(self) -> dict:
         s, r = exchange.exchange_bytes(self.stages, self.kv_bytes_per_token)
         return {"fwd_send": s, "fwd_recv": r, "bwd_send": 2 * r, "bwd_recv": 2 * s}
 
     # ------------------------------------------------------------------ forward
+    # ------------------------------------------------------------------ shape adapter
+    def _pad_d(self, x):
+        return pad_head_dim(x)
+
+    def _q_in(self, x, zero_copy=False):
+        return replicate_q_heads(pad_head_dim(x), self.q_rep, zero_copy)
+
+    def _q_out(self, x):
+        return unreplicate_q(x, self.q_rep, self.user_cfg.head_dim)
+
     def forward(self, q, k, v, pre_event=None):
         """O, LSE of this rank's Q rows.  pre_event: the inputs are complete only once this
         event has fired (a reshuffle still in flight, ``forward_user``); the PRE_WAVE tiles,
         whose rows were in place before, run first, then the stream waits for it."""
+        if self.adapt:
+            if pre_event is not None:
+                torch.cuda.current_stream(self.device).wait_event(pre_event)
+            o, lse = self._forward(self._q_in(q), self._pad_d(k), self._pad_d(v))
+            return self._q_out(o), self._q_out(lse)
+        return self._forward(q, k, v, pre_event)
+
+    def _forward(self, q, k, v, pre_event=None):
         op = self.op
         cur = torch.cuda.current_stream(self.device)
         outs = op.alloc_forward_outputs()
@@ -214,6 +285,15 @@ class FcpExecutor:
 
     # ------------------------------------------------------------------ backward
     def backward(self, q, k, v, o, lse, do):
+        if self.adapt:
+            lse_k = lse.repeat_interleave(self.q_rep, dim=1).contiguous() if self.q_rep > 1 else lse
+            dq, dk, dv = self._backward(self._q_in(q), self._pad_d(k), self._pad_d(v),
+                                        self._q_in(o, zero_copy=True), lse_k, self._q_in(do, zero_copy=True))
+            D = self.user_cfg.head_dim
+            return self._q_out(dq), dk[..., :D].contiguous(), dv[..., :D].contiguous()
+        return self._backward(q, k, v, o, lse, do)
+
+    def _backward(self, q, k, v, o, lse, do):
         op = self.op
         cur = torch.cuda.current_stream(self.device)
         prep = op.backward_prepare(o, lse, do, cur)
@@ -387,7 +467,7 @@ class FcpExecutor:
         t_max = max(x[0] for x in allv)
         per = [WorkerStats(compute_time=c, send_time=sd, recv_time=rv, idle_time=t_max - c,
                            eta=t_max / c if c > 0 else 1.0) for _, c, sd, rv in allv]
-        loads = worker_loads(self.result.assignment, self.result.units, self.result.deps, self.cfg)
+        loads = worker_loads(self.result.assignment, self.result.units, self.result.deps, self.user_cfg)
         flops = 3.5 * float(sum(loads.compute_flops))      # distributor.py:151-155 accounting
         nbytes = int(sum(e.nbytes for st in self.result.plan.stages for e in st))
         return SimReport(t_max, per, stages, flops, nbytes)
@@ -409,7 +489,7 @@ class FcpExecutor:
         and (o, lse)."""
         if self._rs_stream is None:
             self._rs_stream = torch.cuda.Stream(device=self.device)
-        H, D = self.cfg.q_heads, self.cfg.head_dim
+        H, D = self.user_cfg.q_heads, self.user_cfg.head_dim
         q = torch.empty((self.layout.tokens, H, D), dtype=q_u.dtype, device=self.device)
         k, v = self.kv_input_buffers()
         (q, k, v), ev = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens,

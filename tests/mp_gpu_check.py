@@ -42,7 +42,8 @@ def main():
     lengths = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3523,2702,2219,1292,1438,413,544,319").split(",")]
     block = int(sys.argv[2]) if len(sys.argv) > 2 else 512
     hq, hk = (int(x) for x in os.environ.get("FCPB_CHECK_HEADS", "8,2").split(","))
-    model = ModelConfig(q_heads=hq, kv_heads=hk, head_dim=128)
+    dim = int(os.environ.get("FCPB_CHECK_DIM", "128"))
+    model = ModelConfig(q_heads=hq, kv_heads=hk, head_dim=dim)
     sched = os.environ.get("FCPB_CHECK_SCHED", "fcp")
     if sched == "fcp":
         r = schedule(lengths, world, block, model)

@@ -24,11 +24,11 @@ def _port():
         return s.getsockname()[1]
 
 
-def _run(n, sched="fcp", shared=False, args=(), heads="8,2"):
+def _run(n, sched="fcp", shared=False, args=(), heads="8,2", dim=128):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mp_gpu_check.py"), *args]
-    env = dict(os.environ, FCPB_CHECK_SCHED=sched, FCPB_CHECK_HEADS=heads,
+    env = dict(os.environ, FCPB_CHECK_SCHED=sched, FCPB_CHECK_HEADS=heads, FCPB_CHECK_DIM=str(dim),
                FCPB_SHARED_GPU="1" if shared else "0")
     proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     print(proc.stdout[-4000:])
@@ -44,6 +44,7 @@ def test_executor_nccl_parity(n, sched):
 
 
 @pytest.mark.parametrize("n,sched,args,heads", [
+    (2, "fcp", (), "4,4:64"),                   # the C1 tiny model (Hq = Hkv = 4, D = 64)
     (2, "fcp", (), "8,2"),
     (3, "fcp", (), "8,2"),
     (3, "ring", (), "8,2"),
@@ -53,4 +54,5 @@ def test_executor_nccl_parity(n, sched):
 ])
 def test_executor_shared_gpu_parity(n, sched, args, heads):
     """N ranks as N processes on GPU 0: the multi-rank product path on a one-GPU box."""
-    _run(n, sched, shared=True, args=args, heads=heads)
+    heads, _, dim = heads.partition(":")
+    _run(n, sched, shared=True, args=args, heads=heads, dim=int(dim or 128))

@@ -327,3 +327,41 @@ def test_autograd_fcp_attention(runner):
     brep = {n: err(g(b[n]), g(ref)) for n, ref in (("o", ro), ("lse", rl), ("dq", rdq), ("dk", rdk), ("dv", rdv))}
     _report(f"autograd through {runner}", tolerance_report(rep, brep))
     assert_within_tolerance(rep, brep)
+
+
+def test_c1_tiny_model_through_the_executor():
+    """The C1 tiny model itself (Hq = Hkv = 4, D = 64, run in bf16 on the GPU):
+    the executor maps it onto the D=128, even-group kernels (executor.kernel_config: zero
+    padding, q-heads run twice with a zero dO for the copy) -- C1 lengths, block 512, fwd+bwd
+    and autograd against the fp64 oracle at scale 1/sqrt(64)."""
+    import math
+    from oracle.attention_ref import mono_bwd, mono_fwd
+    from oracle.simworkers import gather_rank, global_offsets, global_sequence_rows
+    from paper_2605_08524_b200.executor import FcpExecutor
+    w = configs.c1_tiny(1)
+    model = configs.TINY_MODEL
+    r = schedule(list(w.lengths), 1, 512, model)
+    goff, T = global_offsets(r)
+    q, k, v, do = make_inputs(T, model)
+    ex = FcpExecutor(r, 0, model, torch.device("cuda", 0))
+    assert ex.adapt and ex.q_rep == 2
+    loc = [gather_rank(x, ex.layout, goff, r.deps).cuda() for x in (q, k, v, do)]
+    o, lse, dq, dk, dv = ex.step(*loc)
+    assert o.shape == loc[0].shape and dk.shape == loc[1].shape and lse.shape == (T, 4)
+    rows = global_sequence_rows(r)
+    scale = 1 / math.sqrt(model.head_dim)
+    qf, kf, vf, dof = (x.double() for x in (q, k, v, do))
+    ro, rl = mono_fwd(qf, kf, vf, rows, scale)
+    rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
+    g = lambda x: gather_rank(x, ex.layout, goff, r.deps)
+    rep = {n: err(t.cpu(), g(ref)) for n, t, ref in
+           (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv))}
+    b = bf16_reference(r, model, q, k, v, do)
+    brep = {n: err(g(b[n]), g(ref)) for n, ref in (("o", ro), ("lse", rl), ("dq", rdq), ("dk", rdk), ("dv", rdv))}
+    _report("C1 tiny model (4/4 heads, D=64) through the executor", tolerance_report(rep, brep))
+    assert_within_tolerance(rep, brep)
+    # and through autograd
+    qg, kg, vg = (x.clone().requires_grad_(True) for x in loc[:3])
+    og = ex.attention(qg, kg, vg)
+    (og.float() * loc[3].float()).sum().backward()
+    assert torch.equal(og.detach(), o) and torch.equal(qg.grad, dq) and torch.equal(kg.grad, dk)

@@ -228,3 +228,59 @@ def test_bench_c2_plans_at_eight_ranks(curve):
     w, r = bench.build_workload("c2", 8, None, "fcp", curve)
     works = [build_rank_work(r, k) for k in range(8)]
     assert sum(wk.layout.tokens for wk in works) == sum(s.length for s in w.batch().sequences)
+
+
+def test_kernel_shape_adapter_is_exact():
+    """The executor's adapter for shapes the kernels are not compiled for (C1: Hq = Hkv = 4,
+    D = 64): head dim zero-padded to 128, every q-head run twice with a zero dO for the copy.
+    Through the work-list emulator on the padded shapes at the user's softmax scale, then
+    un-padded: equal to dense attention on the original shapes (fp64)."""
+    from paper_2605_08524_b200.costmodel import ModelConfig
+    from paper_2605_08524_b200.executor import (kernel_config, pad_head_dim, replicate_q_heads,
+                                                unreplicate_q)
+    tiny = ModelConfig(q_heads=4, kv_heads=4, head_dim=64, dtype_bytes=4)
+    kcfg, rep = kernel_config(tiny)
+    assert (kcfg.q_heads, kcfg.kv_heads, kcfg.head_dim, rep) == (8, 4, 128, 2)
+    tpw = -(-sum([700, 300, 129]) // 2)
+    batch = Batch(tuple(Sequence(i, l) for i, l in enumerate([700, 300, 129])), 2, tpw)
+    r = fcp_schedule(batch, 2, ShardingConfig(256), tiny, DEFAULT_EFFICIENCY)
+    goff, T = global_offsets(r)
+    g = torch.Generator().manual_seed(11)
+    q, k, v, do = (torch.randn((T, 4, 64), generator=g, dtype=torch.float64) for _ in range(4))
+    scale = 1 / math.sqrt(64)
+    rows = global_sequence_rows(r)
+    o_ref, l_ref = mono_fwd(q, k, v, rows, scale)
+    dq_ref, dk_ref, dv_ref = mono_bwd(q, k, v, o_ref, l_ref, do, rows, scale)
+    owner = chunk_placement(r.assignment, r.units)
+    works = [build_rank_work(r, w) for w in range(2)]
+    o = torch.zeros_like(q)
+    lse = torch.zeros_like(l_ref)
+    dq = torch.zeros_like(q)
+    dk_loc, dv_loc, dk_recv, dv_recv = [], [], [], []
+    for w, work in enumerate(works):
+        lay = work.layout
+        ql, kl, vl, dol = (gather_rank(x, lay, goff, r.deps) for x in (q, k, v, do))
+        kr, vr = (gather_rank(x, lay, goff, r.deps, recv=True) for x in (k, v))
+        qa, doa = replicate_q_heads(pad_head_dim(ql), rep), replicate_q_heads(pad_head_dim(dol), rep, True)
+        ka, va, kra, vra = (pad_head_dim(x) for x in (kl, vl, kr, vr))
+        oa, la = emulate_forward(work, qa, ka, va, kra, vra, scale)
+        scatter_rank(unreplicate_q(oa, rep, 64), o, lay, goff, r.deps)
+        scatter_rank(unreplicate_q(la, rep, 64), lse, lay, goff, r.deps)
+        # the kernels see O of the duplicates as zero too (only dO*O matters: delta = 0)
+        oa_in = replicate_q_heads(pad_head_dim(unreplicate_q(oa, rep, 64)), rep, True)
+        dqa, dka, dva, dkra, dvra = emulate_backward(work, qa, ka, va, kra, vra, oa_in, la, doa, scale)
+        scatter_rank(unreplicate_q(dqa, rep, 64), dq, lay, goff, r.deps)
+        dk_loc.append(dka[..., :64])
+        dv_loc.append(dva[..., :64])
+        dk_recv.append(dkra[..., :64])
+        dv_recv.append(dvra[..., :64])
+    layouts = [wk.layout for wk in works]
+    return_partials(dk_recv, dk_loc, layouts, r.deps, owner)
+    return_partials(dv_recv, dv_loc, layouts, r.deps, owner)
+    dk = torch.zeros_like(k)
+    dv = torch.zeros_like(v)
+    for w, work in enumerate(works):
+        scatter_rank(dk_loc[w], dk, work.layout, goff, r.deps)
+        scatter_rank(dv_loc[w], dv, work.layout, goff, r.deps)
+    for a, b in ((o, o_ref), (lse, l_ref), (dq, dq_ref), (dk, dk_ref), (dv, dv_ref)):
+        assert torch.allclose(a, b, atol=1e-9), (a - b).abs().max()
