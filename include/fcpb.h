@@ -123,12 +123,12 @@ typedef struct {
 
 FCPB_API int fcpb_attn_bwd_dq(const FcpbDqArgs* args, void* stream);
 
-/* K2: backward dK/dV.  Work is organised by KV tile: for each KV chunk reference (local
- * or received) the list of local Q chunks that attend to it.  dK/dV accumulate in
- * fp32 per KV arena row (plain stores: one CTA owns a KV block for all heads of
- * its GQA group). */
+/* K2: backward dK/dV.  Work is organised by KV tile: for each KV segment (a local run of
+ * chunks, or a group of received chunks back to back in the arena) the list of local Q
+ * runs that attend to it.  dK/dV accumulate in fp32 per KV arena row (plain stores: one
+ * CTA owns a KV block for all heads of its GQA group). */
 typedef struct {
-  int32_t kv_off, kv_len;       /* arena rows of the KV chunk                       */
+  int32_t kv_off, kv_len;       /* arena rows of the KV segment                     */
   int32_t flags;                /* FCPB_KV_RECV: lives in the receive arena         */
   int32_t q_begin, q_end;       /* [q_begin,q_end) into FcpbBwdQRef                  */
   int32_t pad_;
@@ -136,8 +136,10 @@ typedef struct {
 
 typedef struct {
   int32_t q_off, q_len;
-  int32_t diag;                 /* causal diagonal tile (Q chunk == KV chunk)       */
-  int32_t pad_;
+  int32_t diag;                 /* causal diagonal tile (Q run == KV run)           */
+  int32_t kv_limit;             /* 0: every row of the segment is visible; else only
+                                   its first kv_limit rows (a received group's prefix
+                                   of chunks before this Q run)                     */
 } FcpbBwdQRef;
 
 typedef struct {

@@ -289,7 +289,10 @@ def emulate_backward(work, q, k, v, k_recv, v_recv, o, lse, do, scale, dtype=tor
             vv = src_v[kv_off + c0:kv_off + c0 + cn].to(dtype)
             gk = torch.zeros((cn, Hk, D), dtype=dtype)
             gv = torch.zeros((cn, Hk, D), dtype=dtype)
-            for q_off, q_len, diag, _ in launch.qrefs[qb:qe].tolist():
+            for q_off, q_len, diag, kv_limit in launch.qrefs[qb:qe].tolist():
+                if kv_limit and c0 >= kv_limit:   # a received group's prefix (worklist._group_received)
+                    continue
+                kv_end = min(kv_len, kv_limit) if kv_limit else kv_len
                 first = nb if diag else 0
                 for mb in range(first, -(-q_len // TILE)):
                     r0 = mb * TILE
@@ -298,7 +301,7 @@ def emulate_backward(work, q, k, v, k_recv, v_recv, o, lse, do, scale, dtype=tor
                     for h in range(H):
                         kh = h // group
                         qs = q[sl, h].to(dtype)
-                        s, vis = _tile_scores(qs, kk[:, kh], scale, r0, c0, q_len, kv_len, bool(diag))
+                        s, vis = _tile_scores(qs, kk[:, kh], scale, r0, c0, q_len, kv_end, bool(diag))
                         p = torch.exp(s - lse[sl, h].to(dtype).unsqueeze(1)).masked_fill(~vis, 0.0)
                         dp = torch.matmul(do[sl, h].to(dtype), vv[:, kh].transpose(0, 1))
                         ds = p * (dp - delta[sl, h].unsqueeze(1))

@@ -84,7 +84,7 @@ struct RingPos {
 };
 
 struct KvSeg { int32_t kv_off, kv_len, flags, q_begin, q_end, pad_; };
-struct QRef { int32_t q_off, q_len, diag, pad_; };
+struct QRef { int32_t q_off, q_len, diag, kv_limit; };   // kv_limit 0: every KV row visible
 struct Item { int32_t kvseg, nblock; };
 
 struct Smem {
@@ -141,9 +141,14 @@ FCPB_DEV int head_of(int g, const Params& p) {
   return h;
 }
 
-// Q blocks (128 rows) of `qr` that see KV block `nb` (128 rows): diagonal -> mb >= nb.
+// Q blocks [q_first_block, q_end_block) of `qr` see KV block `nb` (128 rows): diagonal ->
+// mb >= nb; a reference that sees only a prefix of the segment (kv_limit > 0, a received
+// group's visible chunks) has none at or past it.
 FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? nb : 0; }
-FCPB_DEV int q_num_blocks(const QRef& qr) { return (qr.q_len + kBQ - 1) / kBQ; }
+FCPB_DEV int q_end_block(const QRef& qr, int nb) {
+  return (qr.kv_limit == 0 || nb * kBK < qr.kv_limit) ? (qr.q_len + kBQ - 1) / kBQ
+                                                      : q_first_block(qr, nb);
+}
 
 // 4-byte async copy with zero fill when !valid; completion tracked by an mbarrier.
 FCPB_DEV void cp_async_4(void* smem_dst, const float* src, bool valid) {
@@ -336,7 +341,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         };
         for (int r = ks.q_begin; r < ks.q_end; ++r) {
           const QRef qr = p.qrefs[r];
-          for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb) {
+          for (int mb = q_first_block(qr, it.nblock); mb < q_end_block(qr, it.nblock); ++mb) {
             const int qrow = qr.q_off + mb * kBQ;
             for (int gq = 0; gq < group; ++gq) {
               const int h = kvh * group + gq;
@@ -431,7 +436,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         int n = 0;
         for (int r = ks.q_begin; r < ks.q_end; ++r) {
           const QRef qr = p.qrefs[r];
-          n += (q_num_blocks(qr) - q_first_block(qr, it.nblock)) * group;
+          n += (q_end_block(qr, it.nblock) - q_first_block(qr, it.nblock)) * group;
         }
         mbar_wait(&sm.kv_full, kv_phase);
         kv_phase ^= 1;
@@ -514,12 +519,13 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       const int kvh = head_of(g, p);
       const KvSeg ks = p.kvsegs[it.kvseg];
       const int kv_row = it.nblock * kBK + tid;
-      const bool kv_live = kv_row < ks.kv_len;
-      const bool kv_full_tile = it.nblock * kBK + kBK <= ks.kv_len;
       int pair = p.ds_out ? p.pair_base[item_of(g, p)] : 0;   // dS tiles: pair * Hq + q head
       for (int r = ks.q_begin; r < ks.q_end; ++r) {
         const QRef qr = p.qrefs[r];
-        for (int mb = q_first_block(qr, it.nblock); mb < q_num_blocks(qr); ++mb, ++pair) {
+        const int kv_end = qr.kv_limit ? min(qr.kv_limit, ks.kv_len) : ks.kv_len;
+        const bool kv_live = kv_row < kv_end;
+        const bool kv_full_tile = it.nblock * kBK + kBK <= kv_end;
+        for (int mb = q_first_block(qr, it.nblock); mb < q_end_block(qr, it.nblock); ++mb, ++pair) {
           const int q_valid = qr.q_len - mb * kBQ;
           // diagonal: column c (q = 128 mb + c) sees kv row 128 nb + tid iff c >= shift
           const int shift0 = it.nblock * kBK - mb * kBQ;
@@ -584,6 +590,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
       tc_fence_after();
       {
         const bool recv = ks.flags & FCPB_KV_RECV;
+        const bool kv_live = kv_row < ks.kv_len;
         const size_t row = (static_cast<size_t>(ks.kv_off + kv_row) * p.num_kv_heads + kvh) * kD + wg * 32;
         uint32_t a[32], bb[32];
         tmem_ld32(tmem + lane_bits + kColDK + wg * 32, a);

@@ -20,11 +20,19 @@ times (``simulator.py:73-109``).  For rank ``r``:
   with coalesced stage s.  A Q run whose tiles span several waves writes one
   fp32 partial (O, LSE) per wave, merged by K3 afterwards; a Q run served by
   a single wave writes its final bf16 O directly.
-* **Backward.**  dK/dV work is keyed by KV source (received chunk or local run):
-  the KV block iterates over every local Q run attending to it.  Received chunks
-  form their own launch so their dK/dV partials can travel back along the
-  reversed plan edges while the local runs compute.  dQ is query-stationary: one
-  segment per local Q run over all of its (by then resident) KV sources.
+* **Received groups.**  Received chunks of one sequence that sit back to back in
+  the arena form one KV source (``RecvGroup``); each consumer Q run sees a prefix
+  of it (``_group_received``).  A zigzag plan often has a rank receive every other
+  chunk of a long sequence, so this removes a ragged KV tile per chunk: C2 at N=2
+  computes 8,305 / 8,533 forward / backward tiles on rank 0 instead of 8,777 / 8,785.
+  The forward also sorts each Q run's refs by (buffer, offset) so that adjacent
+  ranges coalesce (``_merge_refs``).
+* **Backward.**  dK/dV work is keyed by KV source (received group or local run):
+  the KV block iterates over every local Q run attending to it (with its visible
+  prefix, ``FcpbBwdQRef.kv_limit``).  Received groups form their own launch so
+  their dK/dV partials can travel back along the reversed plan edges while the
+  local runs compute.  dQ is query-stationary: one segment per local Q run over
+  all of its (by then resident) KV sources.
 
 Work items are sorted longest-first (LPT over the persistent grid).  Visible-pair
 accounting stays the reference's per-chunk ``tile_token_pairs``.
@@ -94,7 +102,7 @@ class FwdPlan:
 class BwdLaunch:
     recv: bool
     kvsegs: np.ndarray           # int32 [K, 6]: kv_off kv_len flags q_begin q_end pad
-    qrefs: np.ndarray            # int32 [Q, 4]: q_off q_len diag pad
+    qrefs: np.ndarray            # int32 [Q, 4]: q_off q_len diag kv_limit (0: all KV rows)
     items: np.ndarray            # int32 [I, 2]: kvseg nblock
     pairs: int
     costs: np.ndarray | None = None   # int64 [I]: 128x128 tiles per item (LPT key)
@@ -182,6 +190,24 @@ class Run:
         return [(self.seq, i) for i in range(self.first, self.last + 1)]
 
 
+@dataclass(frozen=True)
+class RecvGroup:
+    """Received chunks ``chunks`` (one sequence) that sit back to back in the receive arena,
+    arrive in the same stage and have the same consumer Q runs: one KV source of
+    [off, off + tokens) arena rows, so the forward, dK/dV and dQ tables tile it as one range
+    (a ragged tile only at its end, not at every chunk boundary)."""
+    chunks_: tuple
+    off: int
+    tokens: int
+
+    @property
+    def key(self):
+        return ("recv", self.chunks_[0][0], self.chunks_[0][1], self.chunks_[-1][1])
+
+    def chunks(self):
+        return list(self.chunks_)
+
+
 def local_runs(result: ScheduleResult, lay: RankLayout, merge: bool = True) -> list[Run]:
     """Maximal runs of a rank's chunks (``merge=False``: one run per chunk).  The tile
     geometry of the reference is per chunk (``kv_dependencies``, ``sharding.py:172-201``), and
@@ -244,7 +270,59 @@ def _run_sources(result: ScheduleResult, lay: RankLayout, runs: list[Run]):
     return out
 
 
-def _runs_and_sources(result: ScheduleResult, lay: RankLayout):
+def _group_received(lay: RankLayout, srcs: dict, merge: bool = True, stage_split: bool = False) -> dict:
+    """Replace the ("recv", chunk) sources by ("recv", RecvGroup, visible tokens): maximal
+    sets of received chunks of one sequence, back to back in the arena in increasing chunk
+    order (``merge=False``: one group per chunk; ``stage_split``: and of one arrival stage,
+    for per-stage forward waves).  Every Q run that attends to a group sees a *prefix* of it
+    (causal: the chunks before the run), so a group is one KV range whose consumers carry
+    their visible length -- the dK/dV kernel masks the rows past it (``FcpbBwdQRef.kv_limit``),
+    the query-stationary kernels take it as the ref length.  Where a chunk-zigzag plan has a
+    rank receive every other chunk of a sequence, this turns per-chunk ragged tiles (a
+    920-token chunk computes 8 x 128 rows) into one ragged tile per group.  A candidate group
+    whose consumers do not each see a prefix is split into single chunks."""
+    consumers: dict = {}
+    for q, lst in srcs.items():
+        for src in lst:
+            if src[0] == "recv":
+                consumers.setdefault(src[1], set()).add(q)
+    cands, cur = [], None
+    for c in lay.recv_chunks:
+        if c not in consumers:
+            continue
+        prev = cur[-1] if cur else None
+        if (merge and prev is not None and prev[0] == c[0] and prev[1] < c[1]
+                and lay.recv_offset[prev] + lay.chunk_tokens[prev] == lay.recv_offset[c]
+                and (not stage_split or lay.recv_stage[prev] == lay.recv_stage[c])):
+            cur.append(c)
+        else:
+            cur = [c]
+            cands.append(cur)
+    group_of = {}
+    for cand in cands:
+        # prefix property: the consumer sets shrink along the group
+        ok = all(consumers[cand[i + 1]] <= consumers[cand[i]] for i in range(len(cand) - 1))
+        for part in ([cand] if ok else [[c] for c in cand]):
+            G = RecvGroup(tuple(part), lay.recv_offset[part[0]], sum(lay.chunk_tokens[c] for c in part))
+            for c in part:
+                group_of[c] = G
+    out = {}
+    for q, lst in srcs.items():
+        new, at = [], {}
+        for src in lst:
+            if src[0] == "recv":
+                G = group_of[src[1]]
+                vis = sum(lay.chunk_tokens[c] for c in G.chunks_ if q in consumers[c])
+                if G.key in at:
+                    continue
+                at[G.key] = len(new)
+                src = ("recv", G, vis)
+            new.append(src)
+        out[q] = new
+    return out
+
+
+def _runs_and_sources(result: ScheduleResult, lay: RankLayout, stage_split: bool = False):
     import os
     merge = os.environ.get("FCPB_RUNS", "1") != "0"     # A/B knob: 0 = one segment per chunk
     runs = local_runs(result, lay, merge)
@@ -252,7 +330,8 @@ def _runs_and_sources(result: ScheduleResult, lay: RankLayout):
     if srcs is None:
         runs = local_runs(result, lay, merge=False)
         srcs = _run_sources(result, lay, runs)
-    return runs, srcs
+    groups = merge and os.environ.get("FCPB_RECV_GROUPS", "1") != "0"   # A/B knob
+    return runs, _group_received(lay, srcs, groups, stage_split)
 
 
 def _run_pairs(result: ScheduleResult, R: Run, keep) -> int:
@@ -310,7 +389,7 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
     form PRE_WAVE, which runs while the reshuffle pulls the other rows."""
     deps = result.deps
     last_stage = max(lay.recv_stage.values(), default=LOCAL_WAVE)
-    runs, sources = _runs_and_sources(result, lay)
+    runs, sources = _runs_and_sources(result, lay, stage_split=fuse_remote != "all")
     resident = frozenset(resident or ())
 
     def wave_of(kv):
@@ -335,9 +414,12 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
                     pre_pairs.update((R.key, c) for c in S.chunks())
                 waves.setdefault(w, []).append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
             else:
-                kv = src[1]
-                waves.setdefault(wave_of(kv), []).append((lay.recv_offset[kv], deps.chunk_tokens[kv], KV_RECV, 0))
-        per_q[R.key] = {w: _merge_refs(r) for w, r in waves.items()}
+                G, vis = src[1], src[2]
+                waves.setdefault(wave_of(G.chunks_[0]), []).append((G.off, vis, KV_RECV, 0))
+        # the order of a Q run's KV refs is free (online softmax); sorted by (buffer, offset)
+        # the refs that continue each other in memory become one range (_merge_refs)
+        per_q[R.key] = {w: _merge_refs(sorted(r, key=lambda x: (x[2] & KV_RECV, x[0])))
+                        for w, r in waves.items()}
 
     wave_ids = sorted({w for waves in per_q.values() for w in waves})
     part_rows = 0
@@ -396,36 +478,40 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
         for src in sources[R.key]:
             if src[0] == "run":
                 S = src[1]
-                consumers.setdefault(S.key, []).append((R, src[2]))
+                consumers.setdefault(S.key, []).append((R, src[2], 0))
                 kv_src[S.key] = (S.off, S.tokens, False, S)
             else:
-                kv = src[1]
-                consumers.setdefault(kv, []).append((R, False))
-                kv_src[kv] = (lay.recv_offset[kv], deps.chunk_tokens[kv], True, kv)
+                G, vis = src[1], src[2]
+                consumers.setdefault(G.key, []).append((R, False, vis if vis < G.tokens else 0))
+                kv_src[G.key] = (G.off, G.tokens, True, G)
     launches = []
     for recv in (True, False):
-        keys = ([c for c in lay.recv_chunks if c in consumers] if recv else
-                [R.key for R in runs if R.key in consumers])
+        keys = (sorted((k for k in consumers if k[0] == "recv"), key=lambda k: kv_src[k][0]) if recv
+                else [R.key for R in runs if R.key in consumers])
         kvsegs, qrefs, items, pairs = [], [], [], 0
         kv_keys, q_keys = [], []
         for key in keys:
             off, kn, _, what = kv_src[key]
             qs = consumers[key]
             begin = len(qrefs)
-            for R, diag in qs:
-                qrefs.append((R.off, R.tokens, int(diag), 0))
+            for R, diag, lim in qs:
+                qrefs.append((R.off, R.tokens, int(diag), lim))
                 q_keys.append(R.key)
-                members = set(what.chunks()) if isinstance(what, Run) else {what}
+                members = set(what.chunks())
                 pairs += _run_pairs(result, R, lambda kv: kv in members)
             kidx = len(kvsegs)
             kvsegs.append((off, kn, KV_RECV if recv else 0, begin, len(qrefs), 0))
             kv_keys.append(key)
             for nb in range(_cdiv(kn, TILE)):
                 cost = 0
-                for R, diag in qs:
+                for R, diag, lim in qs:
                     qb = _cdiv(R.tokens, TILE)
+                    if not _qref_sees(lim, nb):
+                        continue
                     cost += qb - nb if diag else qb
-                items.append((cost, kidx, nb, key[0] if recv else key[1]))
+                if cost == 0:       # the kernel would wait forever for an accumulator
+                    raise ConsistencyError(f"KV block {nb} of {key} has no visiting Q block")
+                items.append((cost, kidx, nb, key[1]))
         if not kvsegs:
             continue
         items = _lpt_order(items)
@@ -435,6 +521,12 @@ def build_backward(result: ScheduleResult, lay: RankLayout) -> list[BwdLaunch]:
             np.asarray([(k, b) for _, k, b, _ in items], dtype=np.int32).reshape(-1, 2), pairs,
             np.asarray([c for c, _, _, _ in items], dtype=np.int64), kv_keys, q_keys))
     return launches
+
+
+def _qref_sees(kv_limit: int, nb: int) -> bool:
+    """Does a dK/dV Q reference with visible prefix ``kv_limit`` (0: all rows) reach KV
+    block nb?  (``q_end_block`` in attn_bwd_sm100.cuh.)"""
+    return kv_limit == 0 or nb * TILE < kv_limit
 
 
 def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
@@ -453,9 +545,9 @@ def build_dq(result: ScheduleResult, lay: RankLayout) -> DqPlan:
                 kv_keys.append(S.key)
                 refs.append((S.off, S.tokens, KV_DIAG if diag else 0, 0))
             else:
-                kv = src[1]
-                kv_keys.append(kv)
-                refs.append((lay.recv_offset[kv], deps.chunk_tokens[kv], KV_RECV, 0))
+                G, vis = src[1], src[2]
+                kv_keys.append(G.key)
+                refs.append((G.off, vis, KV_RECV, 0))
         pairs += _run_pairs(result, R, lambda kv: True)
         sidx = len(segs)
         segs.append((R.off, R.tokens, begin, len(refs), -1, 0))
@@ -484,7 +576,9 @@ def build_ds_tiles(bwd: list[BwdLaunch], dq: DqPlan, causal: bool) -> int:
             kv = b.kv_keys[k]
             seg = b.kvsegs[k]
             for r in range(seg[3], seg[4]):
-                q_off, q_len, diag, _ = b.qrefs[r].tolist()
+                q_off, q_len, diag, lim = b.qrefs[r].tolist()
+                if not _qref_sees(lim, nb):
+                    continue
                 first = nb if diag else 0
                 for mb in range(first, _cdiv(q_len, TILE)):
                     ids[(kv, nb, b.q_keys[r], mb)] = nxt

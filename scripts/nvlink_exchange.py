@@ -71,22 +71,29 @@ def main():
             dist.barrier()
             c0, raw = nvlink_counters(phys)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = a.reps if it else 1
+            cs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
             with torch.cuda.stream(ex.comm):
                 s.record(ex.comm)
-                for _ in range(a.reps if it else 1):
+                for i in range(n):
                     x.barrier(which, 0)
+                    cs[i][0].record(ex.comm)
                     if which == "kv":
                         for st in range(len(ex.stages)):
                             x.pull_stage(st, ex.kv_recv)
                     else:
                         x.pull_returns(ex.returns, staging, ex.ret_rows)
+                    cs[i][1].record(ex.comm)
                     x.barrier(which, 1)
                 e.record(ex.comm)
             torch.cuda.synchronize()
             c1, _ = nvlink_counters(phys)
         ms = s.elapsed_time(e) / a.reps
+        copy_ms = sum(b.elapsed_time(c) for b, c in cs) / len(cs)   # the pulls alone, no barriers
         nbytes = b["fwd_recv"] if which == "kv" else b["bwd_recv"]
-        rec = {"plan_bytes_received": nbytes, "ms": ms, "GBps_received": nbytes / (ms * 1e-3) / 1e9 if ms else None}
+        rec = {"plan_bytes_received": nbytes, "ms": ms, "GBps_received": nbytes / (ms * 1e-3) / 1e9 if ms else None,
+               "copies": (sum(len(st) for st in x.stage_pulls) if which == "kv" else None),
+               "copy_ms": copy_ms, "GBps_copies_only": nbytes / (copy_ms * 1e-3) / 1e9 if copy_ms else None}
         if c0 is not None and c1 is not None:
             rx, tx = (c1[0] - c0[0]) / a.reps, (c1[1] - c0[1]) / a.reps
             rec.update({"counter_rx_bytes": rx, "counter_tx_bytes": tx,

@@ -125,6 +125,7 @@ def test_tiled_equals_dense(mask):
     (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "ring"),     # relays, unconsumed chunks
     (4, [1100, 513, 300, 129, 128, 127, 40, 9], 256, 1, "bytescale"),
     (8, [1500, 900, 513, 300, 129, 128, 127, 40, 9], 256, 16, "fcp"),  # the driver's N=8 run
+    (2, [3000, 1100, 513], 256, 16, "fcp"),     # received groups seen by prefixes (kv_limit)
 ])
 def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fuse):
     """Simulated workers: per-rank work lists + in-process exchange == dense attention,
@@ -136,6 +137,9 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
         assert all(sum(1 for wv in wk.fwd.waves if wv.stage >= 0) <= 1 for wk in works)
     if fuse == "all":        # one wave per rank: no partials, no merge
         assert all(len(wk.fwd.waves) == 1 and wk.fwd.partial_rows == 0 for wk in works)
+    if lengths[0] == 3000:   # multi-chunk received groups, visited by prefix-limited Q refs
+        assert any(k[0] == "recv" and k[3] != k[2] for wk in works for b in wk.bwd for k in b.kv_keys)
+        assert any((b.qrefs[:, 3] > 0).any() for wk in works for b in wk.bwd)
     goff, T = global_offsets(r)
     q, k, v, do = _inputs(T, 3)
     scale = 1 / math.sqrt(MODEL.head_dim)
