@@ -241,6 +241,15 @@ FCPB_API int fcpb_ipc_free(int device, void* ptr);
 FCPB_API int fcpb_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                           size_t height, void* stream);
 
+/* K5 pull kernel: copy `num_segs` byte ranges {dst, src, bytes} (a device array of
+ * FcpbGatherSeg; addresses 16-byte aligned, bytes a multiple of 16 and at most
+ * fcpb_gather_seg_bytes()) with SM loads -- src typically a peer's IPC region read over
+ * NVLink -- on `num_ctas` CTAs.  Used when nothing overlaps the forward pulls (one forward
+ * wave after the exchange), where it outruns copy-engine transfers of a few MB each. */
+typedef struct { uint64_t dst; uint64_t src; int64_t bytes; } FcpbGatherSeg;
+FCPB_API int fcpb_gather_copy(const void* segs, int32_t num_segs, int32_t num_ctas, void* stream);
+FCPB_API int64_t fcpb_gather_seg_bytes(void);
+
 /* Workspace queries: bytes the caller provides for
  *  - the backward preprocess outputs lse2_t + delta_t ([Hq, t_pad] fp32 each, t_pad = T
  *    rounded up to 4);

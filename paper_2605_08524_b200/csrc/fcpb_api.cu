@@ -13,6 +13,7 @@
 #include "attn_dqg_sm100.cuh"
 #include "attn_fwd_sm100.cuh"
 #include "aux_kernels.cuh"
+#include "p2p_kernels.cuh"
 
 namespace {
 
@@ -504,6 +505,19 @@ int fcpb_ipc_free(int device, void* ptr) {
   FCPB_CUDA(cudaFree(ptr));
   return FCPB_OK;
 }
+
+int fcpb_gather_copy(const void* segs, int32_t num_segs, int32_t num_ctas, void* stream) {
+  if (num_segs < 0 || num_ctas <= 0) return fail(FCPB_ERR_INVALID, "gather_copy: bad counts");
+  if (num_segs == 0) return FCPB_OK;
+  if (!segs) return fail(FCPB_ERR_INVALID, "gather_copy: null segment table");
+  const int grid = num_ctas < num_segs ? num_ctas : num_segs;
+  fcpb::p2p::gather_kernel<<<grid, fcpb::p2p::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const fcpb::p2p::Seg*>(segs), num_segs);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
+int64_t fcpb_gather_seg_bytes(void) { return fcpb::p2p::kSegBytes; }
 
 int fcpb_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                  size_t height, void* stream) {

@@ -23,6 +23,8 @@ every layer.  One process per GPU (torchrun); ``group`` is the NCCL group.
 
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -138,6 +140,12 @@ class FcpExecutor:
             self.xchg = SymmetricExchange(result, rank, cfg, self.device, group)
         # wave index by stage
         self.wave_of_stage = {self.op.wave_stage(i): i for i in range(self.op.num_waves)}
+        # One forward wave after the exchange (fuse_remote="all"): nothing overlaps the pulls,
+        # so they run as the K5 pull kernel on every SM instead of on copy engines
+        # (FCPB_PULL=ce keeps the copy engines).
+        self.sm_pull = (self.xchg is not None and self.fuse_remote == "all"
+                        and LOCAL_WAVE not in self.wave_of_stage
+                        and os.environ.get("FCPB_PULL", "sm") == "sm")
         H, Hk, D = cfg.q_heads, cfg.kv_heads, cfg.head_dim
         R = self.layout.recv_tokens
         # receive arena: K plane then V plane, so one 2-D copy moves a run of both
@@ -255,7 +263,17 @@ class FcpExecutor:
             cur.wait_event(pre_event)
         x = self.xchg
         events = []
-        if x is not None and self.stages:
+        if x is not None and self.stages and self.sm_pull:
+            cur.wait_stream(self.comm)
+            x.publish_kv(k, v)
+            x.barrier("kv", 0)                          # (compute stream) everyone's K/V readable
+            x.gather_all(self.kv_recv, cur)             # every stage's pulls, one launch
+            self._mark("comm_stage_done", cur)
+            events = [None] * len(self.stages)
+            self.comm.wait_stream(cur)
+            with torch.cuda.stream(self.comm):
+                x.barrier("kv", 1)                      # all pulls done: K/V reusable
+        elif x is not None and self.stages:
             # previous step's pulls of our K/V are complete (comm-stream order + barrier)
             cur.wait_stream(self.comm)
             x.publish_kv(k, v)
@@ -274,7 +292,8 @@ class FcpExecutor:
             self._mark("fwd_local", cur)
         for s_idx, ev in enumerate(events):
             if s_idx in self.wave_of_stage:
-                cur.wait_event(ev)
+                if ev is not None:
+                    cur.wait_event(ev)
                 op.forward_wave(self.wave_of_stage[s_idx], q, k, v, self.k_recv, self.v_recv, outs, cur)
                 self._mark(f"fwd_wave{s_idx}", cur)
         if events:
@@ -352,7 +371,8 @@ class FcpExecutor:
         return out
 
     def exchange_benchmark(self, reps: int = 5) -> dict | None:
-        """Isolated copy-engine exchange bandwidth of this rank (no attention running):
+        """Isolated exchange bandwidth of this rank (no attention running), over the
+        transport the step uses (the K5 pull kernel when ``sm_pull``, else copy engines):
         the forward K/V pulls of every stage and the backward partial-dKV returns, each
         bracketed by the same symmetric-memory barriers the step uses and timed with CUDA
         events on the comm stream.  GB/s = bytes this rank receives / time (the read
@@ -373,7 +393,9 @@ class FcpExecutor:
                     which = "kv" if name == "fwd_kv_pull" else "part"
                     x.barrier(which, 0)
                     s0.record(self.comm)
-                    if which == "kv":
+                    if which == "kv" and self.sm_pull:
+                        x.gather_all(self.kv_recv, self.comm)
+                    elif which == "kv":
                         for s_idx in range(len(self.stages)):
                             x.pull_stage(s_idx, self.kv_recv)
                     else:

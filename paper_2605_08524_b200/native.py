@@ -90,8 +90,9 @@ EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_
            "fcpb_last_error", "fcpb_version", "fcpb_device_supported",
            "fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes",
            "fcpb_debug_counters", "fcpb_ipc_alloc", "fcpb_ipc_open", "fcpb_ipc_close", "fcpb_ipc_free",
-           "fcpb_copy_2d")
+           "fcpb_copy_2d", "fcpb_gather_copy", "fcpb_gather_seg_bytes")
 _SIZE_T = ("fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes")
+_I64 = ("fcpb_gather_seg_bytes",)
 
 _lib = None
 
@@ -129,9 +130,12 @@ def load(path: str | None = None):
     lib.fcpb_copy_2d.argtypes = [c_vp, ctypes.c_size_t, c_vp, ctypes.c_size_t, ctypes.c_size_t,
                                  ctypes.c_size_t, c_vp]
     lib.fcpb_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_int]
+    lib.fcpb_gather_copy.argtypes = [c_vp, c_i32, c_i32, c_vp]
+    lib.fcpb_gather_seg_bytes.argtypes = []
     for name in EXPORTS:
         getattr(lib, name).restype = (ctypes.c_char_p if name == "fcpb_last_error" else
-                                      ctypes.c_size_t if name in _SIZE_T else ctypes.c_int)
+                                      ctypes.c_size_t if name in _SIZE_T else
+                                      ctypes.c_int64 if name in _I64 else ctypes.c_int)
     if path is None:
         _lib = lib
     return lib
@@ -158,6 +162,19 @@ def stream_handle(stream) -> int:
 def copy_2d(dst: int, dpitch: int, src: int, spitch: int, width: int, height: int, stream) -> None:
     """Device-to-device 2-D copy on `stream` (one copy-engine operation)."""
     check(load().fcpb_copy_2d(dst, dpitch, src, spitch, width, height, stream_handle(stream)))
+
+
+def gather_copy(segs, num_ctas: int, stream) -> None:
+    """K5 pull kernel: segs is a device int64 tensor [n, 3] of (dst, src, bytes) ranges
+    (``fcpb_gather_copy``), copied by SM loads on `num_ctas` CTAs, ordered on `stream`."""
+    if str(segs.dtype) != "torch.int64" or segs.dim() != 2 or segs.shape[1] != 3 or not segs.is_cuda:
+        raise ParameterError("gather_copy: segs must be a CUDA int64 tensor [n, 3]")
+    check(load().fcpb_gather_copy(segs.data_ptr(), segs.shape[0], num_ctas, stream_handle(stream)))
+
+
+def gather_seg_bytes() -> int:
+    """Largest byte range one fcpb_gather_copy segment may cover."""
+    return int(load().fcpb_gather_seg_bytes())
 
 
 def stream_signal(flag_addr: int, value: int, stream) -> None:

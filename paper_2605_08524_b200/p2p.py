@@ -337,6 +337,38 @@ class SymmetricExchange:
                            spitch, p.rows * row, 2, stream)
         self._fanout(pulls, sum(p.rows for p in pulls) * self.kv_row_bytes, pull)
 
+    GATHER_CTAS = 2 * 148       # two 512-thread CTAs per SM: 128 KB of peer loads in flight per SM
+
+    def gather_segments(self, kv_recv) -> list[tuple[int, int, int]]:
+        """Every stage's pulls as (dst, src, bytes) ranges for the pull kernel: one range per
+        plane of each merged run, split at ``native.gather_seg_bytes()``."""
+        base, dpitch, row = self._planes(kv_recv)
+        spitch = self.t_max * row
+        step = native.gather_seg_bytes()
+        segs = []
+        for pulls in self.stage_pulls:
+            for p in pulls:
+                n = p.rows * row
+                for plane in range(2):
+                    d = base + plane * dpitch + p.dst * row
+                    s_ = self.peer_kv[p.peer].data_ptr() + plane * spitch + p.src * row
+                    for o in range(0, n, step):
+                        segs.append((d + o, s_ + o, min(step, n - o)))
+        return segs
+
+    def gather_all(self, kv_recv, stream=None) -> None:
+        """All stages' K/V pulls as one pull-kernel launch on `stream` (SM loads from the
+        peers' regions over NVLink, ``fcpb_gather_copy``).  The segment table is built once
+        per receive arena and kept on the device."""
+        key = kv_recv.data_ptr()
+        if getattr(self, "_gather_key", None) != key:
+            segs = self.gather_segments(kv_recv)
+            self._gather_tab = torch.tensor(segs, dtype=torch.int64).reshape(-1, 3).to(self.device)
+            self._gather_key = key
+        if self._gather_tab.shape[0]:
+            native.gather_copy(self._gather_tab, self.GATHER_CTAS,
+                               stream or torch.cuda.current_stream(self.device))
+
     # ------------------------------------------------------------------ backward (K6)
     def partial_views(self):
         """dK/dV partial buffers for the received chunks (the dK/dV kernel writes them)."""

@@ -7,11 +7,11 @@ run) from a buffer on GPU 1 into a receive arena on GPU 0 -- the same bytes and 
 the executor issues, with the peer region replaced by a same-process peer buffer.  The
 copies sit inside a cudaProfilerStart/Stop range, so
 
-    ncu --replay-mode range --profile-from-start off \\
-        --metrics nvlrx__bytes.sum,nvltx__bytes.sum,gpu__time_duration.sum \\
+    ncu --replay-mode range --metrics nvlrx__bytes.sum,nvltx__bytes.sum,gpu__time_duration.sum \\
         python scripts/nvlink_ncu_probe.py --config c3 --world 2
 
-reports the NVLink bytes of GPU 0 during the range.  Without ncu it prints one JSON line with
+reports the NVLink bytes of GPU 0 during the range; with ``--mode sm`` the same bytes move by
+the K5 pull kernel (``fcpb_gather_copy``), which ncu also profiles in kernel mode.  Without ncu it prints one JSON line with
 the CUDA-event GB/s of the same copies (plan bytes / time).
 """
 import argparse
@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--mode", default="ce", choices=["ce", "sm"],
+                    help="ce: native.copy_2d per merged run; sm: the K5 pull kernel (fcpb_gather_copy)")
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs two GPUs in one process"
     w, result = bench.build_workload(a.config, a.world, None)
@@ -48,7 +50,16 @@ def main():
     st = torch.cuda.current_stream(d0)
     nbytes = sum(p.rows for p in pulls) * 2 * row
 
+    step = native.gather_seg_bytes()
+    segs = [(dst.data_ptr() + pl * dst_rows * row + p.dst * row + o,
+             src.data_ptr() + pl * src_rows * row + p.src * row + o, min(step, p.rows * row - o))
+            for p in pulls for pl in range(2) for o in range(0, p.rows * row, step)]
+    tab = torch.tensor(segs, dtype=torch.int64, device=d0)
+
     def pull_all():
+        if a.mode == "sm":
+            native.gather_copy(tab, 2 * 148, st)
+            return
         for p in pulls:
             native.copy_2d(dst.data_ptr() + p.dst * row, dst_rows * row, src.data_ptr() + p.src * row,
                            src_rows * row, p.rows * row, 2, st)
@@ -69,7 +80,8 @@ def main():
     pull_all()
     torch.cuda.synchronize(d0)
     torch.cuda.profiler.stop()
-    print(json.dumps({"what": "rank's forward pull list replayed GPU1 -> GPU0 with native.copy_2d",
+    print(json.dumps({"what": "rank's forward pull list replayed GPU1 -> GPU0 with "
+                              + ("native.copy_2d (copy engine)" if a.mode == "ce" else "the K5 pull kernel"),
                       "config": w.name, "world": a.world, "rank": a.rank, "copies": len(pulls),
                       "plan_bytes": nbytes, "mean_copy_MB": round(nbytes / len(pulls) / 1e6, 2),
                       "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "peak_GBps_per_direction": 900}),

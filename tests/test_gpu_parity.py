@@ -365,3 +365,29 @@ def test_c1_tiny_model_through_the_executor():
     og = ex.attention(qg, kg, vg)
     (og.float() * loc[3].float()).sum().backward()
     assert torch.equal(og.detach(), o) and torch.equal(qg.grad, dq) and torch.equal(kg.grad, dk)
+
+
+def test_gather_copy_pull_kernel_is_exact():
+    """K5 pull kernel (fcpb_gather_copy): byte-exact ranges, 16-byte granularity, full and
+    partial 64 KB segments, and nothing written outside the ranges."""
+    from paper_2605_08524_b200 import native
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    src = torch.randint(-2**31, 2**31 - 1, (1 << 22,), dtype=torch.int32, generator=g).to(dev)
+    dst = torch.zeros(1 << 22, dtype=torch.int32, device=dev)
+    step = native.gather_seg_bytes()
+    assert step % 16 == 0
+    # (src byte offset, dst byte offset, bytes): 16-byte aligned, sizes around the segment size
+    ranges = [(0, 1 << 20, 16), (4096, 0, step), (2 * step, 3 << 20, step - 16),
+              (5 << 20, 6 << 20, 3 * step + 48), (160, 8 << 20, 2048 * 7)]
+    segs = []
+    for so, do_, n in ranges:
+        for o in range(0, n, step):
+            segs.append((dst.data_ptr() + do_ + o, src.data_ptr() + so + o, min(step, n - o)))
+    tab = torch.tensor(segs, dtype=torch.int64, device=dev)
+    native.gather_copy(tab, 7, torch.cuda.current_stream(dev))
+    torch.cuda.synchronize(dev)
+    want = torch.zeros_like(dst)
+    for so, do_, n in ranges:
+        want[do_ // 4:(do_ + n) // 4] = src[so // 4:(so + n) // 4]
+    assert torch.equal(dst, want)
