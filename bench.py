@@ -537,6 +537,9 @@ def main():
 
     # isolated exchange bandwidth (N > 1): min over ranks of the per-rank receive GB/s
     xbw = ex.exchange_benchmark() if world > 1 else None
+    if xbw:
+        xbw["fwd_transport"] = ("K5 pull kernel (SM loads over NVLink)" if ex.sm_pull
+                                else "copy-engine 2-D pulls")
     if xbw is not None:
         for key in ("fwd_kv_pull", "bwd_dkv_return"):
             g = torch.tensor([xbw[key]["GBps"] or 0.0], device=device)

@@ -11,8 +11,8 @@ copies sit inside a cudaProfilerStart/Stop range, so
         python scripts/nvlink_ncu_probe.py --config c3 --world 2
 
 reports the NVLink bytes of GPU 0 during the range; with ``--mode sm`` the same bytes move by
-the K5 pull kernel (``fcpb_gather_copy``), which ncu also profiles in kernel mode.  Without ncu it prints one JSON line with
-the CUDA-event GB/s of the same copies (plan bytes / time).
+the K5 pull kernel (``fcpb_gather_copy``), which ncu also profiles in kernel mode.  Without
+ncu it prints one JSON line with the CUDA-event GB/s of the same copies (plan bytes / time).
 """
 import argparse
 import json
@@ -45,8 +45,15 @@ def main():
     d0, d1 = torch.device("cuda", 0), torch.device("cuda", 1)
     src = torch.randn((2, src_rows, Hk, D), device=d1).to(torch.bfloat16)
     dst = torch.zeros((2, dst_rows, Hk, D), device=d0, dtype=torch.bfloat16)
-    torch.zeros(1, device=d0).copy_(torch.zeros(1, device=d1))   # enables peer access 0 <-> 1
     torch.cuda.set_device(d0)
+    if True:   # peer access 0 -> 1, as the IPC mapping gives the product path (kernel loads need
+        # it; without it a copy-engine transfer between the GPUs is staged at ~30 GB/s)
+        import ctypes
+        import nvidia.cuda_runtime as crt
+        rt = ctypes.CDLL(os.path.join(crt.__path__[0], "lib", "libcudart.so.12"))
+        rt.cudaSetDevice(0)
+        rc = rt.cudaDeviceEnablePeerAccess(1, 0)
+        assert rc in (0, 704), f"cudaDeviceEnablePeerAccess: {rc}"   # 704: already enabled
     st = torch.cuda.current_stream(d0)
     nbytes = sum(p.rows for p in pulls) * 2 * row
 
@@ -76,10 +83,12 @@ def main():
     e.record(st)
     torch.cuda.synchronize(d0)
     ms = s.elapsed_time(e) / a.reps
+    torch.cuda.synchronize(d0)
     torch.cuda.profiler.start()                  # the ncu range: one pass of the pull list
     pull_all()
-    torch.cuda.synchronize(d0)
+    dst[0, 0, 0, :8].add_(0)                     # a kernel in the range (range replay needs one)
     torch.cuda.profiler.stop()
+    torch.cuda.synchronize(d0)
     print(json.dumps({"what": "rank's forward pull list replayed GPU1 -> GPU0 with "
                               + ("native.copy_2d (copy engine)" if a.mode == "ce" else "the K5 pull kernel"),
                       "config": w.name, "world": a.world, "rank": a.rank, "copies": len(pulls),

@@ -51,6 +51,7 @@ def test_executor_nccl_parity(n, sched):
     # ranks none of whose chunks is consumed remotely (no dK/dV comes back)
     (4, "fcp", ("2048,2048,4096", "2048"), "8,2"),
     (2, "fcp", ("9000,4100,3000,2100,1500,700,129", "2048"), "32,8"),   # Llama-3-8B heads
+    (8, "fcp", (), "8,2"),                      # the driver's N=8 path: 7 peers per rank
 ])
 def test_executor_shared_gpu_parity(n, sched, args, heads):
     """N ranks as N processes on GPU 0: the multi-rank product path on a one-GPU box."""
