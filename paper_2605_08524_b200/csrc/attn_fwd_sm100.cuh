@@ -16,6 +16,11 @@
 // 64 columns) overwrites the first half of S_h once S_h has been read.
 // MMA order per KV tile j:  PV0(j), S0(j+1), PV1(j), S1(j+1): the tensor pipe
 // runs one head's matmuls while the other head's warps do the softmax.
+// Stacked tails (stack_tails, GQA group a multiple of 4): the last Q tile of a segment with
+// at most 64 valid rows carries FOUR q-heads -- tile h holds the 64 rows of head 4k+2h in
+// TMEM lanes 0-63 and those of head 4k+2h+1 in lanes 64-127 (all four share the KV head) --
+// so a short Q run's ragged tail costs half a tile pair; the odd head pair of such an item
+// is empty.  At N >= 2 about 5% of C2's forward tiles are such tails.
 #pragma once
 #include "fcpb_types.h"
 #include "sm100_ptx.cuh"
@@ -76,7 +81,16 @@ struct Params {
   float* lse;            // [Tq, Hq]
   float* o_part;         // [P, Hq, D]
   float* lse_part;       // [P, Hq]
+  int32_t stack_tails;   // tail tiles with <= 64 rows carry four q-heads (group % 4 == 0)
 };
+
+constexpr int kStackRows = 64;   // a stacked tile: 64 rows of each of two q-heads
+
+// Does item `it` (128-row block of `seg`) run stacked?  The odd head pair of a stacked item
+// is empty (its four heads ran under the even pair).
+FCPB_DEV bool stacked(const Params& p, const FcpbSegment& seg, const FcpbItem& it) {
+  return p.stack_tails && seg.q_len - it.mblock * kBM <= kStackRows;
+}
 
 FCPB_DEV int item_of(int g, int hp, const Params& p) {
   int it, h;
@@ -177,6 +191,7 @@ static_assert(kRegsCtl + 2 * kRegsSoftmax <= 3 * kRegsLaunch,
 
 __global__ void __launch_bounds__(kThreads, 1)
 attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                const __grid_constant__ CUtensorMap tm_q64,   // Q with 64-row boxes (stacked tails)
                 const __grid_constant__ CUtensorMap tm_k,
                 const __grid_constant__ CUtensorMap tm_v,
                 const __grid_constant__ CUtensorMap tm_k_recv,
@@ -192,6 +207,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_q64);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_k_recv);
@@ -233,15 +249,27 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           const FcpbItem it = p.items[item_of(g, head_pairs, p)];
           const int hp = pair_of(g, head_pairs, p);
           const FcpbSegment seg = p.segs[it.seg];
+          const bool stk = stacked(p, seg, it);
+          if (stk && (hp & 1)) continue;             // ran under the even pair
           const int h0 = 2 * hp;
           const int kvh = h0 / group;
           const int row0 = seg.q_off + it.mblock * kBM;
           mbar_wait(&sm.q_empty, q_phase ^ 1);
           q_phase ^= 1;
           mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
-          for (int h = 0; h < 2; ++h)
-            for (int half = 0; half < 2; ++half)
-              tma_load_3d(&sm.q[h][half * kHalfBytes], &tm_q, &sm.q_full, half * 64, h0 + h, row0);
+          if (stk) {
+            // tile h: rows 0-63 of head h0+2h, then rows 0-63 of head h0+2h+1 (64-row boxes;
+            // 64 swizzled 128-byte rows = 8 KB, a whole number of 1 KB swizzle atoms)
+            for (int h = 0; h < 2; ++h)
+              for (int u = 0; u < 2; ++u)
+                for (int half = 0; half < 2; ++half)
+                  tma_load_3d(&sm.q[h][half * kHalfBytes + u * (kHalfBytes / 2)], &tm_q64, &sm.q_full,
+                              half * 64, h0 + 2 * h + u, row0);
+          } else {
+            for (int h = 0; h < 2; ++h)
+              for (int half = 0; half < 2; ++half)
+                tma_load_3d(&sm.q[h][half * kHalfBytes], &tm_q, &sm.q_full, half * 64, h0 + h, row0);
+          }
           for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
             const FcpbKvRef ref = p.kvrefs[r];
             const bool recv = ref.flags & FCPB_KV_RECV;
@@ -330,6 +358,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
         const FcpbItem it = p.items[item_of(g, head_pairs, p)];
         const FcpbSegment seg = p.segs[it.seg];
+        if (stacked(p, seg, it) && (pair_of(g, head_pairs, p) & 1)) continue;
         int n = 0;
         for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
         mbar_wait(&sm.q_full, q_phase);
@@ -388,8 +417,14 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     SchedCursor sc;
     for (int g; (g = sched_consume(sm.sched, sc)) < total;) {
       const FcpbItem it = p.items[item_of(g, head_pairs, p)];
-      const int head = 2 * pair_of(g, head_pairs, p) + h;
+      const int hp = pair_of(g, head_pairs, p);
       const FcpbSegment seg = p.segs[it.seg];
+      const bool stk = stacked(p, seg, it);
+      if (stk && (hp & 1)) continue;
+      // this thread's query: head and row inside the 128-row block (stacked: lanes 64-127
+      // hold the second head's rows 0-63)
+      const int head = stk ? 2 * hp + 2 * h + (row >> 6) : 2 * hp + h;
+      const int qr = stk ? (row & (kStackRows - 1)) : row;
       float m_run = -INFINITY, l_run = 0.f;
       bool first = true;
       for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
@@ -424,7 +459,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (diag && t == it.mblock) {
 #pragma unroll
             for (int i = 0; i < kBN; ++i)
-              if (i > row) s[i] = -INFINITY;
+              if (i > qr) s[i] = -INFINITY;
           } else if (valid < kBN) {
 #pragma unroll
             for (int i = 0; i < kBN; ++i)
@@ -482,7 +517,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&sm.o_full[h], o_phase);
       o_phase ^= 1;
       tc_fence_after();
-      const int qrow = it.mblock * kBM + row;
+      const int qrow = it.mblock * kBM + qr;
       const bool live = qrow < seg.q_len;
       const float inv_l = (l_run > 0.f) ? 1.f / l_run : 0.f;
       const float lse = (l_run > 0.f) ? (m_run == -INFINITY ? 0.f : m_run) * p.scale + logf(l_run)

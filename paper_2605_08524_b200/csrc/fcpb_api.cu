@@ -132,9 +132,10 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
     return fail(FCPB_ERR_UNSUPPORTED, "need Hq/Hkv even (Hq=%d Hkv=%d)", a->num_q_heads,
                 a->num_kv_heads);
   if (a->num_items <= 0) return FCPB_OK;
-  CUtensorMap tq, tk, tv, tkr, tvr;
+  CUtensorMap tq, tq64, tk, tv, tkr, tvr;
   int rc;
   if ((rc = make_map(&tq, a->q, a->q_tokens, a->num_q_heads, 128, 128))) return rc;
+  if ((rc = make_map(&tq64, a->q, a->q_tokens, a->num_q_heads, 128, fcpb::fwd::kStackRows))) return rc;
   if ((rc = make_map(&tk, a->k, a->kv_tokens, a->num_kv_heads, 128, 128))) return rc;
   if ((rc = make_map(&tv, a->v, a->kv_tokens, a->num_kv_heads, 128, 128))) return rc;
   const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
@@ -159,6 +160,12 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   p.lse_part = a->lse_partial;
   p.head_major = a->head_major;
   p.hm_lead = a->hm_lead;
+  // stacked tails need four q-heads per KV head (FCPB_FWD_STACK=0 turns them off)
+  static const bool stack_env = [] {
+    const char* e = getenv("FCPB_FWD_STACK");
+    return !(e && e[0] == '0');
+  }();
+  p.stack_tails = stack_env && (a->num_q_heads / a->num_kv_heads) % 4 == 0;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
@@ -168,7 +175,7 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
   fcpb::fwd::attn_fwd_kernel<<<grid, fcpb::fwd::kThreads, kFwdSmem,
-                               static_cast<cudaStream_t>(stream)>>>(tq, tk, tv, tkr, tvr, p);
+                               static_cast<cudaStream_t>(stream)>>>(tq, tq64, tk, tv, tkr, tvr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
