@@ -64,6 +64,12 @@ constexpr int kSoftmaxWGs = 4;
 constexpr int kCols = kBQ / kSoftmaxWGs;        // q columns per softmax warpgroup
 constexpr int kThreads = 128 * (1 + kSoftmaxWGs);
 constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 384;
+// Stacked tails (Params::stack_tails, GQA group even): the last Q block of a Q reference with
+// at most 64 valid rows is one 128-column tile for TWO q-heads of the group -- columns 0-63
+// are head gq's rows, 64-127 head gq+1's -- so dV and dK (summed over the group's heads
+// anyway) take both in one pass.  Its dS^T tile goes to head gq's slot; the dQ GEMM reads it
+// as 128 stacked rows (attn_dqg_sm100.cuh).
+constexpr int kStackRows = 64;
 // Register budget: 640 threads x 96 (the __launch_bounds__ allocation); the control and
 // softmax warpgroups both fit in it, so no setmaxnreg split is needed.
 constexpr uint32_t kRegsLaunch = 96;
@@ -126,6 +132,7 @@ struct Params {
   __nv_bfloat16* dv_out;
   __nv_bfloat16* ds_out;  // optional dS^T tiles [pairs * Hq][128 q / 8][128 kv][8 q] for the dQ GEMM
   const int32_t* pair_base;  // per item: first (kv block, q block) pair id (worklist.build_ds_tiles)
+  int32_t stack_tails;     // stacked tails (see kStackRows); requires an even GQA group
 };
 
 // Grid index -> (item, kv head).  head_major: neighbouring CTAs run neighbouring items of
@@ -148,6 +155,16 @@ FCPB_DEV int q_first_block(const QRef& qr, int nb) { return qr.diag ? nb : 0; }
 FCPB_DEV int q_end_block(const QRef& qr, int nb) {
   return (qr.kv_limit == 0 || nb * kBK < qr.kv_limit) ? (qr.q_len + kBQ - 1) / kBQ
                                                       : q_first_block(qr, nb);
+}
+// Is Q block mb of `qr` a stacked tail (two q-heads per tile)?
+FCPB_DEV bool stacked_block(const QRef& qr, int mb, int stack) {
+  return stack && qr.q_len - mb * kBQ <= kStackRows;
+}
+// (Q block, q-head) tiles of `qr` against KV block nb.
+FCPB_DEV int qref_tiles(const QRef& qr, int nb, int group, int stack) {
+  const int b0 = q_first_block(qr, nb), b1 = q_end_block(qr, nb);
+  if (b1 <= b0) return 0;
+  return (b1 - b0) * group - (stacked_block(qr, b1 - 1, stack) ? group / 2 : 0);
 }
 
 // 4-byte async copy with zero fill when !valid; completion tracked by an mbarrier.
@@ -255,6 +272,8 @@ FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const uint32_t (&p
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D], box (64,1,128)
                 const __grid_constant__ CUtensorMap tm_do,     // bf16 [Tq,Hq,D], box (64,1,128)
+                const __grid_constant__ CUtensorMap tm_q64,    // box (64,1,64): stacked tails
+                const __grid_constant__ CUtensorMap tm_do64,
                 const __grid_constant__ CUtensorMap tm_k,      // bf16 [Tkv,Hkv,D], box (64,1,128)
                 const __grid_constant__ CUtensorMap tm_v,
                 const __grid_constant__ CUtensorMap tm_k_recv,
@@ -275,6 +294,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_q64);
+    tma_prefetch_desc(&tm_do64);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_k_recv);
@@ -343,23 +364,36 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           const QRef qr = p.qrefs[r];
           for (int mb = q_first_block(qr, it.nblock); mb < q_end_block(qr, it.nblock); ++mb) {
             const int qrow = qr.q_off + mb * kBQ;
-            for (int gq = 0; gq < group; ++gq) {
+            const bool stk = stacked_block(qr, mb, p.stack_tails);
+            for (int gq = 0; gq < group; gq += stk ? 2 : 1) {
               const int h = kvh * group + gq;
               const uint32_t qs = qr_.slot, ds = dr_.slot;
+              // stacked: 64-row boxes of heads h and h+1 fill rows 0-63 and 64-127 of each
+              // 64-column panel (8 KB apart, whole 1 KB swizzle atoms)
+              auto load_tile = [&](uint8_t* dst, const CUtensorMap* m, const CUtensorMap* m64, uint64_t* bar) {
+                if (stk) {
+                  for (int u = 0; u < 2; ++u)
+                    for (int half = 0; half < 2; ++half)
+                      tma_load_3d_hint(dst + half * kQPanel + u * (kQPanel / 2), m64, bar, half * 64,
+                                       h + u, qrow, keep);
+                } else {
+                  for (int half = 0; half < 2; ++half)
+                    tma_load_3d_hint(dst + half * kQPanel, m, bar, half * 64, h, qrow, keep);
+                }
+              };
               mbar_wait(&sm.q_empty[qs], qr_.phase ^ 1);
               if (lane == 0) {
                 mbar_arrive_expect_tx(&sm.q_full[qs], kQBytes);
-                for (int half = 0; half < 2; ++half)
-                  tma_load_3d_hint(&sm.q[qs][half * kQPanel], &tm_q, &sm.q_full[qs],
-                                   half * 64, h, qrow, keep);
+                load_tile(sm.q[qs], &tm_q, &tm_q64, &sm.q_full[qs]);
               }
-              const float* lsrc = p.lse2_t + static_cast<int64_t>(h) * p.t_pad + qrow;
-              const float* dsrc = p.delta_t + static_cast<int64_t>(h) * p.t_pad + qrow;
+              // column i: head h (+1 for stacked columns 64-127), query row qrow + (i mod 64)
 #pragma unroll
               for (int u = 0; u < kBQ / 32; ++u) {
                 const int i = lane + 32 * u;
-                const bool ok = qrow + i < p.q_tokens;
-                cp_async_4(&sm.lse2[qs][i], ok ? lsrc + i : p.lse2_t, ok);
+                const int hi = stk ? h + (i >> 6) : h, ri = stk ? (i & (kStackRows - 1)) : i;
+                const bool ok = qrow + ri < p.q_tokens;
+                const float* src = p.lse2_t + static_cast<int64_t>(hi) * p.t_pad + qrow + ri;
+                cp_async_4(&sm.lse2[qs][i], ok ? src : p.lse2_t, ok);
               }
               cp_async_arrive_noinc(&sm.q_full[qs]);
               // the first Q tile of an item goes out before K/V (they only wait on the ring)
@@ -367,15 +401,15 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               mbar_wait(&sm.do_empty[ds], dr_.phase ^ 1);
               if (lane == 0) {
                 mbar_arrive_expect_tx(&sm.do_full[ds], kQBytes);
-                for (int half = 0; half < 2; ++half)
-                  tma_load_3d_hint(&sm.dout[ds][half * kQPanel], &tm_do, &sm.do_full[ds],
-                                   half * 64, h, qrow, keep);
+                load_tile(sm.dout[ds], &tm_do, &tm_do64, &sm.do_full[ds]);
               }
 #pragma unroll
               for (int u = 0; u < kBQ / 32; ++u) {
                 const int i = lane + 32 * u;
-                const bool ok = qrow + i < p.q_tokens;
-                cp_async_4(&sm.delta[ds][i], ok ? dsrc + i : p.delta_t, ok);
+                const int hi = stk ? h + (i >> 6) : h, ri = stk ? (i & (kStackRows - 1)) : i;
+                const bool ok = qrow + ri < p.q_tokens;
+                const float* src = p.delta_t + static_cast<int64_t>(hi) * p.t_pad + qrow + ri;
+                cp_async_4(&sm.delta[ds][i], ok ? src : p.delta_t, ok);
               }
               cp_async_arrive_noinc(&sm.do_full[ds]);
               qr_.next();
@@ -436,7 +470,7 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
         int n = 0;
         for (int r = ks.q_begin; r < ks.q_end; ++r) {
           const QRef qr = p.qrefs[r];
-          n += (q_end_block(qr, it.nblock) - q_first_block(qr, it.nblock)) * group;
+          n += qref_tiles(qr, it.nblock, group, p.stack_tails);
         }
         mbar_wait(&sm.kv_full, kv_phase);
         kv_phase ^= 1;
@@ -531,7 +565,9 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
           const int shift0 = it.nblock * kBK - mb * kBQ;
           const bool plain = kv_full_tile && q_valid >= kBQ && (!qr.diag || shift0 + kBK - 1 <= 0);
           const int shift = qr.diag ? shift0 + tid : -(1 << 30);
-          for (int gq = 0; gq < group; ++gq, ++tile) {
+          // stacked tail: two q-heads per tile (recomputed from q_valid where needed, which
+          // keeps the per-tile loop inside its 96 registers)
+          for (int gq = 0; gq < group; gq += (p.stack_tails && q_valid <= kStackRows) ? 2 : 1, ++tile) {
             uint32_t pr[kCols / 2];      // bf16 P pairs, phase 1 -> phase 2
             uint4* gdst = nullptr;
             if (p.ds_out) {
@@ -556,7 +592,10 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
               if (plain)
                 p_chunk<false>(sv, l2, sl2, pr, t_s, true, 0, 0, 0, &sm.p_half);
               else
-                p_chunk<true>(sv, l2, sl2, pr, t_s, kv_live, wg * kCols, q_valid, shift, &sm.p_half);
+                p_chunk<true>(sv, l2, sl2, pr, t_s, kv_live,
+                              // this warpgroup's first column as a query row of its head
+                              ((p.stack_tails && q_valid <= kStackRows) ? (wg & 1) : wg) * kCols,
+                              q_valid, shift, &sm.p_half);
             }
             FCPB_TR(kTrPSt, (int)tile);
             tmem_wait_st();

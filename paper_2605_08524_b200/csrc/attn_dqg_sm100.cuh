@@ -48,7 +48,16 @@ struct Params {
   int32_t head_major, hm_lead;
   float scale;
   __nv_bfloat16* dq;         // [Tq, Hq, D]
+  int32_t stack_tails;       // as fcpb_attn_bwd: a Q block with <= 64 rows has one dS^T tile
+                             // for q-heads (h, h+1), h even, rows stacked 0-63 / 64-127
 };
+
+constexpr int kStackRows = 64;
+// Item (Q block, head h) of a stacked tail: the even head computes both heads' rows; the odd
+// head's item is empty.
+FCPB_DEV bool stacked(const Params& p, const FcpbSegment& seg, const FcpbItem& it) {
+  return p.stack_tails && seg.q_len - it.mblock * kBM <= kStackRows;
+}
 
 FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
   int n = (ref.len + kBN - 1) / kBN;
@@ -101,6 +110,7 @@ attn_dqg_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant_
         grid_map(g, p.num_items, H, p.head_major, p.hm_lead, item, h);
         const FcpbItem it = p.items[item];
         const FcpbSegment seg = p.segs[it.seg];
+        if (stacked(p, seg, it) && (h & 1)) continue;
         const int kvh = h / group;
         int j = p.pair_off[item];
         for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
@@ -132,6 +142,7 @@ attn_dqg_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant_
       grid_map(g, p.num_items, H, p.head_major, p.hm_lead, item, h);
       const FcpbItem it = p.items[item];
       const FcpbSegment seg = p.segs[it.seg];
+      if (stacked(p, seg, it) && (h & 1)) continue;
       int n = 0;
       for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
       const uint32_t b = item_par;
@@ -168,14 +179,18 @@ attn_dqg_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant_
       grid_map(g, p.num_items, H, p.head_major, p.hm_lead, item, h);
       const FcpbItem it = p.items[item];
       const FcpbSegment seg = p.segs[it.seg];
+      const bool stk = stacked(p, seg, it);
+      if (stk && (h & 1)) continue;
       const uint32_t b = item_par;
       item_par ^= 1;
       mbar_wait(&sm.dq_full[b], full_phase[b]);
       full_phase[b] ^= 1;
       tc_fence_after();
-      const int qpos = it.mblock * kBM + row;
+      // stacked: accumulator rows 64-127 are head h+1's rows 0-63
+      const int qpos = it.mblock * kBM + (stk ? (row & (kStackRows - 1)) : row);
+      const int hh = stk ? h + (row >> 6) : h;
       const bool live = qpos < seg.q_len;
-      __nv_bfloat16* dst = p.dq + (static_cast<size_t>(seg.q_off + (live ? qpos : 0)) * H + h) * kD;
+      __nv_bfloat16* dst = p.dq + (static_cast<size_t>(seg.q_off + (live ? qpos : 0)) * H + hh) * kD;
 #pragma unroll
       for (int c = 0; c < kD / 32; ++c) {
         uint32_t v[32];

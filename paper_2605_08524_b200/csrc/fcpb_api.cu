@@ -75,6 +75,14 @@ int make_map(CUtensorMap* m, const void* base, int64_t tokens, int heads, int d,
   return FCPB_OK;
 }
 
+// Stacked ragged tails (two q-heads per 128-row tile when a Q block has <= 64 rows): on by
+// default; FCPB_FWD_STACK=0 / FCPB_BWD_STACK=0 turn off the forward / the backward (dK/dV and
+// the dQ GEMM, which must agree on it).
+bool env_on(const char* name) {
+  const char* e = getenv(name);
+  return !(e && e[0] == '0');
+}
+
 int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -160,11 +168,8 @@ int fcpb_attn_fwd(const FcpbFwdArgs* a, void* stream) {
   p.lse_part = a->lse_partial;
   p.head_major = a->head_major;
   p.hm_lead = a->hm_lead;
-  // stacked tails need four q-heads per KV head (FCPB_FWD_STACK=0 turns them off)
-  static const bool stack_env = [] {
-    const char* e = getenv("FCPB_FWD_STACK");
-    return !(e && e[0] == '0');
-  }();
+  // stacked tails need four q-heads per KV head
+  static const bool stack_env = env_on("FCPB_FWD_STACK");
   p.stack_tails = stack_env && (a->num_q_heads / a->num_kv_heads) % 4 == 0;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
@@ -186,11 +191,13 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   if (a->num_kv_heads <= 0 || a->num_q_heads % a->num_kv_heads)
     return fail(FCPB_ERR_UNSUPPORTED, "Hq %% Hkv != 0");
   if (a->num_items <= 0) return FCPB_OK;
-  CUtensorMap tq, tdo, tk, tv, tkr, tvr;
+  CUtensorMap tq, tdo, tq64, tdo64, tk, tv, tkr, tvr;
   int rc;
   const int H = a->num_q_heads, Hk = a->num_kv_heads;
   if ((rc = make_map(&tq, a->q, a->q_tokens, H, 128, fcpb::bwd::kBQ))) return rc;
   if ((rc = make_map(&tdo, a->dout, a->q_tokens, H, 128, fcpb::bwd::kBQ))) return rc;
+  if ((rc = make_map(&tq64, a->q, a->q_tokens, H, 128, fcpb::bwd::kStackRows))) return rc;
+  if ((rc = make_map(&tdo64, a->dout, a->q_tokens, H, 128, fcpb::bwd::kStackRows))) return rc;
   if ((rc = make_map(&tk, a->k, a->kv_tokens, Hk, 128, fcpb::bwd::kBK))) return rc;
   if ((rc = make_map(&tv, a->v, a->kv_tokens, Hk, 128, fcpb::bwd::kBK))) return rc;
   const bool has_recv = a->k_recv && a->v_recv && a->kv_recv_tokens > 0;
@@ -225,6 +232,8 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   p.dv_out = static_cast<__nv_bfloat16*>(a->dv_out);
   p.ds_out = static_cast<__nv_bfloat16*>(a->ds_out);
   p.pair_base = a->pair_base;
+  static const bool bwd_stack_env = env_on("FCPB_BWD_STACK");
+  p.stack_tails = bwd_stack_env && (H / Hk) % 2 == 0;
   if (p.ds_out && !p.pair_base) return fail(FCPB_ERR_INVALID, "ds_out needs pair_base");
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
@@ -235,7 +244,7 @@ int fcpb_attn_bwd(const FcpbBwdArgs* a, void* stream) {
   int grid = a->num_ctas > 0 ? a->num_ctas : sm_count();
   if (grid > total) grid = total;
   fcpb::bwd::attn_bwd_kernel<<<grid, fcpb::bwd::kThreads, kBwdSmem,
-                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tk, tv, tkr, tvr, p);
+                               static_cast<cudaStream_t>(stream)>>>(tq, tdo, tq64, tdo64, tk, tv, tkr, tvr, p);
   FCPB_CUDA(cudaGetLastError());
   return FCPB_OK;
 }
@@ -321,6 +330,8 @@ int fcpb_attn_bwd_dq_ds(const FcpbDqDsArgs* a, void* stream) {
   p.hm_lead = a->hm_lead;
   p.scale = a->softmax_scale;
   p.dq = static_cast<__nv_bfloat16*>(a->dq);
+  static const bool dqg_stack_env = env_on("FCPB_BWD_STACK");   // must match fcpb_attn_bwd's tiles
+  p.stack_tails = dqg_stack_env && (H / Hk) % 2 == 0;
   if (!a->sched_counter) return fail(FCPB_ERR_INVALID, "sched_counter is required");
   p.sched_counter = a->sched_counter;
   FCPB_CUDA(cudaMemsetAsync(a->sched_counter, 0, sizeof(int32_t), static_cast<cudaStream_t>(stream)));
