@@ -222,7 +222,7 @@ def emulate_forward(work, q, k, v, k_recv, v_recv, scale, dtype=torch.float64):
     lp = torch.full((f.partial_rows, H), -math.inf, dtype=dtype)
     for wave in f.waves:
         for seg_idx, mb in wave.items.tolist():
-            q_off, q_len, kb, ke, out_row, _ = wave.segments[seg_idx].tolist()
+            q_off, q_len, kb, ke, out_row, in_row = wave.segments[seg_idx].tolist()
             r0 = mb * TILE
             nrow = min(TILE, q_len - r0)
             qs = q[q_off + r0:q_off + r0 + nrow].to(dtype).transpose(0, 1)     # [H, n, D]
@@ -249,6 +249,12 @@ def emulate_forward(work, q, k, v, k_recv, v_recv, scale, dtype=torch.float64):
             l = p.sum(-1, keepdim=True)
             out = (torch.matmul(p, vv) / l).transpose(0, 1)
             ls = (m + torch.log(l)).squeeze(-1).transpose(0, 1)
+            if in_row > 0:     # continue an earlier wave's partial (worklist fuse_remote="resume")
+                pr = slice(in_row - 1 + r0, in_row - 1 + r0 + nrow)
+                l0, o0 = lp[pr], op[pr]
+                tot = torch.logaddexp(l0, ls)
+                out = torch.exp(l0 - tot).unsqueeze(-1) * o0 + torch.exp(ls - tot).unsqueeze(-1) * out
+                ls = tot
             if out_row < 0:
                 o[q_off + r0:q_off + r0 + nrow] = out
                 lse[q_off + r0:q_off + r0 + nrow] = ls

@@ -375,9 +375,10 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         issue_s(1, ks);
         commit(&sm.kv_empty[ks]);
         if (n == 1) commit(&sm.q_empty);
+        const bool resumed = seg.in_row > 0;      // O starts from an earlier wave's partial
         for (int j = 0; j < n; ++j) {
           const uint32_t vs = take_full();
-          pv(0, vs, j > 0);
+          pv(0, vs, j > 0 || resumed);
           FCPB_FWTR(kFwPv0Issue, trt);
           if (j == n - 1) commit(&sm.o_full[0]);
           uint32_t ks2 = 0;
@@ -388,7 +389,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
             issue_s(0, ks2);
             FCPB_FWTR(kFwS0Issue, trt + 1);
           }
-          pv(1, vs, j > 0);
+          pv(1, vs, j > 0 || resumed);
           FCPB_FWTR(kFwPv1Issue, trt);
           commit(&sm.kv_empty[vs]);
           if (j == n - 1) commit(&sm.o_full[1]);
@@ -427,6 +428,35 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       const int qr = stk ? (row & (kStackRows - 1)) : row;
       float m_run = -INFINITY, l_run = 0.f;
       bool first = true;
+      if (seg.in_row > 0) {
+        // Continue an earlier wave's (O, LSE) partial: O (normalised, fp32) into TMEM, the
+        // running max at LSE / scale with l = 1, so exp((s - m) * scale) = exp(s * scale - LSE)
+        // carries on exactly; the lazy rescale then applies to the loaded O.  The MMA warp's
+        // first PV accumulates onto it (its p_full wait orders after these stores).
+        const int qrow = it.mblock * kBM + qr;
+        const bool live = qrow < seg.q_len;
+        const size_t prow = static_cast<size_t>(seg.in_row - 1 + qrow) * p.num_q_heads + head;
+        const float4* src = reinterpret_cast<const float4*>(p.o_part + prow * kD);
+#pragma unroll 1
+        for (int c = 0; c < kD / 16; ++c) {
+          uint32_t v[16];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 x = live ? src[c * 4 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * i] = __float_as_uint(x.x);
+            v[4 * i + 1] = __float_as_uint(x.y);
+            v[4 * i + 2] = __float_as_uint(x.z);
+            v[4 * i + 3] = __float_as_uint(x.w);
+          }
+          tmem_st16(t_o + c * 16, v);
+        }
+        tmem_wait_st();
+        if (live) {
+          m_run = p.lse_part[prow] / p.scale;
+          l_run = 1.f;
+        }
+        first = false;
+      }
       for (int r = seg.kv_begin; r < seg.kv_end; ++r) {
         const FcpbKvRef ref = p.kvrefs[r];
         const int nt = kv_tiles(ref, it.mblock);

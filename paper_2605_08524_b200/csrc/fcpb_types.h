@@ -14,7 +14,8 @@ typedef struct {
   int32_t kv_begin;  // [kv_begin, kv_end) into the FcpbKvRef array
   int32_t kv_end;
   int32_t out_row;   // -1: write final O/LSE at q_off; >= 0: fp32 partial rows at out_row
-  int32_t pad_;
+  int32_t in_row;    // forward: 0, or 1 + the fp32 partial row block (O, LSE) an earlier wave
+                     // wrote for this Q chunk, which this segment continues (no K3 merge)
 } FcpbSegment;
 
 // One KV chunk reference.

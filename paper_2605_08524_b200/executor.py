@@ -163,11 +163,10 @@ class FcpExecutor:
         last arrival stage ("all"): no fp32 partials, no LSE merge and one launch tail, for
         the price of the exposed exchange.  Measured at N=4 (`gpurun_out/abm1_*`): C2 4.78 vs
         4.80-4.88 ms, C3 621.4-621.7 vs 621.9-623.6 ms against a local wave overlapped with
-        the pulls plus one fused remote wave.  FCPB_FUSE_REMOTE=0/1/all overrides."""
-        import os
+        the pulls plus one fused remote wave.  FCPB_FUSE_REMOTE=0/1/all/resume overrides."""
         env = os.environ.get("FCPB_FUSE_REMOTE")
         if env is not None:
-            return "all" if env == "all" else env == "1"
+            return env if env in ("all", "resume") else env == "1"
         waves = self.work.fwd.waves
         if self.world == 1 or not any(w.stage >= 0 for w in waves):
             return False

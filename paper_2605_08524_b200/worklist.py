@@ -383,14 +383,19 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
     one wave released by this rank's last arrival stage (one launch, one tail, and at most a
     local and a remote partial per Q run) instead of one wave per coalesced stage;
     fuse_remote="all": the local tiles join that wave too (no partials, no merge) -- for ranks
-    whose exchange is short next to their compute.
+    whose exchange is short next to their compute.  fuse_remote="resume": local wave plus one
+    fused remote wave, the remote wave *continuing* each Q run from the local wave's fp32
+    (O, LSE) partial (``FcpbSegment.in_row``) and writing the final O -- the local tiles hide
+    the exchange and no K3 merge runs.
     resident: chunks whose Q/K/V rows are in place before the reshuffle into the FCP layout
     completes (they stay on this rank); tiles of a resident Q run against a resident local run
     form PRE_WAVE, which runs while the reshuffle pulls the other rows."""
     deps = result.deps
     last_stage = max(lay.recv_stage.values(), default=LOCAL_WAVE)
-    runs, sources = _runs_and_sources(result, lay, stage_split=fuse_remote != "all")
+    runs, sources = _runs_and_sources(result, lay, stage_split=not fuse_remote)
     resident = frozenset(resident or ())
+
+    chain = fuse_remote == "resume"
 
     def wave_of(kv):
         if kv not in lay.recv_offset:
@@ -424,13 +429,19 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
     wave_ids = sorted({w for waves in per_q.values() for w in waves})
     part_rows = 0
     partial_of: dict = {}                 # run key -> [(wave, row)]
-    seg_rows: dict = {}
+    seg_rows: dict = {}                   # (run, wave) -> partial rows it writes
+    seg_in: dict = {}                     # (run, wave) -> partial rows it continues (chain)
     for R in runs:
-        waves = per_q[R.key]
+        waves = sorted(per_q[R.key])
         if len(waves) > 1:
-            for w in sorted(waves):
+            for i, w in enumerate(waves):
+                if chain and i > 0:
+                    seg_in[(R.key, w)] = seg_rows[(R.key, waves[i - 1])]
+                if chain and i == len(waves) - 1:
+                    continue              # the last wave of a chain writes the final O
                 seg_rows[(R.key, w)] = part_rows
-                partial_of.setdefault(R.key, []).append((w, part_rows))
+                if not chain:
+                    partial_of.setdefault(R.key, []).append((w, part_rows))
                 part_rows += R.tokens
     out = []
     for w in wave_ids:
@@ -446,8 +457,9 @@ def build_forward(result: ScheduleResult, lay: RankLayout, fuse_remote: bool = F
             else:
                 pairs += _run_pairs(result, R, lambda kv: wave_of(kv) == w and (R.key, kv) not in pre_pairs)
             out_row = seg_rows.get((R.key, w), -1)
+            in_row = seg_in[(R.key, w)] + 1 if (R.key, w) in seg_in else 0
             sidx = len(segs)
-            segs.append((R.off, R.tokens, begin, len(refs), out_row, 0))
+            segs.append((R.off, R.tokens, begin, len(refs), out_row, in_row))
             for mb in range(_cdiv(R.tokens, TILE)):
                 items.append((_ref_cost(kvs, mb), sidx, mb, R.seq))
         items = _lpt_order(items)

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--mode", default="ce", choices=["ce", "sm"],
                     help="ce: native.copy_2d per merged run; sm: the K5 pull kernel (fcpb_gather_copy)")
+    ap.add_argument("--busy", action="store_true",
+                    help="ce: time the pulls on a side stream while bf16 GEMMs keep every SM busy")
     a = ap.parse_args()
     assert torch.cuda.device_count() >= 2, "needs two GPUs in one process"
     w, result = bench.build_workload(a.config, a.world, None)
@@ -77,6 +79,16 @@ def main():
     for p in pulls[:8]:                          # spot-check the copied bytes
         assert torch.equal(dst[:, p.dst:p.dst + p.rows].cpu(), src[:, p.src:p.src + p.rows].cpu())
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if a.busy:                                   # GEMMs on the default stream, pulls beside them
+        side = torch.cuda.Stream(device=d0)
+        x = torch.randn(8192, 8192, device=d0, dtype=torch.bfloat16)
+        for _ in range(3):
+            x @ x
+        torch.cuda.synchronize(d0)
+        for _ in range(20):                      # ~20 x 0.7 ms of tensor work queued first
+            x @ x
+        st = side
+        torch.cuda.synchronize(d1)
     s.record(st)
     for _ in range(a.reps):
         pull_all()
@@ -92,6 +104,7 @@ def main():
     print(json.dumps({"what": "rank's forward pull list replayed GPU1 -> GPU0 with "
                               + ("native.copy_2d (copy engine)" if a.mode == "ce" else "the K5 pull kernel"),
                       "config": w.name, "world": a.world, "rank": a.rank, "copies": len(pulls),
+                      "beside_busy_sms": a.busy,
                       "plan_bytes": nbytes, "mean_copy_MB": round(nbytes / len(pulls) / 1e6, 2),
                       "ms": ms, "GBps": nbytes / (ms * 1e-3) / 1e9, "peak_GBps_per_direction": 900}),
           flush=True)

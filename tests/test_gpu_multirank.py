@@ -24,12 +24,12 @@ def _port():
         return s.getsockname()[1]
 
 
-def _run(n, sched="fcp", shared=False, args=(), heads="8,2", dim=128):
+def _run(n, sched="fcp", shared=False, args=(), heads="8,2", dim=128, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mp_gpu_check.py"), *args]
     env = dict(os.environ, FCPB_CHECK_SCHED=sched, FCPB_CHECK_HEADS=heads, FCPB_CHECK_DIM=str(dim),
-               FCPB_SHARED_GPU="1" if shared else "0")
+               FCPB_SHARED_GPU="1" if shared else "0", **(env or {}))
     proc = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     print(proc.stdout[-4000:])
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
@@ -57,3 +57,9 @@ def test_executor_shared_gpu_parity(n, sched, args, heads):
     """N ranks as N processes on GPU 0: the multi-rank product path on a one-GPU box."""
     heads, _, dim = heads.partition(":")
     _run(n, sched, shared=True, args=args, heads=heads, dim=int(dim or 128))
+
+
+def test_executor_shared_gpu_resumed_forward():
+    """The executor with the local wave overlapped with copy-engine pulls and the remote wave
+    continuing its partials (FCPB_FUSE_REMOTE=resume), 3 ranks on GPU 0."""
+    _run(3, shared=True, env={"FCPB_FUSE_REMOTE": "resume"})

@@ -236,6 +236,14 @@ def test_fwd_bwd_four_simulated_ranks_fused_remote_wave():
                 name="ragged N=4 fused remote wave")
 
 
+@pytest.mark.parametrize("n", [4, 8])
+def test_fwd_resume_chained_partials(n):
+    """fuse_remote="resume": the remote wave continues each Q run from the local wave's fp32
+    (O, LSE) partial in the forward kernel (FcpbSegment.in_row), no K3 merge."""
+    _full_check([4000, 3100, 2100, 1000, 700, 129, 128, 5], n, 512, GQA_SMALL, fuse_remote="resume",
+                name=f"ragged N={n} resumed remote wave")
+
+
 def test_fwd_bwd_recompute_dq(monkeypatch):
     """The recompute dQ kernel (K2b), used when dS does not fit in HBM (C3, C4): forced
     here on a case the default would run with materialised dS."""

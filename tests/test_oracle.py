@@ -116,7 +116,7 @@ def test_tiled_equals_dense(mask):
     assert torch.allclose(l1, l2, atol=1e-10)
 
 
-@pytest.mark.parametrize("fuse", [False, True, "all"])
+@pytest.mark.parametrize("fuse", [False, True, "all", "resume"])
 @pytest.mark.parametrize("n,lengths,block,coalesce,sched", [
     (1, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
     (2, [700, 260, 130, 100, 50, 9], 256, 16, "fcp"),
@@ -137,6 +137,10 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
         assert all(sum(1 for wv in wk.fwd.waves if wv.stage >= 0) <= 1 for wk in works)
     if fuse == "all":        # one wave per rank: no partials, no merge
         assert all(len(wk.fwd.waves) == 1 and wk.fwd.partial_rows == 0 for wk in works)
+    if fuse == "resume":     # chained partials: no merge groups; some segment continues one
+        assert all(len(wk.fwd.merge_groups) == 0 for wk in works)
+        if n > 1:
+            assert any((wv.segments[:, 5] > 0).any() for wk in works for wv in wk.fwd.waves)
     if lengths[0] == 3000:   # multi-chunk received groups, visited by prefix-limited Q refs
         assert any(k[0] == "recv" and k[3] != k[2] for wk in works for b in wk.bwd for k in b.kv_keys)
         assert any((b.qrefs[:, 3] > 0).any() for wk in works for b in wk.bwd)
@@ -176,7 +180,7 @@ def test_worklist_emulation_matches_dense(n, lengths, block, coalesce, sched, fu
         scatter_rank(dv_loc[w], dv, work.layout, goff, deps)
     for a, b in ((o, o_ref), (lse, l_ref), (dq, dq_ref), (dk, dk_ref), (dv, dv_ref)):
         assert torch.allclose(a, b, atol=1e-9), (a - b).abs().max()
-    if n > 1 and fuse != "all":
+    if n > 1 and fuse not in ("all", "resume"):
         assert any(wk.fwd.partial_rows for wk in works)   # the merge path was exercised
 
 
