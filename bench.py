@@ -519,6 +519,10 @@ def main():
         ex.step(q, k, v, do)
     phases = ex.phases()
     ex.timeline(False)
+    phases_all = None
+    if world > 1:               # every rank's timeline: who waits for whom at the barriers
+        phases_all = [None] * world
+        dist.all_gather_object(phases_all, {kk: round(vv, 3) for kk, vv in phases.items()})
     # e2e: host buffers in, results out, through the public executor API
     e2e = None
     if not args.no_e2e:
@@ -685,6 +689,7 @@ def main():
             "exchange_bw_rank0": xbw,
             "reshuffle": reshuffle,
             "phases_ms_rank0": {kk: round(vv, 3) for kk, vv in phases.items()},
+            "phases_ms_all_ranks": phases_all,
             "comp_imbalance": (max(loads.compute_flops) - sum(loads.compute_flops) / n) / max(loads.compute_flops),
             "gpu_launches": launches,
             "clocks": clocks.summary(),
