@@ -15,7 +15,9 @@ paper on the reference's data model:
 * GQA: q-head h reads kv-head h // (Hq/Hkv) (convention; the reference is silent).
 
 Three levels, each checked against the previous one in ``tests/``:
-  1. ``mono_*``      per-sequence dense attention (float64 or float32, torch CPU);
+  1. ``mono_*``      per-sequence dense attention (float64 or float32, torch; it runs on
+                     the device its inputs live on -- the GPU suites feed it CUDA fp64
+                     tensors so the fp64 checker takes seconds, not minutes);
   2. ``tiled_fwd``   the same computed tile by tile with an LSE merge;
   3. ``emulate_*``   an interpreter of the device work lists (``worklist.py``)
                      that walks segments / KV refs / 128-row items exactly as the
@@ -80,11 +82,13 @@ def mono_fwd(q, k, v, rows, scale, causal=True, dtype=torch.float64):
     One (sequence, head) at a time so the L x L score matrix stays bounded."""
     T, H, D = q.shape
     group = H // k.shape[1]
-    o = torch.zeros((T, H, D), dtype=dtype)
-    lse = torch.full((T, H), -math.inf, dtype=dtype)
+    dev = q.device        # the oracle's arithmetic runs wherever its inputs live (fp64 either way)
+    o = torch.zeros((T, H, D), dtype=dtype, device=dev)
+    lse = torch.full((T, H), -math.inf, dtype=dtype, device=dev)
     for idx in rows.values():
+        idx = idx.to(dev)
         L = idx.numel()
-        keep = torch.ones(L, L, dtype=torch.bool).tril() if causal else None
+        keep = torch.ones(L, L, dtype=torch.bool, device=dev).tril() if causal else None
         for h in range(H):
             qs = q[idx, h].to(dtype)
             ks = k[idx, h // group].to(dtype)
@@ -105,12 +109,14 @@ def mono_bwd(q, k, v, o, lse, do, rows, scale, causal=True, dtype=torch.float64)
     T, H, D = q.shape
     Hk = k.shape[1]
     group = H // Hk
-    dq = torch.zeros((T, H, D), dtype=dtype)
-    dk = torch.zeros((T, Hk, D), dtype=dtype)
-    dv = torch.zeros((T, Hk, D), dtype=dtype)
+    dev = q.device
+    dq = torch.zeros((T, H, D), dtype=dtype, device=dev)
+    dk = torch.zeros((T, Hk, D), dtype=dtype, device=dev)
+    dv = torch.zeros((T, Hk, D), dtype=dtype, device=dev)
     for idx in rows.values():
+        idx = idx.to(dev)
         L = idx.numel()
-        keep = torch.ones(L, L, dtype=torch.bool).tril() if causal else None
+        keep = torch.ones(L, L, dtype=torch.bool, device=dev).tril() if causal else None
         for h in range(H):
             kh = h // group
             qs = q[idx, h].to(dtype)
@@ -138,14 +144,16 @@ def chunk_fwd_bwd(q, k, v, do, q_rows, kv_rows, diag_from, scale, dtype=torch.fl
     H, Hk = q.shape[1], k.shape[1]
     group = H // Hk
     qn, kn = q_rows.numel(), kv_rows.numel()
-    keep = torch.ones(qn, kn, dtype=torch.bool)
-    keep[:, diag_from:] = torch.ones(qn, kn - diag_from, dtype=torch.bool).tril()
+    dev = q.device
+    q_rows, kv_rows = q_rows.to(dev), kv_rows.to(dev)
+    keep = torch.ones(qn, kn, dtype=torch.bool, device=dev)
+    keep[:, diag_from:] = torch.ones(qn, kn - diag_from, dtype=torch.bool, device=dev).tril()
     D = q.shape[2]
-    o = torch.empty((qn, H, D), dtype=dtype)
-    lse = torch.empty((qn, H), dtype=dtype)
-    dq = torch.empty((qn, H, D), dtype=dtype)
-    dk = torch.zeros((kn, Hk, D), dtype=dtype)
-    dv = torch.zeros((kn, Hk, D), dtype=dtype)
+    o = torch.empty((qn, H, D), dtype=dtype, device=dev)
+    lse = torch.empty((qn, H), dtype=dtype, device=dev)
+    dq = torch.empty((qn, H, D), dtype=dtype, device=dev)
+    dk = torch.zeros((kn, Hk, D), dtype=dtype, device=dev)
+    dv = torch.zeros((kn, Hk, D), dtype=dtype, device=dev)
     for h in range(H):
         kh = h // group
         qs, dos = q[q_rows, h].to(dtype), do[q_rows, h].to(dtype)

@@ -86,6 +86,17 @@ struct Params {
 
 constexpr int kStackRows = 64;   // a stacked tile: 64 rows of each of two q-heads
 
+// mbarrier waits on the tile chain: bit 1 = the MMA warp's P waits, bit 2 = the softmax
+// warps' S waits, bit 4 = the MMA warp's K/V waits spin (test_wait) instead of suspending.
+#ifndef FCPB_FWD_SPIN
+#define FCPB_FWD_SPIN 0
+#endif
+template <int kBit>
+FCPB_DEV void chain_wait(uint64_t* bar, uint32_t parity) {
+  if (FCPB_FWD_SPIN & kBit) mbar_wait_spin(bar, parity);
+  else mbar_wait(bar, parity);
+}
+
 // Does item `it` (128-row block of `seg`) run stacked?  The odd head pair of a stacked item
 // is empty (its four heads ran under the even pair).
 FCPB_DEV bool stacked(const Params& p, const FcpbSegment& seg, const FcpbItem& it) {
@@ -333,11 +344,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       // wait for P_h(j) (in two parts when split) and issue O_h += P_h V_j
       auto pv = [&](int h, uint32_t vslot, bool acc) {
         if (kPSplit > 0) {
-          mbar_wait(&sm.p_part[h], p_phase);
+          chain_wait<1>(&sm.p_part[h], p_phase);
           tc_fence_after();
           issue_pv(h, vslot, acc, 0, kKkSplit);
         }
-        mbar_wait(&sm.p_full[h], p_phase);
+        chain_wait<1>(&sm.p_full[h], p_phase);
         if (h == 0) FCPB_FWTR(kFwP0Got, trt); else FCPB_FWTR(kFwP1Got, trt);
         tc_fence_after();
         issue_pv(h, vslot, acc, kPSplit > 0 ? kKkSplit : 0, kBN / 16);
@@ -349,7 +360,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       // Take the next ring position and wait until TMA has filled it.
       auto take_full = [&]() {
         const uint32_t cur = slot;
-        mbar_wait(&sm.kv_full[cur], slot_phase);
+        chain_wait<4>(&sm.kv_full[cur], slot_phase);
         if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
         return cur;
       };
@@ -462,7 +473,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         const int nt = kv_tiles(ref, it.mblock);
         const bool diag = ref.flags & FCPB_KV_DIAG;
         for (int t = 0; t < nt; ++t) {
-          mbar_wait(&sm.s_full[h], s_phase);
+          chain_wait<2>(&sm.s_full[h], s_phase);
           s_phase ^= 1;
           if (h == 0) FCPB_FWTR(kFwS0Got, trt); else FCPB_FWTR(kFwS1Got, trt);
           tc_fence_after();

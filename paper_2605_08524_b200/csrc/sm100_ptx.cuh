@@ -64,14 +64,35 @@ FCPB_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef FCPB_TRYWAIT_NS
+#define FCPB_TRYWAIT_NS 0x989680u
+#endif
+// try_wait without a suspend-time hint lowers to SYNCS.PHASECHK.TRYWAIT (the hardware wait
+// with its own short limit, then YIELD); with a hint it lowers to PHASECHK + NANOSLEEP.SYNCS,
+// whose wake-up sits on every producer->consumer hand-off of the tile chains.  ncu cycles on
+// C2 N=1 (r02, scripts/ab_cycles.sh): K1 5.82M -> 5.60M, K2 10.17M -> 9.63M, K2c unchanged;
+// hints of 20 / 200 / 2,000 ns behave like the 10 ms one.
+#ifndef FCPB_TRYWAIT_HINT
+#define FCPB_TRYWAIT_HINT 0
+#endif
 FCPB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if !FCPB_TRYWAIT_HINT
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(FCPB_TRYWAIT_NS)
       : "memory");
   return ok != 0;
 }

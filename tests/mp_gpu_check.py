@@ -62,9 +62,11 @@ def main():
     torch.cuda.synchronize()
     rows = global_sequence_rows(r)
     scale = 1 / math.sqrt(model.head_dim)
-    qf, kf, vf, dof = (x.double() for x in (q, k, v, do))
+    qf, kf, vf, dof = (x.to(dev, torch.float64) for x in (q, k, v, do))   # fp64 checker on the GPU
     ro, rl = mono_fwd(qf, kf, vf, rows, scale)
     rdq, rdk, rdv = mono_bwd(qf, kf, vf, ro, rl, dof, rows, scale)
+    ro, rl, rdq, rdk, rdv = (x.cpu() for x in (ro, rl, rdq, rdk, rdv))
+    del qf, kf, vf, dof
     rep = {}
     for name, got, ref in (("o", o, ro), ("lse", lse, rl), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
         rep[name] = err(got.cpu(), gather_rank(ref, lay, goff, r.deps))

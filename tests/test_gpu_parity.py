@@ -140,7 +140,8 @@ def _last_chunk_check(lengths, block, model, name, env=None, monkeypatch=None, e
     L = idx.numel()
     q_rows, kv_rows = idx[L - m:], idx
     scale = 1.0 / math.sqrt(model.head_dim)
-    o, lse, dq, dk, dv = chunk_fwd_bwd(q, k, v, do, q_rows, kv_rows, L - m, scale, torch.float64)
+    o, lse, dq, dk, dv = (x.cpu() for x in chunk_fwd_bwd(q.cuda(), k.cuda(), v.cuda(), do.cuda(), q_rows,
+                                                         kv_rows, L - m, scale, torch.float64))
     ref = {"o": o, "lse": lse, "dq": dq, "dk": dk[L - m:], "dv": dv[L - m:]}
     b = bf16_chunk_reference(q, k, v, do, q_rows, kv_rows, L - m, scale)
     b["dk"], b["dv"] = b["dk"][L - m:], b["dv"][L - m:]
