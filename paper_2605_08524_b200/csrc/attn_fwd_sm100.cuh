@@ -31,7 +31,7 @@ namespace fwd {
 #ifdef FCPB_TRACE
 constexpr int kTraceTiles = 256;
 enum FwdEv { kFwKGot, kFwS0Issue, kFwP0Got, kFwPv0Issue, kFwP1Got, kFwPv1Issue, kFwS0Got, kFwP0Arrive,
-             kFwS1Got, kFwP1Arrive, kFwEvents };
+             kFwS1Got, kFwP1Arrive, kFwSLd0, kFwMax0, kFwExp0, kFwEvents };
 __device__ unsigned long long g_trace[kFwEvents * kTraceTiles];
 #define FCPB_FWTR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
     ((ev) < kFwS0Got ? true : (threadIdx.x == 128 || threadIdx.x == 256))) \
@@ -61,6 +61,7 @@ struct Smem {
   uint64_t q_full, q_empty;
   uint64_t kv_full[kSlots], kv_empty[kSlots];
   uint64_t s_full[2], p_part[2], p_full[2], o_full[2], o_empty[2];
+  uint64_t e_done[2];                 // head h finished the exponentials of a tile (FCPB_FWD_ALT)
   SchedRing sched;
   uint32_t tmem_base;
 };
@@ -86,14 +87,34 @@ struct Params {
 
 constexpr int kStackRows = 64;   // a stacked tile: 64 rows of each of two q-heads
 
+// MUFU turns (FCPB_FWD_ALT): the two heads' exp phases strictly alternate -- head 0 tile j,
+// head 1 tile j, head 0 tile j+1, ... -- each waiting for the other's e_done before its first
+// exponential (its S load, masking and row max overlap the other head's exponentials).  Left
+// to themselves the heads settle with their exp phases half overlapped, sharing the SMSP's
+// MUFU, which stretches every softmax (S in registers -> P released ~2,000 cycles, tile-pair
+// period ~3,300: r02 trace) and, through the chain S -> softmax -> PV -> S, the period.
+#ifndef FCPB_FWD_ALT
+#define FCPB_FWD_ALT 0    // measured: 5.59M -> 5.88M cycles with the turns (r02), so off
+#endif
+
 // mbarrier waits on the tile chain: bit 1 = the MMA warp's P waits, bit 2 = the softmax
 // warps' S waits, bit 4 = the MMA warp's K/V waits spin (test_wait) instead of suspending.
 #ifndef FCPB_FWD_SPIN
 #define FCPB_FWD_SPIN 0
 #endif
+// Sleeping (hinted) waits per role: bit 1 = TMA producer, bit 2 = MMA warp.
+#ifndef FCPB_FWD_SLEEP
+#define FCPB_FWD_SLEEP 0
+#endif
 template <int kBit>
 FCPB_DEV void chain_wait(uint64_t* bar, uint32_t parity) {
   if (FCPB_FWD_SPIN & kBit) mbar_wait_spin(bar, parity);
+  else if ((kBit & 5) && (FCPB_FWD_SLEEP & 2)) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
+template <int kRole>
+FCPB_DEV void role_wait(uint64_t* bar, uint32_t parity) {
+  if (FCPB_FWD_SLEEP & kRole) mbar_wait_sleep(bar, parity);
   else mbar_wait(bar, parity);
 }
 
@@ -125,7 +146,7 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
 // (16 columns per 32 scores), returns the row sum.  kPoly: pairs 8u+8-kPolyPairs..8u+7 use
 // ex2_poly2 (finite inputs only).
 #ifndef FCPB_FWD_POLY_PAIRS
-#define FCPB_FWD_POLY_PAIRS 0    // measured: 2/3/4 pairs cost +1/+3/+6% fwd cycles (issue-bound)
+#define FCPB_FWD_POLY_PAIRS 1    // ncu C2 (r02): 1 pair of 8 -2.0% cycles, 2 pairs -1.1%
 #endif
 constexpr int kPolyPairs = FCPB_FWD_POLY_PAIRS;
 // Row sum off the P chain (FA4-style): the exponentials overwrite the scores in registers
@@ -237,6 +258,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_init(&sm.p_full[h], 128);
       mbar_init(&sm.o_full[h], 1);
       mbar_init(&sm.o_empty[h], 128);
+      mbar_init(&sm.e_done[h], 4);
     }
     sched_init(sm.sched, 1 + 8);
     fence_barrier_init();
@@ -265,7 +287,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           const int h0 = 2 * hp;
           const int kvh = h0 / group;
           const int row0 = seg.q_off + it.mblock * kBM;
-          mbar_wait(&sm.q_empty, q_phase ^ 1);
+          role_wait<1>(&sm.q_empty, q_phase ^ 1);
           q_phase ^= 1;
           mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
           if (stk) {
@@ -290,7 +312,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
             for (int t = 0; t < nt; ++t) {
               const int krow = ref.off + t * kBN;
               for (int kv = 0; kv < 2; ++kv) {
-                mbar_wait(&sm.kv_empty[slot], slot_phase ^ 1);
+                role_wait<1>(&sm.kv_empty[slot], slot_phase ^ 1);
                 mbar_arrive_expect_tx(&sm.kv_full[slot], kTileBytes);
                 const CUtensorMap* m = kv ? mv : mk;
                 for (int half = 0; half < 2; ++half)
@@ -372,11 +394,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         if (stacked(p, seg, it) && (pair_of(g, head_pairs, p) & 1)) continue;
         int n = 0;
         for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
-        mbar_wait(&sm.q_full, q_phase);
+        role_wait<2>(&sm.q_full, q_phase);
         q_phase ^= 1;
         // O accumulators of the previous item must have been drained by the epilogue.
-        mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
-        mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
+        role_wait<2>(&sm.o_empty[0], oe_phase ^ 1);
+        role_wait<2>(&sm.o_empty[1], oe_phase ^ 1);
         oe_phase ^= 1;
         tc_fence_after();
         // K(0)
@@ -423,6 +445,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     const uint32_t t_s = tmem + lane_bits + (h ? kColS1 : kColS0);
     const uint32_t t_o = tmem + lane_bits + (h ? kColO1 : kColO0);
     uint32_t s_phase = 0, o_phase = 0;
+    uint32_t tiles_done = 0;                 // this head's tiles so far (MUFU turn parity)
     int trt = 0;
     const float sl2 = p.scale_log2;
 
@@ -495,16 +518,16 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
               s[96 + i] = __uint_as_float(v3[i]);
             }
           }
+          if (h == 0) FCPB_FWTR(kFwSLd0, trt);
           // masking: ragged KV tail, causal diagonal (col <= row within the block)
+          // (one unrolled loop for both: the kernel's code size sits near the instruction
+          // cache's, so every unrolled 128-column loop counts)
           const int valid = ref.len - t * kBN;
-          if (diag && t == it.mblock) {
+          const int lim = (diag && t == it.mblock) ? qr + 1 : valid;
+          if (lim < kBN) {
 #pragma unroll
             for (int i = 0; i < kBN; ++i)
-              if (i > qr) s[i] = -INFINITY;
-          } else if (valid < kBN) {
-#pragma unroll
-            for (int i = 0; i < kBN; ++i)
-              if (i >= valid) s[i] = -INFINITY;
+              if (i >= lim) s[i] = -INFINITY;
           }
           float mp[8];
 #pragma unroll
@@ -516,6 +539,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           // Lazy rescale (FA4): keep exponentiating against the running reference max
           // until the row max grows by more than 2^8 in the exp2 domain, so O is
           // rescaled in TMEM only rarely.  P <= 2^8 stays exact enough in bf16/fp32.
+          if (h == 0) FCPB_FWTR(kFwMax0, trt);
           float m_use;
           if (m_run == -INFINITY) m_use = (mx == -INFINITY) ? 0.f : mx;
           else m_use = ((mx - m_run) * sl2 > 8.f) ? mx : m_run;
@@ -541,9 +565,20 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           // Unmasked tiles (finite scores, x <= 8) send kPolyPairs of every 8 pairs to the
           // FMA pipe (FA4-style).  Masked tiles keep exact zeros from MUFU ex2(-inf).  The
           // choice is CTA-uniform.
-          const bool poly = !(diag && t == it.mblock) && valid >= kBN;
+          const bool poly = kPolyPairs > 0 && !(diag && t == it.mblock) && valid >= kBN;
+          if (FCPB_FWD_ALT) {
+            // head 1's tile j after head 0's tile j; head 0's tile j after head 1's tile j-1
+            if (h == 1) mbar_wait(&sm.e_done[0], tiles_done & 1);
+            else if (tiles_done > 0) mbar_wait(&sm.e_done[1], (tiles_done - 1) & 1);
+          }
           const float sum = poly ? exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h])
                                  : exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
+          if (FCPB_FWD_ALT) {
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&sm.e_done[h]);
+          }
+          ++tiles_done;
+          if (h == 0) FCPB_FWTR(kFwExp0, trt);
           m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;
           tmem_wait_st();

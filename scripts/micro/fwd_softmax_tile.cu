@@ -1,0 +1,173 @@
+// Microbenchmark: K1's per-tile softmax of one head in isolation -- tcgen05.ld of a 128-column
+// S row, masking-free row max (FMNMX3), then fwd::exp_row (FFMA2, MUFU.EX2, bf16 pack, TMEM
+// stores of P, split-arrive) and the final wait -- one warp per SMSP (4 warps = one head) or
+// two (8 warps = both heads at once).  Variants switch parts off to find where the cycles go.
+// Reports cycles per tile per warp (the kernel's S-in-registers -> P-released time).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 fwd_softmax_tile.cu -o fwd_softmax_tile
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../paper_2605_08524_b200/csrc/attn_fwd_sm100.cuh"
+using namespace fcpb;
+
+// kind: 0 full; 1 no TMEM stores of P (exp+pack only); 2 no max (fixed reference);
+//       3 full but no tmem_wait_st at the split; 4 exps into registers only (no pack, no store)
+template <int kKind>
+__global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long long* cyc, float* out, int mma) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar[2];
+  const uint32_t w = threadIdx.x >> 5;
+  if (w == 0) tmem_alloc<512>(&tbase);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1024);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  const int nwarps = blockDim.x / 32 - 1;
+  __shared__ volatile int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (w == 0) {
+    // optional: keep the tensor pipe busy with TS MMAs (A = TMEM cols [256,320), D = [384,512))
+    if (mma && elect_one()) {
+      const uint32_t b = smem_u32(smem_raw);
+      const uint32_t id = idesc_bf16_f32(128, 128, false, true);
+      while (!stop)
+        for (int i = 0; i < 64; ++i)
+          mma_ts(tmem + 384, tmem + 256 + (i & 7) * 8, smem_desc_sw128(b + (i & 7) * 2048, 16384, 1024), id, 1);
+      mma_commit(&bar[1]);
+      mbar_wait(&bar[1], 0);   // all MMAs done before the TMEM is freed
+    }
+    __syncwarp();
+  } else {
+    const int sw = w - 1;
+    const int h = sw >> 2;
+    const uint32_t lane_bits = static_cast<uint32_t>((w & 3) * 32) << 16;
+    const uint32_t t_s = tmem + lane_bits + h * 128;
+    // finite scores in S
+    {
+      uint32_t v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(0.01f * (threadIdx.x & 31) + 0.03f * i - 0.5f);
+      for (int c = 0; c < 8; ++c) tmem_st16(t_s + c * 16, v);
+      tmem_wait_st();
+    }
+    float l = 0.f, m_run = -1.f;
+    const float sl2 = 0.18f;
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      float s[128];
+      {
+        uint32_t v0[32], v1[32], v2[32], v3[32];
+        tmem_ld32(t_s, v0);
+        tmem_ld32(t_s + 32, v1);
+        tmem_ld32(t_s + 64, v2);
+        tmem_ld32(t_s + 96, v3);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          s[i] = __uint_as_float(v0[i]);
+          s[32 + i] = __uint_as_float(v1[i]);
+          s[64 + i] = __uint_as_float(v2[i]);
+          s[96 + i] = __uint_as_float(v3[i]);
+        }
+      }
+      float mx = m_run;
+      if (kKind != 2) {
+        float mp[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mp[i] = fmax3(m_run, s[2 * i], s[2 * i + 1]);
+#pragma unroll
+        for (int i = 16; i < 128; i += 2) mp[(i >> 1) & 7] = fmax3(mp[(i >> 1) & 7], s[i], s[i + 1]);
+        mx = fmax3(fmax3(mp[0], mp[1], mp[2]), fmax3(mp[3], mp[4], mp[5]), fmaxf(mp[6], mp[7]));
+      }
+      const float neg = -mx * sl2;
+      float sum = 0.f;
+      if (kKind == 0 || kKind == 2) {
+        sum = fwd::exp_row<false>(s, sl2, neg, t_s, &bar[0]);
+      } else if (kKind == 3) {
+        float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fwd::exp_chunk<false>(s, c, sl2, neg, t_s, sp2);
+        sum = sp2[0].x + sp2[0].y + sp2[1].x + sp2[1].y;
+      } else if (kKind == 1) {
+        float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t acc = 0;
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), make_float2(sl2, sl2), make_float2(neg, neg));
+          const float2 e = make_float2(ex2(x.x), ex2(x.y));
+          sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
+          acc ^= pack_bf16(e.x, e.y);
+        }
+        sum = sp2[0].x + sp2[0].y + sp2[1].x + sp2[1].y + (acc == 0x12345 ? 1.f : 0.f);
+      } else {
+        float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int i = 0; i < 128; i += 2) {
+          const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), make_float2(sl2, sl2), make_float2(neg, neg));
+          sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], make_float2(ex2(x.x), ex2(x.y)));
+        }
+        sum = sp2[0].x + sp2[0].y + sp2[1].x + sp2[1].y;
+      }
+      tmem_wait_st();
+      l += sum;
+      m_run = -1.f - 1e-7f * it;
+      // restore finite scores over the P columns we wrote (keeps the next tile's S finite)
+      if (kKind == 0 || kKind == 2 || kKind == 3) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(0.01f * (threadIdx.x & 31) + 0.03f * i - 0.5f);
+        tmem_st16(t_s, v);
+        tmem_st16(t_s + 16, v);
+        tmem_st16(t_s + 32, v);
+        tmem_st16(t_s + 48, v);
+        tmem_wait_st();
+      }
+    }
+    const unsigned long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = l;
+    if (threadIdx.x == 32) cyc[blockIdx.x] = t1 - t0;
+    if (threadIdx.x == 32) stop = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (w == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+  (void)nwarps;
+}
+
+template <typename F>
+void run(const char* name, F k, int warps, int mma) {
+  unsigned long long* cyc;
+  float* out;
+  cudaMalloc(&cyc, 148 * 8);
+  cudaMalloc(&out, 148 * 512 * 4);
+  const int iters = 512;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  k<<<148, 32 + warps * 32, 64 * 1024>>>(iters, cyc, out, mma);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h = 0;
+  cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("%-34s softmax warps=%d mma=%d cycles/tile=%7.1f  (MUFU floor %d)  %s\n", name, warps, mma,
+         (double)h / iters, warps / 4 * 1024, cudaGetErrorString(e));
+  cudaFree(cyc);
+  cudaFree(out);
+}
+
+int main() {
+  for (int m : {0, 1})
+    for (int w : {4, 8}) {
+      run("full (ld, max, exp_row, st, split)", tile_loop<0>, w, m);
+      run("no P stores", tile_loop<1>, w, m);
+      run("exp+sum only", tile_loop<4>, w, m);
+    }
+  return 0;
+}
