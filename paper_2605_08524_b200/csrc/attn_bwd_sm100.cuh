@@ -42,7 +42,7 @@ namespace bwd {
 // Debug timeline of CTA 0: [event][tile] clock64 stamps (see scripts/trace_bwd.py).
 constexpr int kTraceTiles = 256;
 enum TraceEv { kTrQIssue, kTrQGot, kTrSIssue, kTrPGot, kTrDvIssue, kTrDsGot, kTrDkIssue,
-               kTrSGot, kTrPArrive, kTrDpGot, kTrDsArrive, kTrSLd, kTrPSt, kTrEvents };
+               kTrSGot, kTrPArrive, kTrDpGot, kTrDsArrive, kTrSLd, kTrPSt, kTrDpLd, kTrDsSt, kTrEvents };
 __device__ unsigned long long g_trace[kTrEvents * kTraceTiles];
 #define FCPB_TR(ev, j) do { if (blockIdx.x == 0 && (j) < kTraceTiles && (threadIdx.x & 31) == 0 && \
     ((ev) < kTrSGot ? true : threadIdx.x == 128)) \
@@ -194,6 +194,10 @@ FCPB_DEV float4 lds128(uint32_t addr) {
 #define FCPB_BWD_PSPLIT 1
 #endif
 constexpr bool kPSplit = FCPB_BWD_PSPLIT != 0;
+#ifndef FCPB_BWD_DS_LATE
+#define FCPB_BWD_DS_LATE 1
+#endif
+constexpr bool kDsLate = FCPB_BWD_DS_LATE != 0;
 
 template <bool kMask>
 FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t (&pk)[16], uint32_t t_p,
@@ -241,11 +245,10 @@ FCPB_DEV void p_chunk(const uint32_t (&s)[32], uint32_t l2, float sl2, uint32_t 
   else tmem_st16(t_p, pk);
 }
 
-// Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds, and (when gdst is
-// set) the same 64 bytes into the materialised dS^T tile for the dQ GEMM.
+// Phase 2, 32 q columns:  dS = P (dP + ndelta[q])  -> bf16 pairs at t_ds and in dk (the caller
+// streams them into the materialised dS^T tile for the dQ GEMM after releasing ds_full).
 FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const uint32_t (&pk)[16], uint32_t t_ds,
-                       uint4* gdst) {
-  uint32_t dk[16];
+                       uint32_t (&dk)[16]) {
 #pragma unroll
   for (int c8 = 0; c8 < 4; ++c8) {
     const float4 da = lds128(dl + c8 * 32), db = lds128(dl + c8 * 32 + 16);
@@ -262,11 +265,15 @@ FCPB_DEV void ds_chunk(const uint32_t (&dp)[32], uint32_t dl, const uint32_t (&p
     }
   }
   tmem_st16(t_ds, dk);
-  if (gdst) {     // tile layout [q/8][kv][8 q]: chunk i of this thread at gdst[i * 128]
+}
+// The 64 bytes of this thread's dS^T row into the tile, layout [q/8][kv][8 q]: chunk i at
+// gdst[i * 128].  Streaming stores (keep L2 for the Q/dO stream), issued after ds_full is
+// released: 32 KB per tile is ~1,100 cycles of one SM's share of HBM write bandwidth, and a
+// full store queue stalling the warp before its arrival put it on the dK chain.
+FCPB_DEV void ds_store(uint4* gdst, const uint32_t (&dk)[16]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)      // streaming: keep L2 for the Q/dO stream
-      st_global_cs(gdst + i * kBK, make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]));
-  }
+  for (int i = 0; i < 4; ++i)
+    st_global_cs(gdst + i * kBK, make_uint4(dk[4 * i], dk[4 * i + 1], dk[4 * i + 2], dk[4 * i + 3]));
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -608,15 +615,26 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,      // bf16 [Tq,Hq,D]
             mbar_wait(&sm.do_full[dr_.slot], dr_.phase);  // delta of this tile landed
             FCPB_TR(kTrDpGot, (int)tile);
             tc_fence_after();
+            uint32_t dsk[16];
             {
               uint32_t dv[32];
               tmem_ld32(t_dp, dv);
               tmem_wait_ld();
-              ds_chunk(dv, dl, pr, t_dp, gdst);
+              FCPB_TR(kTrDpLd, (int)tile);
+              ds_chunk(dv, dl, pr, t_dp, dsk);
+              FCPB_TR(kTrDsSt, (int)tile);
             }
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&sm.ds_full);
+            if (kDsLate) {
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&sm.ds_full);
+              if (gdst) ds_store(gdst, dsk);
+            } else {
+              if (gdst) ds_store(gdst, dsk);
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&sm.ds_full);
+            }
             FCPB_TR(kTrDsArrive, (int)tile);
             qr_.next();
             dr_.next();

@@ -14,7 +14,7 @@ for _ in range(3):
     ex.step(q, k, v, do)
 torch.cuda.synchronize()
 lib = native.load()
-EV = ["QIssue", "QGot", "SIssue", "PGot", "DvIssue", "DsGot", "DkIssue", "SGot", "PArrive", "DpGot", "DsArrive", "SLd", "PSt"]
+EV = ["QIssue", "QGot", "SIssue", "PGot", "DvIssue", "DsGot", "DkIssue", "SGot", "PArrive", "DpGot", "DsArrive", "SLd", "PSt", "DpLd", "DsSt"]
 T = 256
 buf = (ctypes.c_ulonglong * (len(EV) * T))()
 lib.fcpb_debug_bwd_trace(buf, len(EV) * T)
@@ -26,7 +26,7 @@ for j in range(0, int(os.environ.get("NPRINT", "120"))):
     print(f"{j:4d} " + " ".join(f"{a[e, j]:9d}" for e in range(len(EV))))
 d = np.diff(a[EV.index("DkIssue"), 20:120])
 print("median DkIssue period (cycles):", np.median(d))
-for x, y in [("SGot", "PArrive"), ("DpGot", "DsArrive"), ("SIssue", "SGot"), ("SGot", "SLd"), ("SLd", "PSt"), ("PSt", "PArrive")]:
+for x, y in [("SGot", "PArrive"), ("DpGot", "DsArrive"), ("SIssue", "SGot"), ("SGot", "SLd"), ("SLd", "PSt"), ("PSt", "PArrive"), ("PArrive", "DpGot"), ("DpGot", "DpLd"), ("DpLd", "DsSt"), ("DsSt", "DsArrive"), ("DsArrive", "SGot"), ("PGot", "DvIssue"), ("DsGot", "DkIssue"), ("PArrive", "PGot"), ("DsArrive", "DsGot")]:
     print(f"median {x}->{y}:", np.median(a[EV.index(y), 20:120] - a[EV.index(x), 20:120]))
 import time
 s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -61,3 +61,6 @@ for j in range(0, int(os.environ.get("NPRINT3", "20"))):
     print(f"{j:4d} " + " ".join(f"{c3[e, j]:8d}" for e in range(len(EV3))))
 d3 = np.diff(c3[EV3.index("Pv1Issue"), 5:60])
 print("fwd median period (cycles):", np.median(d3))
+print("median DsArrive(j)->SGot(j+1):", np.median(a[EV.index("SGot"), 21:121] - a[EV.index("DsArrive"), 20:120]))
+print("median DkIssue(j)->DpGot(j+1):", np.median(a[EV.index("DpGot"), 21:121] - a[EV.index("DkIssue"), 20:120]))
+print("median DvIssue(j)->SGot(j+1):", np.median(a[EV.index("SGot"), 21:121] - a[EV.index("DvIssue"), 20:120]))
