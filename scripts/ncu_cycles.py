@@ -5,6 +5,8 @@ from collections import defaultdict
 
 for f in sys.argv[1:]:
     rows = [r for r in csv.reader(open(f)) if len(r) > 10]
+    while rows and "Kernel Name" not in rows[0]:
+        rows = rows[1:]
     if not rows:
         print(f, "no rows")
         continue
