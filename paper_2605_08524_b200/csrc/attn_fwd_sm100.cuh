@@ -61,7 +61,6 @@ struct Smem {
   uint64_t q_full, q_empty;
   uint64_t kv_full[kSlots], kv_empty[kSlots];
   uint64_t s_full[2], p_part[2], p_full[2], o_full[2], o_empty[2];
-  uint64_t e_done[2];                 // head h finished the exponentials of a tile (FCPB_FWD_ALT)
   SchedRing sched;
   uint32_t tmem_base;
 };
@@ -86,37 +85,6 @@ struct Params {
 };
 
 constexpr int kStackRows = 64;   // a stacked tile: 64 rows of each of two q-heads
-
-// MUFU turns (FCPB_FWD_ALT): the two heads' exp phases strictly alternate -- head 0 tile j,
-// head 1 tile j, head 0 tile j+1, ... -- each waiting for the other's e_done before its first
-// exponential (its S load, masking and row max overlap the other head's exponentials).  Left
-// to themselves the heads settle with their exp phases half overlapped, sharing the SMSP's
-// MUFU, which stretches every softmax (S in registers -> P released ~2,000 cycles, tile-pair
-// period ~3,300: r02 trace) and, through the chain S -> softmax -> PV -> S, the period.
-#ifndef FCPB_FWD_ALT
-#define FCPB_FWD_ALT 0    // measured: 5.59M -> 5.88M cycles with the turns (r02), so off
-#endif
-
-// mbarrier waits on the tile chain: bit 1 = the MMA warp's P waits, bit 2 = the softmax
-// warps' S waits, bit 4 = the MMA warp's K/V waits spin (test_wait) instead of suspending.
-#ifndef FCPB_FWD_SPIN
-#define FCPB_FWD_SPIN 0
-#endif
-// Sleeping (hinted) waits per role: bit 1 = TMA producer, bit 2 = MMA warp.
-#ifndef FCPB_FWD_SLEEP
-#define FCPB_FWD_SLEEP 0
-#endif
-template <int kBit>
-FCPB_DEV void chain_wait(uint64_t* bar, uint32_t parity) {
-  if (FCPB_FWD_SPIN & kBit) mbar_wait_spin(bar, parity);
-  else if ((kBit & 5) && (FCPB_FWD_SLEEP & 2)) mbar_wait_sleep(bar, parity);
-  else mbar_wait(bar, parity);
-}
-template <int kRole>
-FCPB_DEV void role_wait(uint64_t* bar, uint32_t parity) {
-  if (FCPB_FWD_SLEEP & kRole) mbar_wait_sleep(bar, parity);
-  else mbar_wait(bar, parity);
-}
 
 // Does item `it` (128-row block of `seg`) run stacked?  The odd head pair of a stacked item
 // is empty (its four heads ran under the even pair).
@@ -258,7 +226,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_init(&sm.p_full[h], 128);
       mbar_init(&sm.o_full[h], 1);
       mbar_init(&sm.o_empty[h], 128);
-      mbar_init(&sm.e_done[h], 4);
     }
     sched_init(sm.sched, 1 + 8);
     fence_barrier_init();
@@ -287,7 +254,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           const int h0 = 2 * hp;
           const int kvh = h0 / group;
           const int row0 = seg.q_off + it.mblock * kBM;
-          role_wait<1>(&sm.q_empty, q_phase ^ 1);
+          mbar_wait(&sm.q_empty, q_phase ^ 1);
           q_phase ^= 1;
           mbar_arrive_expect_tx(&sm.q_full, 2 * kTileBytes);
           if (stk) {
@@ -312,7 +279,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
             for (int t = 0; t < nt; ++t) {
               const int krow = ref.off + t * kBN;
               for (int kv = 0; kv < 2; ++kv) {
-                role_wait<1>(&sm.kv_empty[slot], slot_phase ^ 1);
+                mbar_wait(&sm.kv_empty[slot], slot_phase ^ 1);
                 mbar_arrive_expect_tx(&sm.kv_full[slot], kTileBytes);
                 const CUtensorMap* m = kv ? mv : mk;
                 for (int half = 0; half < 2; ++half)
@@ -366,11 +333,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       // wait for P_h(j) (in two parts when split) and issue O_h += P_h V_j
       auto pv = [&](int h, uint32_t vslot, bool acc) {
         if (kPSplit > 0) {
-          chain_wait<1>(&sm.p_part[h], p_phase);
+          mbar_wait(&sm.p_part[h], p_phase);
           tc_fence_after();
           issue_pv(h, vslot, acc, 0, kKkSplit);
         }
-        chain_wait<1>(&sm.p_full[h], p_phase);
+        mbar_wait(&sm.p_full[h], p_phase);
         if (h == 0) FCPB_FWTR(kFwP0Got, trt); else FCPB_FWTR(kFwP1Got, trt);
         tc_fence_after();
         issue_pv(h, vslot, acc, kPSplit > 0 ? kKkSplit : 0, kBN / 16);
@@ -382,7 +349,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
       // Take the next ring position and wait until TMA has filled it.
       auto take_full = [&]() {
         const uint32_t cur = slot;
-        chain_wait<4>(&sm.kv_full[cur], slot_phase);
+        mbar_wait(&sm.kv_full[cur], slot_phase);
         if (++slot == kSlots) { slot = 0; slot_phase ^= 1; }
         return cur;
       };
@@ -394,11 +361,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         if (stacked(p, seg, it) && (pair_of(g, head_pairs, p) & 1)) continue;
         int n = 0;
         for (int r = seg.kv_begin; r < seg.kv_end; ++r) n += kv_tiles(p.kvrefs[r], it.mblock);
-        role_wait<2>(&sm.q_full, q_phase);
+        mbar_wait(&sm.q_full, q_phase);
         q_phase ^= 1;
         // O accumulators of the previous item must have been drained by the epilogue.
-        role_wait<2>(&sm.o_empty[0], oe_phase ^ 1);
-        role_wait<2>(&sm.o_empty[1], oe_phase ^ 1);
+        mbar_wait(&sm.o_empty[0], oe_phase ^ 1);
+        mbar_wait(&sm.o_empty[1], oe_phase ^ 1);
         oe_phase ^= 1;
         tc_fence_after();
         // K(0)
@@ -445,7 +412,6 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
     const uint32_t t_s = tmem + lane_bits + (h ? kColS1 : kColS0);
     const uint32_t t_o = tmem + lane_bits + (h ? kColO1 : kColO0);
     uint32_t s_phase = 0, o_phase = 0;
-    uint32_t tiles_done = 0;                 // this head's tiles so far (MUFU turn parity)
     int trt = 0;
     const float sl2 = p.scale_log2;
 
@@ -496,7 +462,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
         const int nt = kv_tiles(ref, it.mblock);
         const bool diag = ref.flags & FCPB_KV_DIAG;
         for (int t = 0; t < nt; ++t) {
-          chain_wait<2>(&sm.s_full[h], s_phase);
+          mbar_wait(&sm.s_full[h], s_phase);
           s_phase ^= 1;
           if (h == 0) FCPB_FWTR(kFwS0Got, trt); else FCPB_FWTR(kFwS1Got, trt);
           tc_fence_after();
@@ -566,18 +532,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           // FMA pipe (FA4-style).  Masked tiles keep exact zeros from MUFU ex2(-inf).  The
           // choice is CTA-uniform.
           const bool poly = kPolyPairs > 0 && !(diag && t == it.mblock) && valid >= kBN;
-          if (FCPB_FWD_ALT) {
-            // head 1's tile j after head 0's tile j; head 0's tile j after head 1's tile j-1
-            if (h == 1) mbar_wait(&sm.e_done[0], tiles_done & 1);
-            else if (tiles_done > 0) mbar_wait(&sm.e_done[1], (tiles_done - 1) & 1);
-          }
           const float sum = poly ? exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h])
                                  : exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
-          if (FCPB_FWD_ALT) {
-            __syncwarp();
-            if (lane_id() == 0) mbar_arrive(&sm.e_done[h]);
-          }
-          ++tiles_done;
           if (h == 0) FCPB_FWTR(kFwExp0, trt);
           m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;

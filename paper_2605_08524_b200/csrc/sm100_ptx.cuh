@@ -96,19 +96,6 @@ FCPB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// try_wait with a suspend-time hint (PHASECHK + NANOSLEEP.SYNCS): for warps off the chain
-// whose polling would only steal issue slots from the SMSP's math warps.
-FCPB_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
-      : "memory");
-  return ok != 0;
-}
 FCPB_DEV uint64_t global_timer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -151,15 +138,6 @@ FCPB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
       __trap();
     }
-  }
-}
-
-FCPB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait_sleep(bar, parity)) return;
-  const uint64_t t0 = global_timer_ns();
-  uint32_t spins = 0;
-  while (!mbar_try_wait_sleep(bar, parity)) {
-    if ((++spins & 1023u) == 0 && global_timer_ns() - t0 > FCPB_WATCHDOG_NS) __trap();
   }
 }
 
