@@ -1,5 +1,5 @@
 # One bench line per (config, N) for simulator validation -> gpurun_out/configs.jsonl
-out=gpurun_out/configs.jsonl; : > $out
+out=${OUT:-gpurun_out/configs.jsonl}; : > $out
 run() {  # config n steps [block]
   if [ "$2" = 1 ]; then cmd="python bench.py"; else cmd="python -m torch.distributed.run --nnodes=1 --nproc-per-node $2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $2"; fi
   extra=""; [ -n "$4" ] && extra="--block $4"
