@@ -131,14 +131,16 @@ def run_plan_on_gpu(result, model, q, k, v, do, device="cuda", backward=True, fu
     return out
 
 
-def oracle(result, model, q, k, v, do, seq_ids=None, dtype=torch.float64):
-    """fp64 oracle on (a subset of) sequences; returns dict + the row index used."""
+def oracle(result, model, q, k, v, do, seq_ids=None, dtype=torch.float64, device=None):
+    """fp64 oracle on (a subset of) sequences; returns dict + the row index used.  device:
+    where the checker's fp64 arithmetic runs (default: the GPU when there is one)."""
     rows = global_sequence_rows(result)
     if seq_ids is not None:
         rows = {s: rows[s] for s in seq_ids}
     scale = 1.0 / math.sqrt(model.head_dim)
     # fp64 on the GPU when there is one (the checker's arithmetic is the same; minutes -> seconds)
-    odev = torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu")
+    odev = torch.device(device) if device is not None else (
+        torch.device("cuda") if torch.cuda.is_available() else torch.device("cpu"))
     qf, kf, vf, dof = (x.to(odev, dtype) for x in (q, k, v, do))
     causal = result.deps.mask == "causal"
     o, lse = mono_fwd(qf, kf, vf, rows, scale, causal, dtype)
