@@ -110,76 +110,59 @@ FCPB_DEV int kv_tiles(const FcpbKvRef& ref, int mb) {
   return n;
 }
 
-// One row of a 128-column S tile: P = exp2(s*sl2 + neg) as bf16 pairs into TMEM at t_s
-// (16 columns per 32 scores), returns the row sum.  kPoly: pairs 8u+8-kPolyPairs..8u+7 use
-// ex2_poly2 (finite inputs only).
 #ifndef FCPB_FWD_POLY_PAIRS
-#define FCPB_FWD_POLY_PAIRS 1    // ncu C2 (r02): 1 pair of 8 -2.0% cycles, 2 pairs -1.1%
+#define FCPB_FWD_POLY_PAIRS 2    // exp2 pairs of every 8 on the FMA pipe (ncu C2 r02: 2 best)
 #endif
 constexpr int kPolyPairs = FCPB_FWD_POLY_PAIRS;
-// Row sum off the P chain (FA4-style): the exponentials overwrite the scores in registers
-// and are summed after P is released to the MMA warp (FCPB_FWD_LATESUM=0: summed inline).
-#ifndef FCPB_FWD_LATESUM
-#define FCPB_FWD_LATESUM 0    // 1: +8% K1 cycles on C2 (ncu A/B r02), so off
-#endif
-constexpr bool kLateSum = FCPB_FWD_LATESUM != 0;
-
-template <bool kPoly>
-FCPB_DEV void exp_chunk(float (&s)[kBN], int c, float sl2, float neg, uint32_t t_s, float2 (&sp2)[2]) {
-  uint32_t pk[16];
-#pragma unroll
-  for (int i = 0; i < 32; i += 2) {
-    const float2 x = __ffma2_rn(make_float2(s[c * 32 + i], s[c * 32 + i + 1]),
-                                make_float2(sl2, sl2), make_float2(neg, neg));
-    float2 e;
-    if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
-    else e = make_float2(ex2(x.x), ex2(x.y));
-    if (kLateSum) {
-      s[c * 32 + i] = e.x;
-      s[c * 32 + i + 1] = e.y;
-    } else {
-      sp2[(i >> 1) & 1] = __fadd2_rn(sp2[(i >> 1) & 1], e);
-    }
-    pk[i / 2] = pack_bf16(e.x, e.y);
-  }
-  tmem_st16(t_s + c * 16, pk);
-}
-
-// Sum of the 128 exponentials left in s by exp_chunk (kLateSum), 4 independent chains.
-FCPB_DEV float row_sum(const float (&s)[kBN]) {
-  float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-  for (int i = 0; i < kBN; i += 2) a[(i >> 1) & 3] = __fadd2_rn(a[(i >> 1) & 3], make_float2(s[i], s[i + 1]));
-  const float2 b = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
-  return b.x + b.y;
-}
 
 // Split P arrival (FA4-style): after the first kPSplit of the four 32-column chunks of P are
 // in TMEM the softmax warps arrive on p_part, and the MMA warp issues those K steps of
-// O += P V while the last chunk is still being exponentiated; p_full releases the rest.
-// The O rescale (rare) therefore happens before the exponentials.
+// O += P V while the rest are packed and stored; p_full releases the rest.  The O rescale
+// (rare) therefore happens before the exponentials.
 #ifndef FCPB_FWD_PSPLIT
-#define FCPB_FWD_PSPLIT 2    // ncu A/B on C2 (r02): 2 chunks -1.8% cycles, 3 chunks +0.8%, off 0
+#define FCPB_FWD_PSPLIT 2    // ncu A/B on C2 (r02): 2 chunks best (0/1/3: +5% / +4% / +5%)
 #endif
 constexpr int kPSplit = FCPB_FWD_PSPLIT;
 static_assert(kPSplit >= 0 && kPSplit < 4, "P split point in 32-column chunks");
 
-// One row of a 128-column S tile: P = exp2(s*sl2 + neg) as bf16 pairs into TMEM at t_s
-// (16 columns per 32 scores); arrives on p_part after kPSplit chunks; returns the row sum.
-// kPoly: pairs 8u+8-kPolyPairs..8u+7 use ex2_poly2 (finite inputs only).
+// One row of a 128-column S tile, FA4 order: every exponential first, in place in s --
+// P = exp2(s*sl2 + neg), pairs 8u+8-kPolyPairs..8u+7 by ex2_poly2 when kPoly (finite inputs
+// only) -- then the bf16 pack and TMEM store per 32-column chunk (16 columns at t_s + 16c,
+// over S columns already read), arriving on p_part after kPSplit chunks.  The caller sums the
+// exponentials left in s after releasing P (row_sum).  ncu C2 (r02): 5.32M -> 5.23M cycles
+// with 2 polynomial pairs, against inline sums and per-chunk stores with 1 pair.
 template <bool kPoly>
-FCPB_DEV float exp_row(float (&s)[kBN], float sl2, float neg, uint32_t t_s, uint64_t* p_part) {
-  float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+FCPB_DEV void exp_row(float (&s)[kBN], float sl2, float neg, uint32_t t_s, uint64_t* p_part) {
+#pragma unroll
+  for (int i = 0; i < kBN; i += 2) {
+    const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), make_float2(sl2, sl2), make_float2(neg, neg));
+    float2 e;
+    if (kPoly && ((i >> 1) & 7) >= 8 - kPolyPairs) e = ex2_poly2(x);
+    else e = make_float2(ex2(x.x), ex2(x.y));
+    s[i] = e.x;
+    s[i + 1] = e.y;
+  }
 #pragma unroll
   for (int c = 0; c < kBN / 32; ++c) {
-    exp_chunk<kPoly>(s, c, sl2, neg, t_s, sp2);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]);
+    tmem_st16(t_s + c * 16, pk);
     if (kPSplit > 0 && c + 1 == kPSplit) {
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_part);
     }
   }
-  return (sp2[0].x + sp2[0].y) + (sp2[1].x + sp2[1].y);
+}
+
+// Sum of the 128 exponentials exp_row leaves in s, 4 independent chains.
+FCPB_DEV float row_sum(const float (&s)[kBN]) {
+  float2 a[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+  for (int i = 0; i < kBN; i += 2) a[(i >> 1) & 3] = __fadd2_rn(a[(i >> 1) & 3], make_float2(s[i], s[i + 1]));
+  const float2 b = __fadd2_rn(__fadd2_rn(a[0], a[1]), __fadd2_rn(a[2], a[3]));
+  return b.x + b.y;
 }
 
 // setmaxnreg split: one producer/MMA warpgroup, two softmax warpgroups.  setmaxnreg.inc can
@@ -532,8 +515,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           // FMA pipe (FA4-style).  Masked tiles keep exact zeros from MUFU ex2(-inf).  The
           // choice is CTA-uniform.
           const bool poly = kPolyPairs > 0 && !(diag && t == it.mblock) && valid >= kBN;
-          const float sum = poly ? exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h])
-                                 : exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
+          if (poly) exp_row<true>(s, sl2, neg, t_s, &sm.p_part[h]);
+          else exp_row<false>(s, sl2, neg, t_s, &sm.p_part[h]);
           if (h == 0) FCPB_FWTR(kFwExp0, trt);
           m_run = (m_run == -INFINITY && mx == -INFINITY) ? -INFINITY : m_use;
           first = false;
@@ -541,7 +524,7 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
           tc_fence_before();
           mbar_arrive(&sm.p_full[h]);
           if (h == 0) FCPB_FWTR(kFwP0Arrive, trt); else FCPB_FWTR(kFwP1Arrive, trt);
-          l_run = l_run * alpha + (kLateSum ? row_sum(s) : sum);
+          l_run = l_run * alpha + row_sum(s);
           ++trt;
         }
       }

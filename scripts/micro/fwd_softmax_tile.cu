@@ -11,7 +11,7 @@
 using namespace fcpb;
 
 // kind: 0 full; 1 no TMEM stores of P (exp+pack only); 2 no max (fixed reference);
-//       3 full but no tmem_wait_st at the split; 4 exps into registers only (no pack, no store)
+//       4 exps into registers only (no pack, no store)
 template <int kKind>
 __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long long* cyc, float* out, int mma) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -89,12 +89,8 @@ __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long lon
       const float neg = -mx * sl2;
       float sum = 0.f;
       if (kKind == 0 || kKind == 2) {
-        sum = fwd::exp_row<false>(s, sl2, neg, t_s, &bar[0]);
-      } else if (kKind == 3) {
-        float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) fwd::exp_chunk<false>(s, c, sl2, neg, t_s, sp2);
-        sum = sp2[0].x + sp2[0].y + sp2[1].x + sp2[1].y;
+        fwd::exp_row<false>(s, sl2, neg, t_s, &bar[0]);
+        sum = fwd::row_sum(s);
       } else if (kKind == 1) {
         float2 sp2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         uint32_t acc = 0;
@@ -119,7 +115,7 @@ __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long lon
       l += sum;
       m_run = -1.f - 1e-7f * it;
       // restore finite scores over the P columns we wrote (keeps the next tile's S finite)
-      if (kKind == 0 || kKind == 2 || kKind == 3) {
+      if (kKind == 0 || kKind == 2) {
         uint32_t v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(0.01f * (threadIdx.x & 31) + 0.03f * i - 0.5f);
