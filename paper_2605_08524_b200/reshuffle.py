@@ -29,6 +29,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import native
 from .costmodel import ModelConfig
 from .distributor import chunk_placement
 from .errors import ConsistencyError, ParameterError
@@ -184,10 +185,18 @@ class Reshuffler:
                     for t in tensors]
         flat_in = [t.contiguous().reshape(rows_in, e) for t, e in zip(tensors, elems)]
         flat_out = [o.view(rows_out, e) for o, e in zip(outs, elems)]
-        for src, dst in zip(flat_in, flat_out):           # rows that stay here: direct copies
-            for peer, s0, d, n in pulls:
-                if peer == self.rank:
-                    dst[d:d + n].copy_(src[s0:s0 + n], non_blocking=True)
+        self._mark("begin")
+        # rows that stay here: direct copies, all of them in one gather-kernel launch (one
+        # torch copy per (tensor, run) left the GPU waiting on the host's launches: 0.64 ms
+        # for C2's 45 local runs at N=2, scripts/reshuffle_probe.py)
+        local = [(dst.data_ptr() + d * w, src.data_ptr() + s0 * w, n * w)
+                 for src, dst, w in zip(flat_in, flat_out, widths) for peer, s0, d, n in pulls
+                 if peer == self.rank]
+        if not self._gather(local, torch.cuda.current_stream(self.device)):
+            for src, dst in zip(flat_in, flat_out):
+                for peer, s0, d, n in pulls:
+                    if peer == self.rank:
+                        dst[d:d + n].copy_(src[s0:s0 + n], non_blocking=True)
         # one contiguous region per tensor (capacity t_max rows each): publish and pulls are
         # plain contiguous copies and the pulls land directly in the outputs (no unpack)
         region, acc = [], 0
@@ -196,6 +205,7 @@ class Reshuffler:
             acc += self.t_max * w
         cur = torch.cuda.current_stream(self.device)
         st = remote_stream or cur
+        self._mark("local_copies", cur)
         if remote_stream is not None:
             remote_stream.wait_stream(cur)
         with torch.cuda.stream(st):
@@ -204,16 +214,26 @@ class Reshuffler:
                 if src.data_ptr() == dst.data_ptr():    # written in place (input_views)
                     continue
                 dst.view(rows_in, w).copy_(src.view(torch.uint8), non_blocking=True)
+            self._mark("published", st)
             self.flags.barrier(0, st)              # every rank's rows published
-            for dst, w, off in zip(flat_out, widths, region):
-                ob = dst.view(torch.uint8)
-                for peer, s0, d, n in pulls:
-                    if peer == self.rank:
-                        continue
-                    ob[d:d + n].copy_(self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w),
-                                      non_blocking=True)
-                    self.bytes_moved += n * w
+            self._mark("barrier0", st)
+            remote = [(dst.data_ptr() + d * w, self.peer[peer].data_ptr() + off + s0 * w, n * w)
+                      for dst, w, off in zip(flat_out, widths, region) for peer, s0, d, n in pulls
+                      if peer != self.rank]
+            self.bytes_moved += sum(x[2] for x in remote)
+            # Standalone, the pulls are SM loads over NVLink (the K5 pull kernel, one launch);
+            # beside compute (remote_stream) they stay on the copy engines, which need no SM.
+            if remote_stream is not None or not self._gather(remote, st):
+                for dst, w, off in zip(flat_out, widths, region):
+                    ob = dst.view(torch.uint8)
+                    for peer, s0, d, n in pulls:
+                        if peer == self.rank:
+                            continue
+                        ob[d:d + n].copy_(self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w),
+                                          non_blocking=True)
+            self._mark("pulls", st)
             self.flags.barrier(1, st)              # every pull done: buffers reusable
+            self._mark("barrier1", st)
         if remote_stream is None:
             return outs
         ev = torch.cuda.Event()
@@ -221,6 +241,43 @@ class Reshuffler:
         for t in list(tensors) + list(outs):
             t.record_stream(remote_stream)
         return outs, ev
+
+    # Optional per-phase CUDA-event timeline of _move (scripts/reshuffle_probe.py).
+    marks = None
+
+    def _gather(self, ranges, stream) -> bool:
+        """Copy (dst, src, bytes) ranges with one ``fcpb_gather_copy`` launch on `stream`; False
+        (nothing launched) when a range is not 16-byte aligned.  Device tables are cached per
+        range list (the same pointers recur from step to step)."""
+        if not ranges:
+            return True
+        if any((d | s_ | n) & 15 for d, s_, n in ranges):
+            return False
+        key = tuple(ranges)
+        cache = self.__dict__.setdefault("_tabs", {})
+        tab = cache.get(key)
+        if tab is None:
+            import numpy as np
+            step = native.gather_seg_bytes()
+            r = np.asarray(ranges, dtype=np.int64)
+            cnt = (r[:, 2] + step - 1) // step                 # pieces of <= step bytes per range
+            idx = np.repeat(np.arange(len(r)), cnt)
+            o = (np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)) * step
+            segs = np.stack([r[idx, 0] + o, r[idx, 1] + o, np.minimum(step, r[idx, 2] - o)], axis=1)
+            host = torch.from_numpy(np.ascontiguousarray(segs)).pin_memory()
+            tab = (host, host.to(self.device, non_blocking=True))
+            if len(cache) >= 64:
+                cache.clear()
+            cache[key] = tab
+        native.gather_copy(tab[1], 2 * torch.cuda.get_device_properties(self.device).multi_processor_count,
+                           stream)
+        return True
+
+    def _mark(self, name, stream=None):
+        if self.marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream or torch.cuda.current_stream(self.device))
+            self.marks.append((name, ev))
 
     def input_views(self, specs, rows: int | None = None):
         """Tensors of shapes [rows, *shape] / dtypes ``specs`` that live in this rank's
