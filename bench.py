@@ -595,7 +595,7 @@ def main():
                     qf, kf, vf = rs.to_fcp(*usr_qkv)
                     ex_u.forward(qf, kf, vf)
                 else:
-                    ex_u.forward_user(rs, *usr_qkv)
+                    ex_u.forward_user(rs, *usr_qkv, overlap=True)
                 b.record(stream)
                 torch.cuda.synchronize()
                 if it:

@@ -501,18 +501,29 @@ class FcpExecutor:
             self.xchg.close()
             self.xchg = None
 
-    def forward_user(self, rs, q_u, k_u, v_u):
-        """Forward from the user's layout: the reshuffler
-        copies the rows that stay on this rank, its remote pulls into the FCP layout run on a
-        side stream, and the PRE_WAVE tiles (rows in place, build the executor with
-        ``resident=rs.resident_chunks()``) compute meanwhile.  K/V land directly in
-        ``kv_input_buffers`` (no publish copy at N > 1).  Returns the FCP-layout (q, k, v)
-        and (o, lse)."""
-        if self._rs_stream is None:
-            self._rs_stream = torch.cuda.Stream(device=self.device)
+    def forward_user(self, rs, q_u, k_u, v_u, overlap: bool | None = None):
+        """Forward from the user's layout.  K/V land directly
+        in ``kv_input_buffers`` (no publish copy at N > 1).  Returns the FCP-layout (q, k, v)
+        and (o, lse).
+
+        overlap=True: the reshuffler copies the rows that stay on this rank, its remote pulls
+        run on copy engines on a side stream, and the PRE_WAVE tiles (rows in place; build the
+        executor with ``resident=rs.resident_chunks()``) compute meanwhile.  overlap=False
+        (default; FCPB_RESHUFFLE_OVERLAP=1 flips it): the whole to-FCP move first (the remote
+        pulls as the K5 pull kernel at NVLink speed), then the forward -- measured faster on
+        C2 at N=2 (2.63-2.73 vs 2.90-2.94 ms), because the exposed move is ~0.3 ms and the
+        split forward's extra launch tail costs more (profiles/r02_notes.md)."""
+        if overlap is None:
+            overlap = os.environ.get("FCPB_RESHUFFLE_OVERLAP", "0") == "1"
         H, D = self.user_cfg.q_heads, self.user_cfg.head_dim
         q = torch.empty((self.layout.tokens, H, D), dtype=q_u.dtype, device=self.device)
         k, v = self.kv_input_buffers()
+        if not overlap:
+            q, k, v = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens, rs.plan.fcp_tokens,
+                               outs=[q, k, v])
+            return (q, k, v), self.forward(q, k, v)
+        if self._rs_stream is None:
+            self._rs_stream = torch.cuda.Stream(device=self.device)
         (q, k, v), ev = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens,
                                  rs.plan.fcp_tokens, outs=[q, k, v], remote_stream=self._rs_stream)
         o, lse = self.forward(q, k, v, pre_event=ev)

@@ -98,12 +98,15 @@ def main():
     # of the rows that stay here (an executor built with the reshuffler's resident chunks)
     ex_u = FcpExecutor(r, rank, model, dev, resident=rs.resident_chunks())
     usr3 = [x.clone() for x in usr[:3]]
-    (qf, kf, vf), (o_u, lse_u) = ex_u.forward_user(rs, *usr3)
-    torch.cuda.synchronize()
-    user_fwd_ok = torch.equal(qf, loc[0]) and torch.equal(kf, loc[1]) and torch.equal(vf, loc[2])
-    rep_u = {"o": err(o_u.cpu(), gather_rank(ro, lay, goff, r.deps)),
-             "lse": err(lse_u.cpu(), gather_rank(rl, lay, goff, r.deps))}
-    user_fwd_ok = user_fwd_ok and within_fixed_caps(rep_u)
+    user_fwd_ok = True
+    for overlap in (True, False):       # PRE_WAVE beside copy-engine pulls / move, then forward
+        (qf, kf, vf), (o_u, lse_u) = ex_u.forward_user(rs, *usr3, overlap=overlap)
+        torch.cuda.synchronize()
+        user_fwd_ok = user_fwd_ok and torch.equal(qf, loc[0]) and torch.equal(kf, loc[1]) \
+            and torch.equal(vf, loc[2])
+        rep_u = {"o": err(o_u.cpu(), gather_rank(ro, lay, goff, r.deps)),
+                 "lse": err(lse_u.cpu(), gather_rank(rl, lay, goff, r.deps))}
+        user_fwd_ok = user_fwd_ok and within_fixed_caps(rep_u)
     ok = ok and user_fwd_ok
     # measured SimReport-shaped record (collective): one WorkerStats per rank, one record per stage
     mr = ex.measured_report(*loc, reps=2)
