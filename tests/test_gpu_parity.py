@@ -72,6 +72,14 @@ def test_full_mask():
     _full_check([700, 300, 64], 2, 256, GQA_SMALL, mask="full", name="full mask N=2")
 
 
+def test_many_q_heads_405b_shape():
+    """Llama-3.1-405B-shaped heads (128 q / 8 kv, GQA group 16): more q-heads than one block of
+    the backward preprocess covers (64 per gridDim.y slice), 2 simulated ranks."""
+    from paper_2605_08524_b200.costmodel import ModelConfig
+    _full_check([900, 300, 129], 2, 512, ModelConfig(q_heads=128, kv_heads=8, head_dim=128),
+                name="128/8 heads N=2")
+
+
 def test_c2_llama8b_n1_every_sequence():
     """C2 (Llama-3-8B GQA 32/8, 62,956-token packed batch, block 2K) at N=1, every sequence
     against the fp64 oracle, including the 16,561-token one whose last Q chunk has an
