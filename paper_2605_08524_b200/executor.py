@@ -242,9 +242,12 @@ class FcpExecutor:
     def forward(self, q, k, v, pre_event=None):
         """O, LSE of this rank's Q rows.  pre_event: the inputs are complete only once this
         event has fired (a reshuffle still in flight, ``forward_user``); the PRE_WAVE tiles,
-        whose rows were in place before, run first, then the stream waits for it."""
+        whose rows were in place before, run first, then the stream waits for it.  A callable
+        pre_event is called right after the PRE_WAVE launch and returns the event."""
         if self.adapt:
             if pre_event is not None:
+                if callable(pre_event):
+                    pre_event = pre_event()
                 torch.cuda.current_stream(self.device).wait_event(pre_event)
             o, lse = self._forward(self._q_in(q), self._pad_d(k), self._pad_d(v))
             return self._q_out(o), self._q_out(lse)
@@ -259,6 +262,8 @@ class FcpExecutor:
             op.forward_wave(self.wave_of_stage[PRE_WAVE], q, k, v, self.k_recv, self.v_recv, outs, cur)
             self._mark("fwd_pre", cur)
         if pre_event is not None:
+            if callable(pre_event):      # a deferred reshuffle: enqueue it behind the PRE_WAVE
+                pre_event = pre_event()
             cur.wait_event(pre_event)
         x = self.xchg
         events = []
@@ -506,15 +511,15 @@ class FcpExecutor:
         in ``kv_input_buffers`` (no publish copy at N > 1).  Returns the FCP-layout (q, k, v)
         and (o, lse).
 
-        overlap=True: the reshuffler copies the rows that stay on this rank, its remote pulls
-        run on copy engines on a side stream, and the PRE_WAVE tiles (rows in place; build the
-        executor with ``resident=rs.resident_chunks()``) compute meanwhile.  overlap=False
-        (default; FCPB_RESHUFFLE_OVERLAP=1 flips it): the whole to-FCP move first (the remote
-        pulls as the K5 pull kernel at NVLink speed), then the forward -- measured faster on
-        C2 at N=2 (2.63-2.73 vs 2.90-2.94 ms), because the exposed move is ~0.3 ms and the
-        split forward's extra launch tail costs more (profiles/r02_notes.md)."""
+        overlap=True (default; FCPB_RESHUFFLE_OVERLAP=0 flips it): the reshuffler copies the
+        rows that stay on this rank (one gather launch), the PRE_WAVE tiles (rows in place;
+        build the executor with ``resident=rs.resident_chunks()``) are enqueued next, and the
+        remote pulls run on copy engines on a side stream beside them.  overlap=False: the
+        whole to-FCP move first (remote pulls as the K5 pull kernel), then the forward.  C2 at
+        N=2 (scripts/forward_user_probe.py): 2.32 vs 2.58 ms.
+        """
         if overlap is None:
-            overlap = os.environ.get("FCPB_RESHUFFLE_OVERLAP", "0") == "1"
+            overlap = os.environ.get("FCPB_RESHUFFLE_OVERLAP", "1") == "1"
         H, D = self.user_cfg.q_heads, self.user_cfg.head_dim
         q = torch.empty((self.layout.tokens, H, D), dtype=q_u.dtype, device=self.device)
         k, v = self.kv_input_buffers()
@@ -524,9 +529,10 @@ class FcpExecutor:
             return (q, k, v), self.forward(q, k, v)
         if self._rs_stream is None:
             self._rs_stream = torch.cuda.Stream(device=self.device)
-        (q, k, v), ev = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens,
-                                 rs.plan.fcp_tokens, outs=[q, k, v], remote_stream=self._rs_stream)
-        o, lse = self.forward(q, k, v, pre_event=ev)
+        (q, k, v), start = rs._move([q_u, k_u, v_u], rs.plan.to_fcp, rs.plan.user_tokens,
+                                    rs.plan.fcp_tokens, outs=[q, k, v], remote_stream=self._rs_stream,
+                                    defer_remote=True)
+        o, lse = self.forward(q, k, v, pre_event=start)
         return (q, k, v), (o, lse)
 
     def attention(self, q, k, v, return_lse: bool = False):

@@ -162,13 +162,18 @@ class Reshuffler:
         dist.barrier(group=group)                       # every rank's flags are zero
         self.bytes_moved = 0
 
-    def _move(self, tensors, pulls, rows_in: int, rows_out: int, outs=None, remote_stream=None):
+    def _move(self, tensors, pulls, rows_in: int, rows_out: int, outs=None, remote_stream=None,
+              defer_remote: bool = False):
         """Move rows of every tensor along `pulls`.  Rows that stay on this rank are copied
         straight from the inputs on the current stream; the others go through the peers'
         regions (publish, flag barrier, copy-engine pulls, flag barrier).  With
         `remote_stream` that remote part runs there, concurrently with whatever the caller
         queues next on the current stream, and the method returns (outs, event): the
-        outputs are complete once the current stream has also waited for the event."""
+        outputs are complete once the current stream has also waited for the event.
+        defer_remote (with remote_stream): return (outs, start) after the local copies;
+        start() enqueues the remote part and returns the event, so the caller can enqueue its
+        own work on the current stream first (the remote part's ~40 host-side copy launches
+        would otherwise hold back the host's next launch: 0.4 ms, scripts/forward_user_probe.py)."""
         widths, elems = [], []
         for t in tensors:
             if t.shape[0] != rows_in:
@@ -206,41 +211,55 @@ class Reshuffler:
         cur = torch.cuda.current_stream(self.device)
         st = remote_stream or cur
         self._mark("local_copies", cur)
-        if remote_stream is not None:
-            remote_stream.wait_stream(cur)
-        with torch.cuda.stream(st):
-            for src, w, off in zip(flat_in, widths, region):                # publish
-                dst = self.buf[off:off + rows_in * w]
-                if src.data_ptr() == dst.data_ptr():    # written in place (input_views)
-                    continue
-                dst.view(rows_in, w).copy_(src.view(torch.uint8), non_blocking=True)
-            self._mark("published", st)
-            self.flags.barrier(0, st)              # every rank's rows published
-            self._mark("barrier0", st)
-            remote = [(dst.data_ptr() + d * w, self.peer[peer].data_ptr() + off + s0 * w, n * w)
-                      for dst, w, off in zip(flat_out, widths, region) for peer, s0, d, n in pulls
-                      if peer != self.rank]
-            self.bytes_moved += sum(x[2] for x in remote)
-            # Standalone, the pulls are SM loads over NVLink (the K5 pull kernel, one launch);
-            # beside compute (remote_stream) they stay on the copy engines, which need no SM.
-            if remote_stream is not None or not self._gather(remote, st):
-                for dst, w, off in zip(flat_out, widths, region):
-                    ob = dst.view(torch.uint8)
-                    for peer, s0, d, n in pulls:
-                        if peer == self.rank:
-                            continue
-                        ob[d:d + n].copy_(self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w),
-                                          non_blocking=True)
-            self._mark("pulls", st)
-            self.flags.barrier(1, st)              # every pull done: buffers reusable
-            self._mark("barrier1", st)
+        # the remote part waits for the inputs and the local copies, not for whatever the
+        # caller enqueues on the current stream before calling a deferred start()
+        local_done = torch.cuda.Event()
+        local_done.record(cur)
+
+        def remote_part():
+            if remote_stream is not None:
+                remote_stream.wait_event(local_done)
+            with torch.cuda.stream(st):
+                for src, w, off in zip(flat_in, widths, region):                # publish
+                    dst = self.buf[off:off + rows_in * w]
+                    if src.data_ptr() == dst.data_ptr():    # written in place (input_views)
+                        continue
+                    dst.view(rows_in, w).copy_(src.view(torch.uint8), non_blocking=True)
+                self._mark("published", st)
+                self.flags.barrier(0, st)              # every rank's rows published
+                self._mark("barrier0", st)
+                remote = [(dst.data_ptr() + d * w, self.peer[peer].data_ptr() + off + s0 * w, n * w)
+                          for dst, w, off in zip(flat_out, widths, region) for peer, s0, d, n in pulls
+                          if peer != self.rank]
+                self.bytes_moved += sum(x[2] for x in remote)
+                # Standalone, the pulls are SM loads over NVLink (the K5 pull kernel, one
+                # launch); beside compute (remote_stream) they stay on the copy engines, which
+                # need no SM.
+                if remote_stream is not None or not self._gather(remote, st):
+                    for dst, w, off in zip(flat_out, widths, region):
+                        ob = dst.view(torch.uint8)
+                        for peer, s0, d, n in pulls:
+                            if peer == self.rank:
+                                continue
+                            ob[d:d + n].copy_(self.peer[peer][off + s0 * w:off + (s0 + n) * w].view(n, w),
+                                              non_blocking=True)
+                self._mark("pulls", st)
+                self.flags.barrier(1, st)              # every pull done: buffers reusable
+                self._mark("barrier1", st)
+            if remote_stream is None:
+                return None
+            ev = torch.cuda.Event()
+            ev.record(remote_stream)
+            for t in list(tensors) + list(outs):
+                t.record_stream(remote_stream)
+            return ev
+
         if remote_stream is None:
+            remote_part()
             return outs
-        ev = torch.cuda.Event()
-        ev.record(remote_stream)
-        for t in list(tensors) + list(outs):
-            t.record_stream(remote_stream)
-        return outs, ev
+        if defer_remote:
+            return outs, remote_part
+        return outs, remote_part()
 
     # Optional per-phase CUDA-event timeline of _move (scripts/reshuffle_probe.py).
     marks = None
