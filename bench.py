@@ -601,6 +601,8 @@ def main():
                 if it:
                     {"to3": to3_t, "seq": seq_t, "ovl": ovl_t}[mode].append(a.elapsed_time(b))
         med = lambda xs: sorted(xs)[len(xs) // 2]
+        if os.environ.get("FCPB_BENCH_DEBUG"):
+            print(json.dumps({"rank": rank, "to3": to3_t, "seq": seq_t, "ovl": ovl_t}), file=sys.stderr, flush=True)
         t = torch.tensor([to_ms, from_ms, med(seq_t), med(ovl_t), med(to3_t)], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         rc = reshuffle_cost(default_contiguous_layout(result.units, n), result.assignment, result.units,

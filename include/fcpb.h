@@ -250,6 +250,14 @@ typedef struct { uint64_t dst; uint64_t src; int64_t bytes; } FcpbGatherSeg;
 FCPB_API int fcpb_gather_copy(const void* segs, int32_t num_segs, int32_t num_ctas, void* stream);
 FCPB_API int64_t fcpb_gather_seg_bytes(void);
 
+/* The same copy with base-relative segments: dst and src of each segment are
+ * (base index << 56) | byte offset into bases[index] (num_bases <= FCPB_GATHER_MAX_BASES, the
+ * bases passed by value).  A segment table that depends only on a move's shape (the
+ * reshuffler's runs) is uploaded once and reused whatever the tensors' addresses are. */
+#define FCPB_GATHER_MAX_BASES 32
+FCPB_API int fcpb_gather_copy_based(const void* segs, int32_t num_segs, const uint64_t* bases,
+                                    int32_t num_bases, int32_t num_ctas, void* stream);
+
 /* Workspace queries: bytes the caller provides for
  *  - the backward preprocess outputs lse2_t + delta_t ([Hq, t_pad] fp32 each, t_pad = T
  *    rounded up to 4);

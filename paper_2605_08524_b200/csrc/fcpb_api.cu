@@ -537,6 +537,22 @@ int fcpb_gather_copy(const void* segs, int32_t num_segs, int32_t num_ctas, void*
 
 int64_t fcpb_gather_seg_bytes(void) { return fcpb::p2p::kSegBytes; }
 
+int fcpb_gather_copy_based(const void* segs, int32_t num_segs, const uint64_t* bases, int32_t num_bases,
+                           int32_t num_ctas, void* stream) {
+  static_assert(fcpb::p2p::kMaxBases == FCPB_GATHER_MAX_BASES, "header and kernel agree");
+  if (num_segs < 0 || num_ctas <= 0 || num_bases < 0 || num_bases > fcpb::p2p::kMaxBases)
+    return fail(FCPB_ERR_INVALID, "gather_copy_based: bad counts");
+  if (num_segs == 0) return FCPB_OK;
+  if (!segs || (num_bases && !bases)) return fail(FCPB_ERR_INVALID, "gather_copy_based: null table");
+  fcpb::p2p::Bases b{};
+  for (int i = 0; i < num_bases; ++i) b.p[i] = bases[i];
+  const int grid = num_ctas < num_segs ? num_ctas : num_segs;
+  fcpb::p2p::gather_based_kernel<<<grid, fcpb::p2p::kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const fcpb::p2p::Seg*>(segs), num_segs, b);
+  FCPB_CUDA(cudaGetLastError());
+  return FCPB_OK;
+}
+
 int fcpb_copy_2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                  size_t height, void* stream) {
   if (width == 0 || height == 0) return FCPB_OK;

@@ -90,7 +90,7 @@ EXPORTS = ("fcpb_attn_fwd", "fcpb_attn_bwd", "fcpb_attn_bwd_dq", "fcpb_attn_bwd_
            "fcpb_last_error", "fcpb_version", "fcpb_device_supported",
            "fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes",
            "fcpb_debug_counters", "fcpb_ipc_alloc", "fcpb_ipc_open", "fcpb_ipc_close", "fcpb_ipc_free",
-           "fcpb_copy_2d", "fcpb_gather_copy", "fcpb_gather_seg_bytes")
+           "fcpb_copy_2d", "fcpb_gather_copy", "fcpb_gather_copy_based", "fcpb_gather_seg_bytes")
 _SIZE_T = ("fcpb_bwd_preprocess_bytes", "fcpb_fwd_partial_bytes", "fcpb_ds_tile_bytes")
 _I64 = ("fcpb_gather_seg_bytes",)
 
@@ -131,6 +131,7 @@ def load(path: str | None = None):
                                  ctypes.c_size_t, c_vp]
     lib.fcpb_debug_counters.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int, ctypes.c_int]
     lib.fcpb_gather_copy.argtypes = [c_vp, c_i32, c_i32, c_vp]
+    lib.fcpb_gather_copy_based.argtypes = [c_vp, c_i32, ctypes.POINTER(ctypes.c_uint64), c_i32, c_i32, c_vp]
     lib.fcpb_gather_seg_bytes.argtypes = []
     for name in EXPORTS:
         getattr(lib, name).restype = (ctypes.c_char_p if name == "fcpb_last_error" else
@@ -170,6 +171,19 @@ def gather_copy(segs, num_ctas: int, stream) -> None:
     if str(segs.dtype) != "torch.int64" or segs.dim() != 2 or segs.shape[1] != 3 or not segs.is_cuda:
         raise ParameterError("gather_copy: segs must be a CUDA int64 tensor [n, 3]")
     check(load().fcpb_gather_copy(segs.data_ptr(), segs.shape[0], num_ctas, stream_handle(stream)))
+
+
+def gather_copy_based(segs, bases, num_ctas: int, stream) -> None:
+    """K5 pull kernel over base-relative segments (``fcpb_gather_copy_based``): segs is a
+    device int64 tensor [n, 3] of ((base << 56) | offset, (base << 56) | offset, bytes), bases a
+    list of at most 32 addresses passed by value."""
+    if str(segs.dtype) != "torch.int64" or segs.dim() != 2 or segs.shape[1] != 3 or not segs.is_cuda:
+        raise ParameterError("gather_copy_based: segs must be a CUDA int64 tensor [n, 3]")
+    if len(bases) > 32:
+        raise ParameterError("gather_copy_based: at most 32 bases")
+    arr = (ctypes.c_uint64 * max(len(bases), 1))(*bases)
+    check(load().fcpb_gather_copy_based(segs.data_ptr(), segs.shape[0], arr, len(bases), num_ctas,
+                                        stream_handle(stream)))
 
 
 def gather_seg_bytes() -> int:

@@ -194,10 +194,12 @@ class Reshuffler:
         # rows that stay here: direct copies, all of them in one gather-kernel launch (one
         # torch copy per (tensor, run) left the GPU waiting on the host's launches: 0.64 ms
         # for C2's 45 local runs at N=2, scripts/reshuffle_probe.py)
-        local = [(dst.data_ptr() + d * w, src.data_ptr() + s0 * w, n * w)
-                 for src, dst, w in zip(flat_in, flat_out, widths) for peer, s0, d, n in pulls
-                 if peer == self.rank]
-        if not self._gather(local, torch.cuda.current_stream(self.device)):
+        m = len(tensors)      # bases: outputs 0..m-1, inputs m..2m-1, peer regions 2m..
+        bases = ([o.data_ptr() for o in flat_out] + [t.data_ptr() for t in flat_in] +
+                 [x.data_ptr() for x in self.peer])
+        local = [(i, d * w, m + i, s0 * w, n * w) for i, w in enumerate(widths)
+                 for peer, s0, d, n in pulls if peer == self.rank]
+        if not self._gather(local, bases, torch.cuda.current_stream(self.device)):
             for src, dst in zip(flat_in, flat_out):
                 for peer, s0, d, n in pulls:
                     if peer == self.rank:
@@ -228,14 +230,14 @@ class Reshuffler:
                 self._mark("published", st)
                 self.flags.barrier(0, st)              # every rank's rows published
                 self._mark("barrier0", st)
-                remote = [(dst.data_ptr() + d * w, self.peer[peer].data_ptr() + off + s0 * w, n * w)
-                          for dst, w, off in zip(flat_out, widths, region) for peer, s0, d, n in pulls
+                remote = [(i, d * w, 2 * m + peer, off + s0 * w, n * w)
+                          for i, (w, off) in enumerate(zip(widths, region)) for peer, s0, d, n in pulls
                           if peer != self.rank]
-                self.bytes_moved += sum(x[2] for x in remote)
+                self.bytes_moved += sum(x[4] for x in remote)
                 # Standalone, the pulls are SM loads over NVLink (the K5 pull kernel, one
                 # launch); beside compute (remote_stream) they stay on the copy engines, which
                 # need no SM.
-                if remote_stream is not None or not self._gather(remote, st):
+                if remote_stream is not None or not self._gather(remote, bases, st):
                     for dst, w, off in zip(flat_out, widths, region):
                         ob = dst.view(torch.uint8)
                         for peer, s0, d, n in pulls:
@@ -264,13 +266,21 @@ class Reshuffler:
     # Optional per-phase CUDA-event timeline of _move (scripts/reshuffle_probe.py).
     marks = None
 
-    def _gather(self, ranges, stream) -> bool:
-        """Copy (dst, src, bytes) ranges with one ``fcpb_gather_copy`` launch on `stream`; False
-        (nothing launched) when a range is not 16-byte aligned.  Device tables are cached per
-        range list (the same pointers recur from step to step)."""
+    def _mark(self, name, stream=None):
+        if self.marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream or torch.cuda.current_stream(self.device))
+            self.marks.append((name, ev))
+
+    def _gather(self, ranges, bases, stream) -> bool:
+        """Copy ranges (dst base, dst offset, src base, src offset, bytes) with one
+        ``fcpb_gather_copy_based`` launch on `stream`; False (nothing launched) when an address
+        or size is not 16-byte aligned.  The segment table depends only on the move's shape, so
+        it is uploaded once per shape and reused whatever the tensors' addresses are (a
+        per-call upload from freshly pinned memory stalled the host for up to 100 ms)."""
         if not ranges:
             return True
-        if any((d | s_ | n) & 15 for d, s_, n in ranges):
+        if len(bases) > 32 or any(b & 15 for b in bases) or any((do | so | n) & 15 for _, do, _, so, n in ranges):
             return False
         key = tuple(ranges)
         cache = self.__dict__.setdefault("_tabs", {})
@@ -279,24 +289,16 @@ class Reshuffler:
             import numpy as np
             step = native.gather_seg_bytes()
             r = np.asarray(ranges, dtype=np.int64)
-            cnt = (r[:, 2] + step - 1) // step                 # pieces of <= step bytes per range
+            cnt = (r[:, 4] + step - 1) // step                 # pieces of <= step bytes per range
             idx = np.repeat(np.arange(len(r)), cnt)
             o = (np.arange(int(cnt.sum())) - np.repeat(np.cumsum(cnt) - cnt, cnt)) * step
-            segs = np.stack([r[idx, 0] + o, r[idx, 1] + o, np.minimum(step, r[idx, 2] - o)], axis=1)
-            host = torch.from_numpy(np.ascontiguousarray(segs)).pin_memory()
-            tab = (host, host.to(self.device, non_blocking=True))
-            if len(cache) >= 64:
-                cache.clear()
+            segs = np.stack([(r[idx, 0] << 56) | (r[idx, 1] + o), (r[idx, 2] << 56) | (r[idx, 3] + o),
+                             np.minimum(step, r[idx, 4] - o)], axis=1)
+            tab = torch.from_numpy(np.ascontiguousarray(segs)).to(self.device)   # once per shape
             cache[key] = tab
-        native.gather_copy(tab[1], 2 * torch.cuda.get_device_properties(self.device).multi_processor_count,
-                           stream)
+        native.gather_copy_based(tab, bases, 2 * torch.cuda.get_device_properties(self.device).multi_processor_count,
+                                 stream)
         return True
-
-    def _mark(self, name, stream=None):
-        if self.marks is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(stream or torch.cuda.current_stream(self.device))
-            self.marks.append((name, ev))
 
     def input_views(self, specs, rows: int | None = None):
         """Tensors of shapes [rows, *shape] / dtypes ``specs`` that live in this rank's

@@ -34,6 +34,26 @@ def main():
     for a, b in zip(views, usr):
         a.copy_(b)
     res = {}
+    # the bench's interleaving first: to-FCP alone, move-then-forward, overlapped (ms each)
+    inter = []
+    for it in range(4):
+        row = {}
+        for mode in ("to3", "seq", "ovl"):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if mode == "to3":
+                rs.to_fcp(*views)
+            elif mode == "seq":
+                ex.forward(*rs.to_fcp(*views))
+            else:
+                ex.forward_user(rs, *views, overlap=True)
+            b.record()
+            torch.cuda.synchronize()
+            row[mode] = round(a.elapsed_time(b), 3)
+        inter.append(row)
+    res["interleaved"] = inter
     for overlap in (True, False):
         for it in range(4):
             dist.barrier()
