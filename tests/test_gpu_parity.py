@@ -75,7 +75,6 @@ def test_full_mask():
 def test_many_q_heads_405b_shape():
     """Llama-3.1-405B-shaped heads (128 q / 8 kv, GQA group 16): more q-heads than one block of
     the backward preprocess covers (64 per gridDim.y slice), 2 simulated ranks."""
-    from paper_2605_08524_b200.costmodel import ModelConfig
     _full_check([900, 300, 129], 2, 512, ModelConfig(q_heads=128, kv_heads=8, head_dim=128),
                 name="128/8 heads N=2")
 
@@ -408,3 +407,31 @@ def test_gather_copy_pull_kernel_is_exact():
     for so, do_, n in ranges:
         want[do_ // 4:(do_ + n) // 4] = src[so // 4:(so + n) // 4]
     assert torch.equal(dst, want)
+
+
+def test_gather_copy_based_is_exact():
+    """fcpb_gather_copy_based: base-relative segments resolve against the bases passed by
+    value (two sources, two destinations), byte-exact, nothing written outside the ranges,
+    and the same table reused with other bases."""
+    from paper_2605_08524_b200 import native
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device="cpu").manual_seed(11)
+    srcs = [torch.randint(-2**31, 2**31 - 1, (1 << 20,), dtype=torch.int32, generator=g).to(dev) for _ in range(2)]
+    step = native.gather_seg_bytes()
+    # (dst base, dst off, src base, src off, bytes); bases 0/1 destinations, 2/3 sources
+    ranges = [(0, 0, 2, 4096, 16), (1, 64, 3, 0, step + 32), (0, 1 << 16, 3, 1 << 18, 2 * step),
+              (1, 1 << 19, 2, 160, 2048 * 3)]
+    segs = []
+    for db, do_, sb, so, n in ranges:
+        for o in range(0, n, step):
+            segs.append(((db << 56) | (do_ + o), (sb << 56) | (so + o), min(step, n - o)))
+    tab = torch.tensor(segs, dtype=torch.int64, device=dev)
+    for _ in range(2):                        # the same table against fresh destinations
+        dsts = [torch.zeros(1 << 20, dtype=torch.int32, device=dev) for _ in range(2)]
+        bases = [d.data_ptr() for d in dsts] + [s.data_ptr() for s in srcs]
+        native.gather_copy_based(tab, bases, 5, torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        want = [torch.zeros_like(d) for d in dsts]
+        for db, do_, sb, so, n in ranges:
+            want[db][do_ // 4:(do_ + n) // 4] = srcs[sb - 2][so // 4:(so + n) // 4]
+        assert all(torch.equal(a, b) for a, b in zip(dsts, want))
