@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long lon
         }
       }
       float mx = m_run;
+      const bool maxonly = (kKind == 5 && h == 1);
       if (kKind != 2) {
         float mp[8];
 #pragma unroll
@@ -88,7 +89,9 @@ __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long lon
       }
       const float neg = -mx * sl2;
       float sum = 0.f;
-      if (kKind == 0 || kKind == 2) {
+      if (maxonly) {
+        sum = mx;                                   // the other head: load + max only
+      } else if (kKind == 0 || kKind == 2 || kKind == 5) {
         fwd::exp_row<false>(s, sl2, neg, t_s, &bar[0]);
         sum = fwd::row_sum(s);
       } else if (kKind == 1) {
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(288, 1) tile_loop(int iters, unsigned long lon
       l += sum;
       m_run = -1.f - 1e-7f * it;
       // restore finite scores over the P columns we wrote (keeps the next tile's S finite)
-      if (kKind == 0 || kKind == 2) {
+      if ((kKind == 0 || kKind == 2 || kKind == 5) && !maxonly) {
         uint32_t v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(0.01f * (threadIdx.x & 31) + 0.03f * i - 0.5f);
@@ -164,6 +167,7 @@ int main() {
       run("full (ld, max, exp_row, st, split)", tile_loop<0>, w, m);
       run("no P stores", tile_loop<1>, w, m);
       run("exp+sum only", tile_loop<4>, w, m);
+      if (w == 8) run("head0 full, head1 ld+max only", tile_loop<5>, w, m);
     }
   return 0;
 }
