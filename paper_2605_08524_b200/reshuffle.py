@@ -161,6 +161,7 @@ class Reshuffler:
         torch.cuda.synchronize(self.device)
         dist.barrier(group=group)                       # every rank's flags are zero
         self.bytes_moved = 0
+        self._tabs = {}            # gather segment tables per move shape (_gather)
 
     def _move(self, tensors, pulls, rows_in: int, rows_out: int, outs=None, remote_stream=None,
               defer_remote: bool = False):
@@ -283,7 +284,7 @@ class Reshuffler:
         if len(bases) > 32 or any(b & 15 for b in bases) or any((do | so | n) & 15 for _, do, _, so, n in ranges):
             return False
         key = tuple(ranges)
-        cache = self.__dict__.setdefault("_tabs", {})
+        cache = self._tabs
         tab = cache.get(key)
         if tab is None:
             import numpy as np
@@ -295,6 +296,8 @@ class Reshuffler:
             segs = np.stack([(r[idx, 0] << 56) | (r[idx, 1] + o), (r[idx, 2] << 56) | (r[idx, 3] + o),
                              np.minimum(step, r[idx, 4] - o)], axis=1)
             tab = torch.from_numpy(np.ascontiguousarray(segs)).to(self.device)   # once per shape
+            if len(cache) >= 64:
+                cache.clear()
             cache[key] = tab
         native.gather_copy_based(tab, bases, 2 * torch.cuda.get_device_properties(self.device).multi_processor_count,
                                  stream)
