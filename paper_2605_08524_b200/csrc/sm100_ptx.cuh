@@ -85,8 +85,7 @@ FCPB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
-  return ok != 0;
-#endif
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
@@ -94,6 +93,7 @@ FCPB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity), "r"(FCPB_TRYWAIT_NS)
       : "memory");
+#endif
   return ok != 0;
 }
 FCPB_DEV uint64_t global_timer_ns() {
